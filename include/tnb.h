@@ -1,0 +1,161 @@
+/*
+ * tnb.h -- C ABI of libtnb.so, the B200 (sm_100a) engine for the tensor-operation
+ * hot path of the reference `tnkit` package (arxiv 2401.01921, Cytnx paper).
+ *
+ * The reference is pure Python; its hot path reaches numpy/OpenBLAS at exactly
+ * these call sites, which are the seams this ABI replaces:
+ *
+ *   tnb_permute            <- np.ascontiguousarray(self.view())
+ *                             pkg/src/tnkit/storage.py:122 (contiguous),
+ *                             storage.py:126 (contiguous_), storage.py:143 (reshape)
+ *   tnb_contract_dense     <- np.tensordot(a.view(), b.view(), axes=(a_pos, b_pos))
+ *                             + np.ascontiguousarray(res)
+ *                             pkg/src/tnkit/contract.py:127-132 (contract_pair, dense)
+ *   tnb_bs_plan / tnb_bs_execute
+ *                          <- _contract_pair_blocks, pkg/src/tnkit/contract.py:137-167
+ *                             (b_by_key pairing :148-151, per-pair tensordot :157-158,
+ *                              ordered += into the output block :162-164)
+ *   tnb_zero_flux_blocks   <- _zero_flux_combos, pkg/src/tnkit/unitensor.py:31-45
+ *   tnb_optimal_order      <- find_optimal_order, pkg/src/tnkit/contract.py:271-343
+ *
+ * Conventions (mirroring the reference's error behaviour, README.md:112-114):
+ *   - every entry point returns int status: 0 = TNB_OK, otherwise an error code;
+ *     tnb_last_error() returns a thread-local message for the last failure.
+ *   - structure is validated by the host layer before these calls (ValueError /
+ *     TypeError are raised in Python before any arithmetic, contract.py:107-123);
+ *     the ABI re-checks what it needs for memory safety and returns
+ *     TNB_EINVAL rather than faulting.
+ *   - the caller allocates every output buffer; the library never frees caller
+ *     memory. Device pointers are plain CUDA device pointers; `stream` is a
+ *     cudaStream_t (NULL = legacy default stream). All device work is
+ *     asynchronous on `stream`.
+ *   - tensors are described in the reference's storage model (storage.py:40-57):
+ *     a C-contiguous buffer with storage shape `shape[0..rank)` and a logical
+ *     permutation `perm` (logical axis k lives on storage axis perm[k]).
+ *   - no CPU fallback: compute entry points return TNB_ENODEV without a GPU.
+ */
+#ifndef TNB_H_
+#define TNB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TNB_MAX_RANK 16
+
+/* status codes */
+#define TNB_OK 0
+#define TNB_EINVAL 1   /* bad argument (shape, perm, dtype, sizes) */
+#define TNB_ECUDA 2    /* CUDA runtime error (launch / async fault) */
+#define TNB_ENODEV 3   /* no CUDA device */
+#define TNB_ENOMEM 4   /* workspace allocation failed */
+#define TNB_EUNSUP 5   /* unsupported dtype / feature (no fallback path) */
+
+/* dtype codes (storage.py:15-20); contraction supports F64 and C128 only */
+#define TNB_F64 0
+#define TNB_C128 1
+#define TNB_I64 2
+#define TNB_BOOL 3
+
+/* complex GEMM formulation */
+#define TNB_CPLX_4M 0  /* four real DMMA products per complex MAC (exact 4M) */
+#define TNB_CPLX_3M 1  /* Gauss/Karatsuba 3M: three real products           */
+
+/* ---- library / device -------------------------------------------------- */
+int tnb_version(void);                       /* ABI version, e.g. 100 */
+int64_t tnb_launch_count(void);              /* kernels launched by libtnb so far (process-wide) */
+const char* tnb_last_error(void);            /* thread-local, never NULL */
+int tnb_device_count(int* count);            /* 0 devices is not an error */
+int tnb_set_device(int device);
+int tnb_synchronize(void* stream);           /* waits; surfaces async faults */
+
+/* ---- a7: permute materialisation (storage.py:114-144) ---------------------
+ * dst[row-major over logical shape] = src viewed with storage shape `shape`
+ * and logical permutation `perm`; bit-exact data movement for element sizes
+ * 1, 2, 4, 8, 16 bytes. src and dst must not overlap. */
+int tnb_permute(const void* src, void* dst, int elem_size, int rank,
+                const int64_t* shape, const int32_t* perm, void* stream);
+
+/* ---- a11: dense pairwise contraction (contract.py:100-134) ----------------
+ * out[a_free..., b_free...] = sum_{shared} A[...] * B[...]
+ *   a_* / b_* : storage shape + perm of each operand (lazy permutes are read
+ *               in place, never materialised)
+ *   nc, a_axes[nc], b_axes[nc]: LOGICAL axes contracted pairwise, in the
+ *               order of the shared labels (a's order, contract.py:112-114)
+ *   dtype_a/b : TNB_F64 or TNB_C128; out dtype = result_type (C128 if any)
+ *   out       : C-contiguous, shape = a_free dims then b_free dims
+ *   cplx_mode : TNB_CPLX_4M or TNB_CPLX_3M (ignored for real)
+ * Returns TNB_EUNSUP for I64/BOOL (the reference accepts them; the engine
+ * has no CPU fallback and says so). */
+int tnb_contract_dense(const void* a, int dtype_a, int rank_a,
+                       const int64_t* shape_a, const int32_t* perm_a,
+                       const void* b, int dtype_b, int rank_b,
+                       const int64_t* shape_b, const int32_t* perm_b,
+                       int nc, const int32_t* a_axes, const int32_t* b_axes,
+                       void* out, int cplx_mode, void* stream);
+
+/* ---- a3: zero-flux block enumeration (unitensor.py:31-45), host only ------
+ * Bonds are given as flattened charge tables:
+ *   nbonds, nsyms; nsec[b]; btype[b] (+1 IN, -1 OUT);
+ *   charges: for bond b, sector s, symmetry y at
+ *            charges[(sec_off[b] + s) * nsyms + y], sec_off = prefix sum of nsec
+ *   sym_n[y]: 0 for U(1), n for Z_n
+ * Writes up to max_out tuples (row-major enumeration, first bond outermost)
+ * into out_qn[count * nbonds] and sets *count to the total number found
+ * (call with max_out = 0 to size). */
+int tnb_zero_flux_blocks(int nbonds, int nsyms, const int32_t* nsec,
+                         const int32_t* btype, const int64_t* charges,
+                         const int32_t* sym_n, int64_t max_out,
+                         int32_t* out_qn, int64_t* count);
+
+/* ---- a12: U(1)/Z_n block-sparse pairwise contraction (contract.py:137-167)
+ * Block metadata is uploaded once per call in one device buffer; pairing is
+ * computed ON DEVICE:
+ *   for i in a-block order, for j ascending with key(b_j) == key(a_i):
+ *       out[out_idx(i,j)] += A_i . B_j
+ * and each output tile is owned by one CTA that accumulates its pairs in that
+ * order (deterministic, no atomics).
+ *
+ * Plan (host -> device):
+ *   na, nb, nout      : block counts
+ *   rank_a, rank_b    : tensor ranks (every block shares them)
+ *   a_qn[na*rank_a], b_qn[nb*rank_b]: qn-index tuples per block (logical order)
+ *   a_shape[na*rank_a], b_shape[nb*rank_b]: block STORAGE shapes
+ *   a_perm[rank_a], b_perm[rank_b]: the common lazy permutation of the blocks
+ *   nc, a_axes, b_axes: contracted logical axes
+ *   out_qn[nout*rank_out]: output block qn tuples (zero-flux enumeration)
+ *   out_shape[nout*rank_out]: output block shapes
+ * Data: a_ptrs[na], b_ptrs[nb], out_ptrs[nout] device pointers (host arrays);
+ *       every output block is fully overwritten (blocks without pairs are zeroed).
+ * Returns the number of pairs in *npairs. If pairs_out != NULL it must hold
+ * 3*max_pairs int32 and receives (i, j, out_idx) triples in reference order
+ * (copied back from the device table) for bit-exact bookkeeping checks. */
+int tnb_bs_contract(int dtype, int na, int nb, int nout,
+                    int rank_a, int rank_b,
+                    const int32_t* a_qn, const int64_t* a_shape, const int32_t* a_perm,
+                    const int32_t* b_qn, const int64_t* b_shape, const int32_t* b_perm,
+                    int nc, const int32_t* a_axes, const int32_t* b_axes,
+                    const int32_t* out_qn, const int64_t* out_shape,
+                    const void* const* a_ptrs, const void* const* b_ptrs,
+                    void* const* out_ptrs,
+                    int64_t max_pairs, int32_t* pairs_out, int64_t* npairs,
+                    void* stream);
+
+/* ---- a14: optimal contraction order DP (contract.py:271-343), host only ---
+ * n tensors (n <= 16). Labels are interned to ints: nlab[t] labels for tensor
+ * t at labels[lab_off[t] ..], dims[label_id] their dimensions (int64).
+ * names_rank[t]: rank of tensor t's name in the lexicographic order of the
+ * rendered strings' alphabet -- the host passes the names themselves:
+ * names = concatenated NUL-terminated strings.
+ * Output: the rendered order string "((A,B),C)" into out[cap]; *cost the
+ * total cost as a decimal string (costs may exceed 64 bits) in cost_out[64].*/
+int tnb_optimal_order(int n, const char* names, const int32_t* nlab,
+                      const int32_t* labels, const int64_t* dims,
+                      char* out, int64_t cap, char* cost_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TNB_H_ */

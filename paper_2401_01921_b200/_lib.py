@@ -1,0 +1,232 @@
+"""ctypes binding of libtnb.so (the C ABI declared in include/tnb.h).
+
+This is the only module that talks to native code. Every compute entry point
+needs a CUDA device and the in-tree ``libtnb.so``; there is no CPU fallback:
+if either is missing the call raises :class:`EngineUnavailable`.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtnb.so")
+
+TNB_OK, TNB_EINVAL, TNB_ECUDA, TNB_ENODEV, TNB_ENOMEM, TNB_EUNSUP = 0, 1, 2, 3, 4, 5
+TNB_F64, TNB_C128, TNB_I64, TNB_BOOL = 0, 1, 2, 3
+CPLX_4M, CPLX_3M = 0, 1
+
+# exported symbols, kept in sync with include/tnb.h (tests check both directions)
+EXPORTS = (
+    "tnb_version", "tnb_launch_count", "tnb_last_error", "tnb_device_count", "tnb_set_device",
+    "tnb_synchronize", "tnb_permute", "tnb_contract_dense",
+    "tnb_zero_flux_blocks", "tnb_bs_contract", "tnb_optimal_order",
+)
+
+
+class EngineError(RuntimeError):
+    """A libtnb call failed (CUDA error, resource limit)."""
+
+
+class EngineUnavailable(EngineError):
+    """No GPU or no libtnb.so: the engine has no CPU fallback."""
+
+
+_lib = None
+_load_error = None
+
+_p = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_pi32 = ctypes.POINTER(ctypes.c_int32)
+_pi64 = ctypes.POINTER(ctypes.c_int64)
+
+
+def _declare(lib):
+    sig = {
+        "tnb_version": ([], ctypes.c_int),
+        "tnb_launch_count": ([], ctypes.c_int64),
+        "tnb_last_error": ([], ctypes.c_char_p),
+        "tnb_device_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+        "tnb_set_device": ([ctypes.c_int], ctypes.c_int),
+        "tnb_synchronize": ([_p], ctypes.c_int),
+        "tnb_permute": ([_p, _p, ctypes.c_int, ctypes.c_int, _pi64, _pi32, _p], ctypes.c_int),
+        "tnb_contract_dense": ([_p, ctypes.c_int, ctypes.c_int, _pi64, _pi32,
+                                _p, ctypes.c_int, ctypes.c_int, _pi64, _pi32,
+                                ctypes.c_int, _pi32, _pi32, _p, ctypes.c_int, _p], ctypes.c_int),
+        "tnb_zero_flux_blocks": ([ctypes.c_int, ctypes.c_int, _pi32, _pi32, _pi64, _pi32,
+                                  _i64, _pi32, _pi64], ctypes.c_int),
+        "tnb_bs_contract": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                             ctypes.c_int, ctypes.c_int,
+                             _pi32, _pi64, _pi32, _pi32, _pi64, _pi32,
+                             ctypes.c_int, _pi32, _pi32, _pi32, _pi64,
+                             _p, _p, _p, _i64, _pi32, _pi64, _p], ctypes.c_int),
+        "tnb_optimal_order": ([ctypes.c_int, ctypes.c_char_p, _pi32, _pi32, _pi64,
+                               ctypes.c_char_p, _i64, ctypes.c_char_p], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+
+
+def lib():
+    """The loaded library (raises EngineUnavailable if it is not built)."""
+    global _lib, _load_error
+    if _lib is not None:
+        return _lib
+    if _load_error is not None:
+        raise EngineUnavailable(_load_error)
+    if not os.path.exists(LIB_PATH):
+        _load_error = (f"{LIB_PATH} is not built; run `python -m paper_2401_01921_b200._build` "
+                       "(the engine has no CPU fallback)")
+        raise EngineUnavailable(_load_error)
+    try:
+        handle = ctypes.CDLL(LIB_PATH)
+        _declare(handle)
+    except OSError as e:
+        _load_error = f"cannot load {LIB_PATH}: {e}"
+        raise EngineUnavailable(_load_error) from e
+    _lib = handle
+    return _lib
+
+
+def launch_count():
+    """Number of kernels libtnb has launched in this process."""
+    return int(lib().tnb_launch_count())
+
+
+def last_error():
+    return lib().tnb_last_error().decode(errors="replace")
+
+
+def check(rc, what):
+    if rc == TNB_OK:
+        return
+    msg = f"{what}: {last_error()}"
+    if rc == TNB_ENODEV:
+        raise EngineUnavailable(msg)
+    if rc == TNB_EINVAL:
+        raise ValueError(msg)
+    if rc == TNB_EUNSUP:
+        raise TypeError(msg)
+    raise EngineError(msg)
+
+
+def device_count():
+    n = ctypes.c_int(0)
+    check(lib().tnb_device_count(ctypes.byref(n)), "device_count")
+    return n.value
+
+
+def _arr64(seq):
+    a = np.ascontiguousarray(np.asarray(seq, dtype=np.int64))
+    return a, a.ctypes.data_as(_pi64)
+
+
+def _arr32(seq):
+    a = np.ascontiguousarray(np.asarray(seq, dtype=np.int32))
+    return a, a.ctypes.data_as(_pi32)
+
+
+def permute(src_ptr, dst_ptr, elem_size, shape, perm, stream):
+    """dst = ascontiguousarray(src.reshape(shape).transpose(perm)) on the GPU."""
+    s, sp = _arr64(shape)
+    p, pp = _arr32(perm)
+    check(lib().tnb_permute(src_ptr, dst_ptr, elem_size, len(shape), sp, pp, stream), "permute")
+
+
+def contract_dense(a_ptr, a_dt, a_shape, a_perm, b_ptr, b_dt, b_shape, b_perm,
+                   a_axes, b_axes, out_ptr, cplx_mode, stream):
+    sa, psa = _arr64(a_shape)
+    pa, ppa = _arr32(a_perm)
+    sb, psb = _arr64(b_shape)
+    pb, ppb = _arr32(b_perm)
+    xa, pxa = _arr32(a_axes)
+    xb, pxb = _arr32(b_axes)
+    check(lib().tnb_contract_dense(a_ptr, a_dt, len(a_shape), psa, ppa,
+                                   b_ptr, b_dt, len(b_shape), psb, ppb,
+                                   len(a_axes), pxa, pxb, out_ptr, cplx_mode, stream),
+          "contract_dense")
+
+
+def zero_flux_blocks(nsec, btype, charges, sym_n):
+    """Row-major zero-flux sector tuples (host C++; unitensor.py:31-45)."""
+    L = lib()
+    ns, pns = _arr32(nsec)
+    bt, pbt = _arr32(btype)
+    ch, pch = _arr64(charges)
+    sn, psn = _arr32(sym_n)
+    total = 1
+    for n in nsec:
+        total *= int(n)
+    cap = total
+    out = np.empty((max(cap, 1), len(nsec)), dtype=np.int32)
+    count = ctypes.c_int64(0)
+    check(L.tnb_zero_flux_blocks(len(nsec), len(sym_n), pns, pbt, pch, psn, cap,
+                                 out.ctypes.data_as(_pi32), ctypes.byref(count)),
+          "zero_flux_blocks")
+    return out[:count.value]
+
+
+def bs_contract(dtype, a_qn, a_shapes, a_perm, b_qn, b_shapes, b_perm, a_axes, b_axes,
+                out_qn, out_shapes, a_ptrs, b_ptrs, out_ptrs, stream, want_pairs=False):
+    na, nb, nout = len(a_ptrs), len(b_ptrs), len(out_ptrs)
+    ra, rb = len(a_perm), len(b_perm)
+    aq, paq = _arr32(np.asarray(a_qn, dtype=np.int32).reshape(-1))
+    ash, pash = _arr64(np.asarray(a_shapes, dtype=np.int64).reshape(-1))
+    ap, pap = _arr32(a_perm)
+    bq, pbq = _arr32(np.asarray(b_qn, dtype=np.int32).reshape(-1))
+    bsh, pbsh = _arr64(np.asarray(b_shapes, dtype=np.int64).reshape(-1))
+    bp, pbp = _arr32(b_perm)
+    xa, pxa = _arr32(a_axes)
+    xb, pxb = _arr32(b_axes)
+    oq, poq = _arr32(np.asarray(out_qn, dtype=np.int32).reshape(-1))
+    osh, posh = _arr64(np.asarray(out_shapes, dtype=np.int64).reshape(-1))
+    aptr = (ctypes.c_void_p * max(na, 1))(*a_ptrs)
+    bptr = (ctypes.c_void_p * max(nb, 1))(*b_ptrs)
+    optr = (ctypes.c_void_p * max(nout, 1))(*out_ptrs)
+    npairs = ctypes.c_int64(0)
+    pairs = None
+    cap = 0
+    if want_pairs:
+        cap = max(na * nb, 1)
+        pairs = np.zeros((cap, 3), dtype=np.int32)
+    check(lib().tnb_bs_contract(dtype, na, nb, nout, ra, rb, paq, pash, pap, pbq, pbsh, pbp,
+                                len(a_axes), pxa, pxb, poq, posh,
+                                ctypes.cast(aptr, _p), ctypes.cast(bptr, _p), ctypes.cast(optr, _p),
+                                cap, pairs.ctypes.data_as(_pi32) if want_pairs else None,
+                                ctypes.byref(npairs) if want_pairs else None, stream),
+          "bs_contract")
+    if want_pairs:
+        return pairs[:npairs.value].copy()
+    return None
+
+
+def optimal_order(names, label_lists, dims):
+    """Native DP (contract.py:271-343); returns (rendered order, cost) or None on overflow."""
+    ids = {}
+    flat, nlab = [], []
+    for labels in label_lists:
+        nlab.append(len(labels))
+        for l in labels:
+            if l not in ids:
+                ids[l] = len(ids)
+            flat.append(ids[l])
+    dimv = [0] * len(ids)
+    for l, i in ids.items():
+        dimv[i] = int(dims[l])
+    if any(d >= 2 ** 63 for d in dimv):
+        return None
+    blob = b"".join(n.encode() + b"\0" for n in names)
+    nl, pnl = _arr32(nlab)
+    fl, pfl = _arr32(flat if flat else [0])
+    dv, pdv = _arr64(dimv if dimv else [1])
+    cap = 64 + 4 * sum(len(n) + 3 for n in names)
+    out = ctypes.create_string_buffer(cap)
+    cost = ctypes.create_string_buffer(64)
+    rc = lib().tnb_optimal_order(len(names), blob, pnl, pfl, pdv, out, cap, cost)
+    if rc == TNB_EUNSUP:
+        return None
+    check(rc, "optimal_order")
+    return out.value.decode(), int(cost.value.decode())

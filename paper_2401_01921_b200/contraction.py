@@ -1,0 +1,410 @@
+"""Label-driven contraction: the hot path's host layer.
+
+Public functions and their reference counterparts (pkg/src/tnkit/contract.py):
+
+* ``contract_pair``       -> contract_pair :100-134 (dense) / _contract_pair_blocks :137-167
+* ``contract``            -> contract :172-219, ``execute_tree`` :222-226
+* ``find_optimal_order``  -> find_optimal_order :271-343 (native DP, same tie-break)
+* ``contraction_cost``, ``brute_force_order``, ``parse_order``, ``render_order``,
+  ``tree_leaves``          -> :19-79, :253-268, :351-372
+
+Validation (labels, directions, sectors, duplicate free labels) happens here,
+before any device work, with the reference's exception types. The arithmetic
+is libtnb: ``tnb_contract_dense`` (DMMA GEMM reading lazily permuted operands in
+place) and ``tnb_bs_contract`` (device pairing + grouped GEMM). There is no CPU
+fallback: int64/bool contractions raise TypeError.
+"""
+import itertools
+import os
+import re
+
+import numpy as np
+import torch
+
+from . import _lib, dense
+from .charges import REGULAR
+from .dense import Complex128, DenseTensor, Float64
+from .labeled import UniTensor
+
+_NAME_RE = re.compile(r"[A-Za-z0-9_*'+\-]+")
+
+_CPLX_MODE = _lib.CPLX_3M if os.environ.get("TNB_CPLX", "4M").upper() == "3M" else _lib.CPLX_4M
+
+
+def set_complex_mode(mode):
+    """'4M' (four real DMMA products per complex MAC) or '3M' (Gauss, 3 products)."""
+    global _CPLX_MODE
+    mode = str(mode).upper()
+    if mode not in ("4M", "3M"):
+        raise ValueError("complex mode must be '4M' or '3M'")
+    _CPLX_MODE = _lib.CPLX_3M if mode == "3M" else _lib.CPLX_4M
+
+
+def get_complex_mode():
+    return "3M" if _CPLX_MODE == _lib.CPLX_3M else "4M"
+
+
+# -- order trees: leaf = name (str), node = (left, right) ------------------------------
+def render_order(tree):
+    return tree if isinstance(tree, str) else "(" + render_order(tree[0]) + "," + render_order(tree[1]) + ")"
+
+
+def parse_order(text):
+    """Grammar ``name | "(" order "," order ")"`` (whitespace allowed between tokens)."""
+    n = len(text)
+
+    def bad(pos, msg):
+        raise ValueError(f"malformed order string {text!r} at {pos}: {msg}")
+
+    def ws(pos):
+        while pos < n and text[pos].isspace():
+            pos += 1
+        return pos
+
+    def node(pos):
+        pos = ws(pos)
+        if pos >= n:
+            bad(pos, "unexpected end")
+        if text[pos] == "(":
+            left, pos = node(pos + 1)
+            pos = ws(pos)
+            if pos >= n or text[pos] != ",":
+                bad(pos, "expected ','")
+            right, pos = node(pos + 1)
+            pos = ws(pos)
+            if pos >= n or text[pos] != ")":
+                bad(pos, "expected ')'")
+            return (left, right), pos + 1
+        m = _NAME_RE.match(text, pos)
+        if not m:
+            bad(pos, "expected a tensor name")
+        return m.group(), m.end()
+
+    tree, pos = node(0)
+    pos = ws(pos)
+    if pos != n:
+        bad(pos, "trailing characters")
+    return tree
+
+
+def tree_leaves(tree):
+    if isinstance(tree, str):
+        return [tree]
+    return tree_leaves(tree[0]) + tree_leaves(tree[1])
+
+
+# -- pairwise ---------------------------------------------------------------------------------
+def _check_pair_bond(label, ba, bb):
+    if ba.dim != bb.dim:
+        raise ValueError(f"label {label!r}: dimension mismatch ({ba.dim} vs {bb.dim})")
+    if (ba.btype == REGULAR) != (bb.btype == REGULAR):
+        raise ValueError(f"label {label!r}: cannot contract a REGULAR bond with a directed bond")
+    if ba.btype != REGULAR and ba.btype == bb.btype:
+        raise ValueError(f"label {label!r}: only bonds with opposite directions can be contracted "
+                         f"(both {ba.btype})")
+    if (ba.has_qnums or bb.has_qnums) and (ba.syms != bb.syms or ba.sectors != bb.sectors):
+        raise ValueError(f"label {label!r}: quantum-number sectors do not match")
+
+
+def _pair_layout(a, b):
+    """Shared labels (a's order), contracted/free positions, output labels/bonds."""
+    al, bl = a._labels, b._labels
+    bset = set(bl)
+    shared = [l for l in al if l in bset]
+    a_pos = [al.index(l) for l in shared]
+    b_pos = [bl.index(l) for l in shared]
+    for l, pa, pb in zip(shared, a_pos, b_pos):
+        _check_pair_bond(l, a._bonds[pa], b._bonds[pb])
+    sset = set(shared)
+    a_free = [i for i, l in enumerate(al) if l not in sset]
+    b_free = [i for i, l in enumerate(bl) if l not in sset]
+    out_labels = [al[i] for i in a_free] + [bl[i] for i in b_free]
+    if len(set(out_labels)) != len(out_labels):
+        raise ValueError(f"duplicate free labels in contraction result: {out_labels}")
+    out_bonds = [a._bonds[i] for i in a_free] + [b._bonds[i] for i in b_free]
+    return a_pos, b_pos, a_free, b_free, out_labels, out_bonds
+
+
+def _result_dtype(da, db):
+    dt = np.result_type(da, db)
+    if dt not in (Float64, Complex128):
+        raise TypeError(f"contraction of {da} x {db} is not supported on the GPU engine "
+                        "(float64 / complex128 only; there is no CPU fallback)")
+    return dt
+
+
+def contract_pair(a, b):
+    """Contract two UniTensors over all shared labels; output = a_free then b_free labels."""
+    if not isinstance(a, UniTensor) or not isinstance(b, UniTensor):
+        raise TypeError("contract expects UniTensors")
+    if a.is_sym != b.is_sym:
+        raise ValueError("cannot contract a block-sparse tensor with a dense one; use convert_from first")
+    a_pos, b_pos, a_free, b_free, out_labels, out_bonds = _pair_layout(a, b)
+    if not a.is_sym:
+        return _contract_dense(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds)
+    return _contract_blocks(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds)
+
+
+def _contract_dense(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds):
+    A, B = a._blocks[0], b._blocks[0]
+    dt = _result_dtype(A.dtype, B.dtype)
+    out_shape = [A.shape[i] for i in a_free] + [B.shape[j] for j in b_free]
+    out = DenseTensor.empty(out_shape, dt)
+    _lib.contract_dense(A.data_ptr, dense.dtype_code(A.dtype), A.storage_shape, A.perm,
+                        B.data_ptr, dense.dtype_code(B.dtype), B.storage_shape, B.perm,
+                        a_pos, b_pos, out.data_ptr, _CPLX_MODE, dense.stream_handle())
+    if not out_shape:
+        return UniTensor.scalar(out)
+    return UniTensor._assemble(out_bonds, out_labels, len(a_free), "", [out], None)
+
+
+def _common_perm(t):
+    perms = {blk.perm for blk in t._blocks}
+    if len(perms) == 1:
+        return t._blocks, next(iter(perms))
+    # blocks were permuted individually (put_block_/contiguous_ on one block): materialise
+    return [blk.contiguous() for blk in t._blocks], tuple(range(t.rank))
+
+
+def _widen(blocks, dt):
+    return [b if b.dtype == dt else b.astype(dt) for b in blocks]
+
+
+def _contract_blocks(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds):
+    dt = _result_dtype(a.dtype, b.dtype)
+    ablk, aperm = _common_perm(a)
+    bblk, bperm = _common_perm(b)
+    ablk, bblk = _widen(ablk, dt), _widen(bblk, dt)
+    if not out_bonds:
+        return _contract_blocks_scalar(a, b, ablk, bblk, a_pos, b_pos, dt)
+    from .labeled import _slab_blocks, zero_flux_combos
+    if not all(x.syms == out_bonds[0].syms for x in out_bonds):
+        raise ValueError("all bonds must carry the same symmetries")
+    qns = zero_flux_combos(out_bonds)
+    if not qns:
+        raise ValueError("no valid blocks: no combination of these bonds' sectors has zero flux")
+    shapes = [tuple(x.sectors[k][1] for x, k in zip(out_bonds, qn)) for qn in qns]
+    oblk, _ = _slab_blocks(shapes, dt, zero=False)  # every output block is fully written by the kernel
+    _lib.bs_contract(dense.dtype_code(dt), a._qns, [x.storage_shape for x in ablk], aperm,
+                     b._qns, [x.storage_shape for x in bblk], bperm, a_pos, b_pos,
+                     qns, shapes, [x.data_ptr for x in ablk], [x.data_ptr for x in bblk],
+                     [x.data_ptr for x in oblk], dense.stream_handle())
+    return UniTensor._assemble(out_bonds, out_labels, len(a_free), "", oblk, qns)
+
+
+def block_pairs(a, b):
+    """Device pairing table of a block-sparse contraction as (i, j, out_idx) rows in
+    reference accumulation order (contract.py:148-164); runs the contraction."""
+    a_pos, b_pos, a_free, b_free, out_labels, out_bonds = _pair_layout(a, b)
+    dt = _result_dtype(a.dtype, b.dtype)
+    ablk, aperm = _common_perm(a)
+    bblk, bperm = _common_perm(b)
+    ablk, bblk = _widen(ablk, dt), _widen(bblk, dt)
+    from .labeled import _slab_blocks, zero_flux_combos
+    qns = zero_flux_combos(out_bonds)
+    shapes = [tuple(x.sectors[k][1] for x, k in zip(out_bonds, qn)) for qn in qns]
+    oblk, _ = _slab_blocks(shapes, dt, zero=False)
+    return _lib.bs_contract(dense.dtype_code(dt), a._qns, [x.storage_shape for x in ablk], aperm,
+                            b._qns, [x.storage_shape for x in bblk], bperm, a_pos, b_pos,
+                            qns, shapes, [x.data_ptr for x in ablk], [x.data_ptr for x in bblk],
+                            [x.data_ptr for x in oblk], dense.stream_handle(), want_pairs=True)
+
+
+def _contract_blocks_scalar(a, b, ablk, bblk, a_pos, b_pos, dt):
+    """Fully contracted block-sparse pair: sum over matching block pairs in reference
+    order, each pair a device dot product (rare path; contract.py:159-166)."""
+    by_key = {}
+    for j, q in enumerate(b._qns):
+        by_key.setdefault(tuple(q[p] for p in b_pos), []).append(j)
+    parts = []
+    for i, q in enumerate(a._qns):
+        for j in by_key.get(tuple(q[p] for p in a_pos), ()):
+            A, B = ablk[i], bblk[j]
+            out = DenseTensor.empty((), dt)
+            _lib.contract_dense(A.data_ptr, dense.dtype_code(A.dtype), A.storage_shape, A.perm,
+                                B.data_ptr, dense.dtype_code(B.dtype), B.storage_shape, B.perm,
+                                a_pos, b_pos, out.data_ptr, _CPLX_MODE, dense.stream_handle())
+            parts.append(out.storage())
+    total = DenseTensor.empty((), dt)
+    total.storage().zero_()
+    for p in parts:  # fixed order, deterministic
+        total.storage().add_(p)
+    return UniTensor.scalar(total)
+
+
+# -- multi-tensor ------------------------------------------------------------------------------------
+def contract(first, *rest, order=None, optimal=True):
+    """contract(a, b) or contract([t1, t2, ...], order=None, optimal=True)."""
+    if isinstance(first, UniTensor):
+        tensors = [first, *rest]
+    else:
+        tensors = list(first)
+        if rest:
+            raise TypeError("pass either several tensors or one list")
+    if not tensors:
+        raise ValueError("nothing to contract")
+    if not all(isinstance(t, UniTensor) for t in tensors):
+        raise TypeError("contract expects UniTensors")
+    if len(tensors) == 1:
+        return tensors[0].clone()
+    _reject_hyperedges(tensors)
+    if len(tensors) == 2:
+        return contract_pair(tensors[0], tensors[1])
+    if order is None and not optimal:
+        acc = tensors[0]
+        for t in tensors[1:]:
+            acc = contract_pair(acc, t)
+        return acc
+    names = [t.name for t in tensors]
+    if any(not n for n in names):
+        raise ValueError("multi-tensor contraction with an order or the optimal search needs every tensor named")
+    if len(set(names)) != len(names):
+        raise ValueError(f"tensor names must be distinct, got {names}")
+    by_name = dict(zip(names, tensors))
+    if order is not None:
+        tree = parse_order(order) if isinstance(order, str) else order
+        if sorted(tree_leaves(tree)) != sorted(names):
+            raise ValueError(f"order {render_order(tree)!r} does not cover exactly the tensors {names}")
+    else:
+        tree = find_optimal_order({n: t.labels for n, t in by_name.items()}, _label_dims(tensors))
+    return execute_tree(tree, by_name)
+
+
+def execute_tree(tree, by_name):
+    if isinstance(tree, str):
+        return by_name[tree]
+    return contract_pair(execute_tree(tree[0], by_name), execute_tree(tree[1], by_name))
+
+
+def _reject_hyperedges(tensors):
+    counts = {}
+    for t in tensors:
+        for l in t.labels:
+            counts[l] = counts.get(l, 0) + 1
+    bad = [l for l, c in counts.items() if c > 2]
+    if bad:
+        raise ValueError(f"labels {bad} appear on more than two tensors; hyper-edge contraction is not supported")
+
+
+def _label_dims(tensors):
+    dims = {}
+    for t in tensors:
+        for l, b in zip(t.labels, t.bonds):
+            if l in dims and dims[l] != b.dim:
+                raise ValueError(f"label {l!r} has inconsistent dimensions ({dims[l]} vs {b.dim})")
+            dims[l] = b.dim
+    return dims
+
+
+# -- order search ---------------------------------------------------------------------------------------
+def contraction_cost(tree, label_sets, dims):
+    """Total multiplication count of executing ``tree`` (step = prod of union of free labels)."""
+
+    def walk(node):
+        if isinstance(node, str):
+            return 0, list(dict.fromkeys(label_sets[node]))
+        c1, f1 = walk(node[0])
+        c2, f2 = walk(node[1])
+        s1, s2 = set(f1), set(f2)
+        union = f1 + [l for l in f2 if l not in s1]
+        step = 1
+        for l in union:
+            step *= dims[l]
+        return c1 + c2 + step, [l for l in union if (l in s1) != (l in s2)]
+
+    return walk(tree)[0]
+
+
+def find_optimal_order(label_sets, dims):
+    """Minimal-cost binary tree by subset DP; ties -> smallest rendered string, smaller child left.
+
+    Runs natively (tnb_optimal_order) and falls back to the identical Python DP
+    only when a cost exceeds 128 bits or the library is not built.
+    """
+    names = list(label_sets)
+    if not names:
+        raise ValueError("empty tensor network")
+    if len(names) == 1:
+        return names[0]
+    if len(names) > 16:
+        raise ValueError(f"order search over {len(names)} tensors is not supported (limit 16)")
+    try:
+        res = _lib.optimal_order(names, [list(label_sets[n]) for n in names], dims)
+    except _lib.EngineUnavailable:
+        res = None
+    if res is not None:
+        return parse_order(res[0])
+    return _find_optimal_order_py(names, label_sets, dims)
+
+
+def _find_optimal_order_py(names, label_sets, dims):
+    n = len(names)
+    full = (1 << n) - 1
+    lists = [list(label_sets[nm]) for nm in names]
+    free = [frozenset()] * (full + 1)
+    for mask in range(1, full + 1):
+        cnt = {}
+        for i in range(n):
+            if mask >> i & 1:
+                for l in lists[i]:
+                    cnt[l] = cnt.get(l, 0) + 1
+        free[mask] = frozenset(l for l, c in cnt.items() if c == 1)
+
+    def pcost(m1, m2):
+        c = 1
+        for l in free[m1] | free[m2]:
+            c *= dims[l]
+        return c
+
+    cap = max(1, min(pcost(1 << i, 1 << j) for i in range(n) for j in range(i + 1, n)))
+    masks = [m for pc in range(2, n + 1) for m in range(1, full + 1) if bin(m).count("1") == pc]
+    while True:
+        best = {1 << i: (0, names[i], names[i]) for i in range(n)}
+        for mask in masks:
+            sub = (mask - 1) & mask
+            while sub:
+                rest = mask ^ sub
+                s1, s2 = (sub, rest) if sub < rest else (rest, sub)
+                sub = (sub - 1) & mask
+                if s1 not in best or s2 not in best:
+                    continue
+                c1, t1, r1 = best[s1]
+                c2, t2, r2 = best[s2]
+                cost = c1 + c2 + pcost(s1, s2)
+                if cost > cap:
+                    continue
+                tree, rendered = (((t1, t2), f"({r1},{r2})") if r1 <= r2 else ((t2, t1), f"({r2},{r1})"))
+                cur = best.get(mask)
+                if cur is None or (cost, rendered) < (cur[0], cur[2]):
+                    best[mask] = (cost, tree, rendered)
+        if full in best:
+            return best[full][1]
+        cap *= 2
+
+
+def brute_force_order(label_sets, dims):
+    """Exhaustive minimum over all binary trees (test helper; small n only)."""
+    names = list(label_sets)
+
+    def trees(items):
+        if len(items) == 1:
+            yield items[0]
+            return
+        head = items[0]
+        for k in range(1, len(items)):
+            for left in itertools.combinations(items, k):
+                if head not in left:
+                    continue
+                right = [x for x in items if x not in left]
+                if not right:
+                    continue
+                for lt in trees(list(left)):
+                    for rt in trees(right):
+                        yield (lt, rt)
+
+    best = None
+    for t in trees(names):
+        c = contraction_cost(t, label_sets, dims)
+        if best is None or c < best[0]:
+            best = (c, t)
+    return best[1]

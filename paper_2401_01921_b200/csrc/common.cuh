@@ -1,0 +1,55 @@
+// Shared helpers for libtnb (sm_100a): status/error plumbing, fast integer
+// division, and small host utilities.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/tnb.h"
+
+namespace tnb {
+
+// Thread-local last-error message (tnb_last_error).
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define TNB_CUDA_CHECK(expr)                                   \
+  do {                                                         \
+    cudaError_t _e = (expr);                                   \
+    if (_e != cudaSuccess) return ::tnb::cuda_fail(_e, #expr); \
+  } while (0)
+
+// Returns TNB_OK iff at least one CUDA device is visible (cached).
+int require_device();
+int sm_count();
+
+// Counts every kernel this library launches (tnb_launch_count); bench.py reports it.
+void count_launch(int n = 1);
+
+// Unsigned 32-bit division by a runtime-invariant divisor via multiply-high
+// (Granlund-Montgomery). Valid for 0 <= n < 2^31 and 1 <= d < 2^31.
+struct FastDiv {
+  uint32_t d, m, s;
+  FastDiv() : d(1), m(0), s(0) {}
+  explicit FastDiv(uint32_t div) {
+    d = div;
+    if (d == 1) { m = 0; s = 0; return; }
+    s = 0;
+    while ((1ull << s) < d) ++s;  // s = ceil(log2 d)
+    uint64_t mm = ((1ull << 32) * ((1ull << s) - d)) / d + 1;
+    m = (uint32_t)mm;
+  }
+  __host__ __device__ __forceinline__ uint32_t div(uint32_t n) const {
+#ifdef __CUDA_ARCH__
+    if (d == 1) return n;
+    uint32_t t = __umulhi(n, m);
+    return (t + n) >> s;
+#else
+    return n / d;
+#endif
+  }
+};
+
+}  // namespace tnb

@@ -1,0 +1,540 @@
+// a11: dense pairwise contraction on FP64 tensor cores (DMMA) -- the B200
+// replacement for np.tensordot(a.view(), b.view(), axes=(a_pos, b_pos)) +
+// np.ascontiguousarray (pkg/src/tnkit/contract.py:127-132).
+//
+// The contraction is a GEMM C[M,N] = A[M,K] . B[K,N] whose operands are read
+// IN PLACE from the reference's storage model (buffer + lazy permutation): the
+// permute is fused into the operand loads. Each operand index group (A rows,
+// A contracted, B contracted, B cols) is a short list of (dim, stride) digits;
+// a row/col offset table is built once per CTA tile and a K offset table once
+// per k-tile (per stage), so every element address is
+//     base + row_off[m] + k_off[k]
+// and the cp.async gathers go straight into shared memory.
+//
+// Math: mma.sync.m8n8k4 f64 (SASS DMMA.8x8x4), the FP64 tensor-core path on
+// sm_100a (tcgen05 has no f64 kind). Complex128 is either 4M (four real DMMAs
+// per fragment pair, exact products) or 3M (Gauss: three real DMMAs; (Ar+Ai),
+// (Br+Bi) formed from the staged fragments in registers).
+//
+// Tile shape and split-K are chosen per problem on the host to fill the 148 SMs;
+// split-K partials are reduced by a second deterministic kernel (fixed order,
+// no atomics). Very skinny problems (N, K <= 64: e.g. the MPO step of
+// L.A.W.R) go to a separate memory-bound kernel.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "gemm_core.cuh"
+
+namespace tnb {
+
+int permute_device(const void* src, void* dst, int es, int rank, const int64_t* shape, const int32_t* perm,
+                   cudaStream_t st);
+
+namespace {
+
+struct GemmDesc {
+  int M, N, K;
+  int tiles_m, tiles_n, splitk;
+  int k_per_split;  // multiple of BK
+  int a_mfast, b_nfast;
+  int out_ld;       // = N
+  KAffine kaff;
+  Group rowA, kA, kB, colB;
+};
+
+// Warp-specialised dense tile GEMM (producer warpgroup + DMMA warps).
+template <bool CPLX, int MODE, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
+__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32 + 128, 1)
+    gemm_ws_kernel(const typename Elem<CPLX>::T* __restrict__ A, const typename Elem<CPLX>::T* __restrict__ B,
+                   typename Elem<CPLX>::T* __restrict__ C, const GemmDesc d) {
+  using Core = TileCoreWS<CPLX, MODE, BM, BN, BK, WARPS_M, WARPS_N, STAGES, 0, 0>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  int bid = blockIdx.x;
+  const int split = bid % d.splitk;
+  bid /= d.splitk;
+  int tm, tn;
+  {
+    const int group = 8;
+    const int per_group = group * d.tiles_n;
+    const int g = bid / per_group;
+    const int first_m = g * group;
+    const int gsz = min(d.tiles_m - first_m, group);
+    const int in_g = bid - g * per_group;
+    tm = first_m + in_g % gsz;
+    tn = in_g / gsz;
+  }
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int kbeg = split * d.k_per_split;
+  const int kend = min(d.K, kbeg + d.k_per_split);
+  typename Core::Acc acc;
+  Core::zero(acc);
+  if (Core::run(smem, A, B, d.rowA, d.kA, d.kB, d.colB, m0, n0, d.M, d.N, kbeg, kend, d.a_mfast != 0,
+                d.b_nfast != 0, d.kaff, acc))
+    Core::store(C + (size_t)split * (size_t)d.M * (size_t)d.out_ld, d.out_ld, m0, n0, d.M, d.N, acc);
+}
+
+// Dense tile GEMM: one CTA per (tile, K split); tile raster in groups of 8
+// tile-rows so concurrently running CTAs share B panels in L2.
+template <bool CPLX, int MODE, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB>
+__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
+    gemm_kernel(const typename Elem<CPLX>::T* __restrict__ A, const typename Elem<CPLX>::T* __restrict__ B,
+                typename Elem<CPLX>::T* __restrict__ C, const GemmDesc d) {
+  using Core = TileCore<CPLX, MODE, BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  int bid = blockIdx.x;
+  const int split = bid % d.splitk;
+  bid /= d.splitk;
+  int tm, tn;
+  {
+    const int group = 8;
+    const int per_group = group * d.tiles_n;
+    const int g = bid / per_group;
+    const int first_m = g * group;
+    const int gsz = min(d.tiles_m - first_m, group);
+    const int in_g = bid - g * per_group;
+    tm = first_m + in_g % gsz;
+    tn = in_g / gsz;
+  }
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int kbeg = split * d.k_per_split;
+  const int kend = min(d.K, kbeg + d.k_per_split);
+  typename Core::Acc acc;
+  Core::zero(acc);
+  Core::mainloop(smem, A, B, d.rowA, d.kA, d.kB, d.colB, m0, n0, d.M, d.N, kbeg, kend, d.a_mfast != 0,
+                 d.b_nfast != 0, acc);
+  Core::store(C + (size_t)split * (size_t)d.M * (size_t)d.out_ld, d.out_ld, m0, n0, d.M, d.N, acc);
+}
+
+// split-K reduction: out[i] = sum_{s in order} ws[s][i]
+template <bool CPLX>
+__global__ void splitk_reduce_kernel(const typename Elem<CPLX>::T* __restrict__ ws,
+                                     typename Elem<CPLX>::T* __restrict__ out, int64_t n, int S) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    if constexpr (!CPLX) {
+      double s = ws[i];
+      for (int q = 1; q < S; ++q) s += ws[(size_t)q * n + i];
+      out[i] = s;
+    } else {
+      double2 s = ws[i];
+      for (int q = 1; q < S; ++q) {
+        double2 v = ws[(size_t)q * n + i];
+        s.x += v.x;
+        s.y += v.y;
+      }
+      out[i] = s;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ skinny kernel
+// C[M, N] with N <= 64 and K <= 64: memory-bound. Each CTA stages a 128-row
+// panel of A (gathered through the offset groups) and all of B in shared
+// memory, computes its 128 x N outputs with FMAs, and writes the panel --
+// which is one contiguous run of C -- coalesced.
+template <bool CPLX>
+__global__ void __launch_bounds__(256) skinny_kernel(const typename Elem<CPLX>::T* __restrict__ A,
+                                                     const typename Elem<CPLX>::T* __restrict__ B,
+                                                     typename Elem<CPLX>::T* __restrict__ C, const GemmDesc d) {
+  using T = typename Elem<CPLX>::T;
+  constexpr int RM = 128;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int K = d.K, N = d.N;
+  T* Bs = reinterpret_cast<T*>(smem);          // [K][N]
+  T* As = Bs + K * N;                          // [RM][K+1]
+  T* Cs = As + RM * (K + 1);                   // [RM * N]
+  int64_t* kA = reinterpret_cast<int64_t*>(Cs + RM * N);  // [K]
+  int64_t* rA = kA + K;                                   // [RM]
+  const int tid = threadIdx.x;
+  for (int i = tid; i < K; i += blockDim.x) kA[i] = group_offset(d.kA, i);
+  for (int i = tid; i < K * N; i += blockDim.x) {
+    int k = i / N, n = i - k * N;
+    Bs[i] = B[group_offset(d.kB, k) + group_offset(d.colB, n)];
+  }
+  for (int m0 = blockIdx.x * RM; m0 < d.M; m0 += gridDim.x * RM) {
+    const int rows = min(RM, d.M - m0);
+    __syncthreads();
+    for (int i = tid; i < rows; i += blockDim.x) rA[i] = group_offset(d.rowA, m0 + i);
+    __syncthreads();
+    for (int i = tid; i < rows * K; i += blockDim.x) {
+      int r = i / K, k = i - r * K;
+      As[r * (K + 1) + k] = __ldg(A + rA[r] + kA[k]);
+    }
+    __syncthreads();
+    for (int i = tid; i < rows * N; i += blockDim.x) {
+      int r = i / N, n = i - r * N;
+      const T* a = As + r * (K + 1);
+      if constexpr (!CPLX) {
+        double s = 0.0;
+        for (int k = 0; k < K; ++k) s = fma(a[k], Bs[k * N + n], s);
+        Cs[i] = s;
+      } else {
+        double sr = 0.0, si = 0.0;
+        for (int k = 0; k < K; ++k) {
+          double2 x = a[k], y = Bs[k * N + n];
+          sr = fma(x.x, y.x, sr);
+          sr = fma(-x.y, y.y, sr);
+          si = fma(x.x, y.y, si);
+          si = fma(x.y, y.x, si);
+        }
+        Cs[i] = make_double2(sr, si);
+      }
+    }
+    __syncthreads();
+    T* out = C + (size_t)m0 * N;
+    for (int i = tid; i < rows * N; i += blockDim.x) out[i] = Cs[i];
+  }
+}
+
+// ------------------------------------------------------------------ host side
+struct Digit {
+  int64_t dim, stride;
+};
+
+bool build_group(const std::vector<Digit>& digs, Group& g, int64_t& total) {
+  memset(&g, 0, sizeof(g));
+  total = 1;
+  for (auto& x : digs) total *= x.dim;
+  if ((int)digs.size() > kMaxDig) return false;
+  g.n = (int)digs.size();
+  for (int q = 0; q < g.n; ++q) {
+    if (digs[q].dim >= (1ll << 31)) return false;
+    g.dim[q] = (int32_t)digs[q].dim;
+    g.div[q] = FastDiv((uint32_t)digs[q].dim);
+    g.stride[q] = digs[q].stride;
+  }
+  return true;
+}
+
+// merge adjacent digits (outer q, inner q+1) when stride_q == dim_{q+1} * stride_{q+1}
+std::vector<Digit> merge_digits(const std::vector<Digit>& in) {
+  std::vector<Digit> out;
+  for (auto& x : in) {
+    if (x.dim == 1) continue;
+    if (!out.empty() && out.back().stride == x.dim * x.stride) {
+      out.back().dim *= x.dim;
+      out.back().stride = x.stride;
+    } else {
+      out.push_back(x);
+    }
+  }
+  return out;
+}
+
+struct Operand {
+  int rank;
+  std::vector<int64_t> ldim, lstride;  // logical
+};
+
+int make_operand(int rank, const int64_t* shape, const int32_t* perm, Operand& o) {
+  if (rank < 0 || rank > TNB_MAX_RANK) return fail(TNB_EINVAL, "contract: rank out of range");
+  std::vector<int64_t> ss(rank, 1);
+  for (int a = rank - 2; a >= 0; --a) ss[a] = ss[a + 1] * shape[a + 1];
+  std::vector<int> seen(rank, 0);
+  o.rank = rank;
+  o.ldim.resize(rank);
+  o.lstride.resize(rank);
+  for (int k = 0; k < rank; ++k) {
+    int p = perm[k];
+    if (p < 0 || p >= rank || seen[p]) return fail(TNB_EINVAL, "contract: invalid permutation");
+    seen[p] = 1;
+    if (shape[p] < 1) return fail(TNB_EINVAL, "contract: dimensions must be >= 1");
+    o.ldim[k] = shape[p];
+    o.lstride[k] = ss[p];
+  }
+  return TNB_OK;
+}
+
+struct Cfg {
+  int bm, bn;
+};
+
+int sms() { return sm_count(); }
+
+// WS = 1: warp-specialised kernel (producer warpgroup + DMMA warps); 0: single-role kernel.
+template <bool CPLX, int MODE, int BM, int BN, int BK, int WM, int WN, int ST, int MINB, int WS = 0>
+struct Tiled {
+  static constexpr int ES = CPLX ? 16 : 8;
+  static constexpr size_t smem = WS ? TileCoreWS<CPLX, MODE, BM, BN, BK, WM, WN, ST, 0, 0>::kSmem
+                                    : TileCore<CPLX, MODE, BM, BN, BK, WM, WN, ST>::kSmem;
+  static constexpr int threads = WM * WN * 32 + (WS ? 128 : 0);
+  using KernT = void (*)(const typename Elem<CPLX>::T*, const typename Elem<CPLX>::T*, typename Elem<CPLX>::T*,
+                         const GemmDesc);
+  static KernT kernel() {
+    if constexpr (WS) return gemm_ws_kernel<CPLX, MODE, BM, BN, BK, WM, WN, ST>;
+    else return gemm_kernel<CPLX, MODE, BM, BN, BK, WM, WN, ST, MINB>;
+  }
+  // resident CTAs per SM (queried once; one process drives one device)
+  static int per_sm() {
+    static int cached = -1;
+    if (cached < 0) {
+      auto kern = kernel();
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+      }
+      int n = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+      }
+      cached = n;
+    }
+    return cached;
+  }
+  // estimated time (arbitrary units: SM-cycles at the DMMA rate) and the split-K factor
+  static double plan(const GemmDesc& d, int& split, double tile_penalty) {
+    int psm = per_sm();
+    if (psm < 1) return 1e300;
+    const int slots = sms() * psm;
+    const int64_t tiles = (int64_t)((d.M + BM - 1) / BM) * ((d.N + BN - 1) / BN);
+    const int kt_total = (d.K + BK - 1) / BK;
+    const double step = (double)BM * BN * BK * (CPLX ? (MODE == 1 ? 3 : 4) : 1) / 64.0 * psm * tile_penalty;
+    double best = 1e300;
+    split = 1;
+    for (int s = 1; s <= 128; ++s) {
+      if (s > 1 && kt_total / s < 4) break;
+      int64_t waves = (tiles * s + slots - 1) / slots;
+      double t = (double)waves * ((kt_total + s - 1) / s) * step;
+      if (s > 1) t += (double)(s + 1) * d.M * (double)d.N * ES / 6.0e12 * 1.9e9 + 3000.0;  // reduce pass
+      if (t < best * 0.98) {
+        best = t;
+        split = s;
+      }
+    }
+    return best;
+  }
+  static int run(const void* A, const void* B, void* C, GemmDesc d, int split, cudaStream_t st) {
+    using T = typename Elem<CPLX>::T;
+    auto kern = kernel();
+    if (per_sm() < 1) return fail(TNB_ECUDA, "contract: GEMM kernel does not fit on an SM");
+    d.tiles_m = (d.M + BM - 1) / BM;
+    d.tiles_n = (d.N + BN - 1) / BN;
+    const int kt_total = (d.K + BK - 1) / BK;
+    int kts = (kt_total + split - 1) / split;
+    d.k_per_split = kts * BK;
+    d.splitk = (kt_total + kts - 1) / kts;
+    if (d.splitk < 1) d.splitk = 1;
+    int64_t grid = (int64_t)d.tiles_m * d.tiles_n * d.splitk;
+    if (grid >= (1ll << 31)) return fail(TNB_EUNSUP, "contract: problem too large for the tile grid");
+    if (d.splitk == 1) {
+      kern<<<(unsigned)grid, threads, smem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B),
+                                                  static_cast<T*>(C), d);
+      count_launch();
+      TNB_CUDA_CHECK(cudaGetLastError());
+      return TNB_OK;
+    }
+    size_t n = (size_t)d.M * d.N;
+    void* ws = nullptr;
+    TNB_CUDA_CHECK(cudaMallocAsync(&ws, n * d.splitk * ES, st));
+    kern<<<(unsigned)grid, threads, smem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B),
+                                                static_cast<T*>(ws), d);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) {
+      int blocks = (int)std::min<size_t>((n + 255) / 256, (size_t)sms() * 8);
+      splitk_reduce_kernel<CPLX><<<blocks, 256, 0, st>>>(static_cast<const T*>(ws), static_cast<T*>(C), (int64_t)n,
+                                                           d.splitk);
+      count_launch();
+      e = cudaGetLastError();
+    }
+    cudaFreeAsync(ws, st);
+    if (e != cudaSuccess) return cuda_fail(e, "contract: split-K GEMM launch");
+    return TNB_OK;
+  }
+};
+
+template <bool CPLX>
+size_t skinny_smem(const GemmDesc& d);
+
+template <bool CPLX>
+int run_skinny(const void* A, const void* B, void* C, GemmDesc d, cudaStream_t st) {
+  using T = typename Elem<CPLX>::T;
+  constexpr int ES = CPLX ? 16 : 8;
+  size_t smem = skinny_smem<CPLX>(d);
+  auto kern = skinny_kernel<CPLX>;
+  if (smem > 48 * 1024) TNB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  TNB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+  if (per_sm < 1) per_sm = 1;
+  int64_t panels = (d.M + 127) / 128;
+  int64_t grid = std::min<int64_t>(panels, (int64_t)sms() * per_sm);
+  kern<<<(unsigned)grid, 256, smem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B), static_cast<T*>(C), d);
+  count_launch();
+  TNB_CUDA_CHECK(cudaGetLastError());
+  return TNB_OK;
+}
+
+template <bool CPLX>
+size_t skinny_smem(const GemmDesc& d) {
+  constexpr int ES = CPLX ? 16 : 8;
+  return (size_t)ES * (d.K * d.N + 128 * (d.K + 1) + 128 * d.N) + 8 * (d.K + 128);
+}
+
+template <bool CPLX, int MODE>
+int dispatch(const void* A, const void* B, void* C, GemmDesc& d, cudaStream_t st) {
+  if (d.N <= 64 && d.K <= 64 && d.M >= 4096 && skinny_smem<CPLX>(d) <= 160 * 1024)
+    return run_skinny<CPLX>(A, B, C, d, st);
+  if constexpr (!CPLX) {
+    using Big = Tiled<false, 0, 128, 128, 16, 4, 4, 4, 1, 1>;
+    using Small = Tiled<false, 0, 64, 64, 16, 2, 2, 3, 2>;
+    int sb = 1, ss = 1;
+    double tb = Big::plan(d, sb, 1.0), ts = Small::plan(d, ss, 1.15);
+    if (tb <= ts) return Big::run(A, B, C, d, sb, st);
+    return Small::run(A, B, C, d, ss, st);
+  } else {
+    using Big = Tiled<true, MODE, 64, (MODE == 1 ? 64 : 128), 8, 4, 4, 4, 1, 1>;
+    using Small = Tiled<true, MODE, 64, 64, 8, 2, 2, 3, 2>;
+    int sb = 1, ss = 1;
+    double tb = Big::plan(d, sb, 1.0), ts = Small::plan(d, ss, 1.1);
+    if (tb <= ts) return Big::run(A, B, C, d, sb, st);
+    return Small::run(A, B, C, d, ss, st);
+  }
+}
+
+// f64 -> c128 widening (mixed-dtype contraction promotes like np.result_type)
+__global__ void widen_kernel(const double* __restrict__ x, double2* __restrict__ y, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) y[i] = make_double2(x[i], 0.0);
+}
+
+}  // namespace
+
+int contract_dense_device(const void* a, int dta, int ra, const int64_t* sa, const int32_t* pa, const void* b,
+                          int dtb, int rb, const int64_t* sb, const int32_t* pb, int nc, const int32_t* aax,
+                          const int32_t* bax, void* out, int cplx_mode, cudaStream_t st) {
+  if ((dta != TNB_F64 && dta != TNB_C128) || (dtb != TNB_F64 && dtb != TNB_C128))
+    return fail(TNB_EUNSUP, "contract: only float64 and complex128 are supported on the GPU path (no CPU fallback)");
+  Operand A, B;
+  int rc = make_operand(ra, sa, pa, A);
+  if (rc) return rc;
+  rc = make_operand(rb, sb, pb, B);
+  if (rc) return rc;
+  if (nc < 0 || nc > ra || nc > rb) return fail(TNB_EINVAL, "contract: bad number of contracted axes");
+  std::vector<int> acon(ra, 0), bcon(rb, 0);
+  for (int i = 0; i < nc; ++i) {
+    int x = aax[i], y = bax[i];
+    if (x < 0 || x >= ra || y < 0 || y >= rb || acon[x] || bcon[y])
+      return fail(TNB_EINVAL, "contract: bad contracted axis list");
+    if (A.ldim[x] != B.ldim[y]) return fail(TNB_EINVAL, "contract: contracted dimensions differ");
+    acon[x] = bcon[y] = 1;
+  }
+  // mixed dtypes: widen the f64 operand into a temporary c128 buffer
+  void* tmp = nullptr;
+  bool cplx = (dta == TNB_C128) || (dtb == TNB_C128);
+  if (cplx && (dta != dtb)) {
+    const Operand& R = (dta == TNB_F64) ? A : B;
+    int64_t n = 1;
+    for (int k = 0; k < R.rank; ++k) n *= R.ldim[k];
+    TNB_CUDA_CHECK(cudaMallocAsync(&tmp, (size_t)n * 16, st));
+    int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms() * 8);
+    widen_kernel<<<std::max(blocks, 1), 256, 0, st>>>(static_cast<const double*>(dta == TNB_F64 ? a : b),
+                                                      static_cast<double2*>(tmp), n);
+    count_launch();
+    if (dta == TNB_F64) a = tmp;
+    else b = tmp;
+  }
+  std::vector<Digit> rowA, kA, kB, colB;
+  for (int k = 0; k < ra; ++k)
+    if (!acon[k]) rowA.push_back({A.ldim[k], A.lstride[k]});
+  for (int k = 0; k < rb; ++k)
+    if (!bcon[k]) colB.push_back({B.ldim[k], B.lstride[k]});
+  // contracted digits: merge only when both operands allow it
+  std::vector<Digit> ka_raw, kb_raw;
+  for (int i = 0; i < nc; ++i) {
+    if (A.ldim[aax[i]] == 1) continue;
+    ka_raw.push_back({A.ldim[aax[i]], A.lstride[aax[i]]});
+    kb_raw.push_back({B.ldim[bax[i]], B.lstride[bax[i]]});
+  }
+  for (size_t i = 0; i < ka_raw.size(); ++i) {
+    if (!kA.empty() && kA.back().stride == ka_raw[i].dim * ka_raw[i].stride &&
+        kB.back().stride == kb_raw[i].dim * kb_raw[i].stride) {
+      kA.back().dim *= ka_raw[i].dim;
+      kA.back().stride = ka_raw[i].stride;
+      kB.back().dim *= kb_raw[i].dim;
+      kB.back().stride = kb_raw[i].stride;
+    } else {
+      kA.push_back(ka_raw[i]);
+      kB.push_back(kb_raw[i]);
+    }
+  }
+  rowA = merge_digits(rowA);
+  colB = merge_digits(colB);
+  // Contraction order over K is free (only the summation order changes): put the
+  // digit that makes every 16-wide k-tile affine innermost, preferring a digit
+  // that is contiguous in one of the operands.
+  if (kA.size() > 1) {
+    int best = -1;
+    int64_t best_score = -1;
+    for (size_t i = 0; i < kA.size(); ++i) {
+      if (kA[i].dim % 16) continue;
+      int64_t score = kA[i].dim + ((kA[i].stride == 1 || kB[i].stride == 1) ? (int64_t(1) << 40) : 0);
+      if (score > best_score) {
+        best_score = score;
+        best = (int)i;
+      }
+    }
+    if (best >= 0 && best != (int)kA.size() - 1) {
+      Digit da = kA[best], db = kB[best];
+      kA.erase(kA.begin() + best);
+      kB.erase(kB.begin() + best);
+      kA.push_back(da);
+      kB.push_back(db);
+    }
+  }
+  GemmDesc d;
+  memset(&d, 0, sizeof(d));
+  int64_t M, N, K, K2;
+  if (!build_group(rowA, d.rowA, M) || !build_group(colB, d.colB, N) || !build_group(kA, d.kA, K) ||
+      !build_group(kB, d.kB, K2)) {
+    if (tmp) cudaFreeAsync(tmp, st);
+    return fail(TNB_EUNSUP, "contract: index group has too many non-mergeable axes or a dimension >= 2^31");
+  }
+  if (M >= (1ll << 31) || N >= (1ll << 31) || K >= (1ll << 31) || M * N >= (1ll << 40)) {
+    if (tmp) cudaFreeAsync(tmp, st);
+    return fail(TNB_EUNSUP, "contract: GEMM extent >= 2^31");
+  }
+  d.M = (int)M;
+  d.N = (int)N;
+  d.K = (int)K;
+  d.kaff.ok = 0;
+  if (d.kA.n == 0) {
+    d.kaff.ok = 0;  // K == 1: the single (partial) k-tile takes the table path
+  } else if (d.kA.dim[d.kA.n - 1] % 16 == 0) {
+    d.kaff.ok = 1;
+    d.kaff.ksA = d.kA.stride[d.kA.n - 1];
+    d.kaff.ksB = d.kB.stride[d.kB.n - 1];
+  }
+  d.out_ld = (int)N;
+  d.a_mfast = 1;
+  if (!(d.rowA.n > 0 && d.rowA.stride[d.rowA.n - 1] == 1 && d.rowA.dim[d.rowA.n - 1] >= 4) && d.kA.n > 0 &&
+      d.kA.stride[d.kA.n - 1] == 1)
+    d.a_mfast = 0;
+  d.b_nfast = 1;
+  if (!(d.colB.n > 0 && d.colB.stride[d.colB.n - 1] == 1 && d.colB.dim[d.colB.n - 1] >= 4) && d.kB.n > 0 &&
+      d.kB.stride[d.kB.n - 1] == 1)
+    d.b_nfast = 0;
+  if (!cplx) rc = dispatch<false, 0>(a, b, out, d, st);
+  else if (cplx_mode == TNB_CPLX_3M) rc = dispatch<true, 1>(a, b, out, d, st);
+  else rc = dispatch<true, 0>(a, b, out, d, st);
+  if (tmp) cudaFreeAsync(tmp, st);
+  return rc;
+}
+
+}  // namespace tnb
+
+extern "C" int tnb_contract_dense(const void* a, int dtype_a, int rank_a, const int64_t* shape_a,
+                                  const int32_t* perm_a, const void* b, int dtype_b, int rank_b,
+                                  const int64_t* shape_b, const int32_t* perm_b, int nc, const int32_t* a_axes,
+                                  const int32_t* b_axes, void* out, int cplx_mode, void* stream) {
+  int rc = tnb::require_device();
+  if (rc) return rc;
+  if ((rank_a > 0 && (!shape_a || !perm_a)) || (rank_b > 0 && (!shape_b || !perm_b)) ||
+      (nc > 0 && (!a_axes || !b_axes)) || !a || !b || !out)
+    return tnb::fail(TNB_EINVAL, "contract: NULL argument");
+  return tnb::contract_dense_device(a, dtype_a, rank_a, shape_a, perm_a, b, dtype_b, rank_b, shape_b, perm_b, nc,
+                                    a_axes, b_axes, out, cplx_mode, (cudaStream_t)stream);
+}

@@ -1,0 +1,753 @@
+// a7: materialise a lazy permute -- the B200 replacement for
+//     np.ascontiguousarray(self.view())   (pkg/src/tnkit/storage.py:122, :126, :143)
+//
+// Design:
+//   * host: drop unit axes, merge logical axes that stay adjacent in storage,
+//     then choose a tile = (input-fast axis group G_in) x (output-fast group
+//     G_out): G_in is a storage suffix long enough that each warp READS >=256 B
+//     contiguous runs, G_out an output suffix long enough that each warp
+//     WRITES >=256 B contiguous runs. All other axes are "batch" axes.
+//   * device: persistent CTAs loop over tiles. Each tile is read in storage
+//     order (coalesced 8/16-byte lanes) into a padded shared-memory tile, then
+//     written in output order (coalesced). Per-tile index math is O(rank);
+//     per-element math is one multiply-high division and 1-3 shared-memory
+//     table lookups (tables built once per CTA).
+//   * bit-exact: pure data movement of elem_size-byte words.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace tnb {
+namespace {
+
+constexpr int kMaxR = TNB_MAX_RANK;
+constexpr int kThreads = 512;
+
+template <int ES>
+struct Word;
+template <>
+struct Word<1> { using T = uint8_t; };
+template <>
+struct Word<2> { using T = uint16_t; };
+template <>
+struct Word<4> { using T = uint32_t; };
+template <>
+struct Word<8> { using T = unsigned long long; };
+template <>
+struct Word<16> { using T = uint4; };
+
+struct PermDesc {
+  int r;                     // merged rank
+  int nb;                    // number of batch axes (nt > 1), output order outer->inner
+  int nuin, nuout;           // |U| in input order / output order (same set)
+  int gin, gout;             // innermost counts forming G_in (of uin) / G_out (of uout)
+  int N_t, N_in, N_out, rowp;  // tile elements, input run, output run, padded row length
+  int n_hi_in, n_hi_out;     // N_t / N_in, N_t / N_out
+  int a_in, a_out;           // partial (split) axes or -1
+  int64_t ntiles;
+  int64_t dim[kMaxR];
+  int64_t istride[kMaxR];    // storage stride of storage axis a
+  int64_t ostride[kMaxR];    // output stride of storage axis a
+  int32_t ext[kMaxR];        // tile extent along storage axis a (1 if not in U)
+  int32_t bax[kMaxR];        // batch axes
+  uint32_t bnt[kMaxR];       // tiles along batch axis
+  FastDiv bdiv[kMaxR];
+  int32_t uin[kMaxR];        // U axes in storage order (outer->inner)
+  int32_t uout[kMaxR];       // U axes in output order (outer->inner)
+  int32_t pts[kMaxR];        // padded smem tile stride of storage axis a
+  int32_t tsi[kMaxR];        // unpadded input-order tile stride (boundary path)
+  int32_t tso[kMaxR];        // output-order tile stride (boundary path)
+  FastDiv div_in, div_out;   // by N_in, N_out
+  FastDiv tsi_div[kMaxR], tso_div[kMaxR], ext_div[kMaxR];
+};
+
+// Shared-memory layout per CTA: [tile data (N_t padded) | inhi | outhi | shi | slo]
+template <int ES>
+__global__ void __launch_bounds__(kThreads, 2) permute_tiled_kernel(
+    const typename Word<ES>::T* __restrict__ src, typename Word<ES>::T* __restrict__ dst,
+    const PermDesc d) {
+  using T = typename Word<ES>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* tile = reinterpret_cast<T*>(smem_raw);
+  const int tile_words = d.n_hi_in * d.rowp;
+  int64_t* inhi = reinterpret_cast<int64_t*>(smem_raw + (((size_t)tile_words * ES + 15) & ~(size_t)15));
+  int64_t* outhi = inhi + d.n_hi_in;
+  int32_t* shi = reinterpret_cast<int32_t*>(outhi + d.n_hi_out);
+  int32_t* slo = shi + d.n_hi_out;
+
+  // ---- per-CTA tables -------------------------------------------------------
+  // inhi[h]: storage offset of the hi part (U \ G_in, storage order) of input index h
+  for (int h = threadIdx.x; h < d.n_hi_in; h += blockDim.x) {
+    int64_t off = 0;
+    int rem = h;
+    for (int q = d.nuin - d.gin - 1; q >= 0; --q) {
+      int a = d.uin[q];
+      int e = d.ext[a];
+      int dig = rem % e;
+      rem /= e;
+      off += (int64_t)dig * d.istride[a];
+    }
+    inhi[h] = off;
+  }
+  // outhi[g], shi[g]: output offset / smem offset of the hi part (U \ G_out, output order)
+  for (int g = threadIdx.x; g < d.n_hi_out; g += blockDim.x) {
+    int64_t off = 0;
+    int32_t s = 0;
+    int rem = g;
+    for (int q = d.nuout - d.gout - 1; q >= 0; --q) {
+      int a = d.uout[q];
+      int e = d.ext[a];
+      int dig = rem % e;
+      rem /= e;
+      off += (int64_t)dig * d.ostride[a];
+      s += dig * d.pts[a];
+    }
+    outhi[g] = off;
+    shi[g] = s;
+  }
+  // slo[l]: smem offset of the lo part (G_out, output order)
+  for (int l = threadIdx.x; l < d.N_out; l += blockDim.x) {
+    int32_t s = 0;
+    int rem = l;
+    for (int q = d.nuout - 1; q >= d.nuout - d.gout; --q) {
+      int a = d.uout[q];
+      int e = d.ext[a];
+      int dig = rem % e;
+      rem /= e;
+      s += dig * d.pts[a];
+    }
+    slo[l] = s;
+  }
+  __syncthreads();
+
+  constexpr int kMaxItems = 8;  // N_t <= kThreads * kMaxItems
+  for (int64_t tileid = blockIdx.x; tileid < d.ntiles; tileid += gridDim.x) {
+    // tile coordinates -> base offsets, boundary limits
+    int64_t base_in = 0, base_out = 0;
+    int lim_in = 1 << 30, lim_out = 1 << 30;
+    {
+      uint32_t rem_hi = (uint32_t)(tileid >> 31);  // ntiles < 2^31 enforced on host
+      (void)rem_hi;
+      uint32_t rem = (uint32_t)tileid;
+      for (int q = d.nb - 1; q >= 0; --q) {
+        int a = d.bax[q];
+        uint32_t quo = d.bdiv[q].div(rem);
+        uint32_t c = rem - quo * d.bnt[q];
+        rem = quo;
+        int64_t start = (int64_t)c * d.ext[a];
+        base_in += start * d.istride[a];
+        base_out += start * d.ostride[a];
+        if (a == d.a_in) lim_in = (int)(d.dim[a] - start);
+        if (a == d.a_out) lim_out = (int)(d.dim[a] - start);
+      }
+    }
+    const bool boundary = (d.a_in >= 0 && lim_in < d.ext[d.a_in]) ||
+                          (d.a_out >= 0 && lim_out < d.ext[d.a_out]);
+    const T* s = src + base_in;
+    T* o = dst + base_out;
+    if (!boundary) {
+      T v[kMaxItems];
+#pragma unroll
+      for (int it = 0; it < kMaxItems; ++it) {
+        int t = threadIdx.x + it * kThreads;
+        if (t < d.N_t) {
+          uint32_t hi = d.div_in.div((uint32_t)t);
+          uint32_t lo = (uint32_t)t - hi * (uint32_t)d.N_in;
+          v[it] = __ldg(s + inhi[hi] + lo);
+        }
+      }
+#pragma unroll
+      for (int it = 0; it < kMaxItems; ++it) {
+        int t = threadIdx.x + it * kThreads;
+        if (t < d.N_t) {
+          uint32_t hi = d.div_in.div((uint32_t)t);
+          uint32_t lo = (uint32_t)t - hi * (uint32_t)d.N_in;
+          tile[hi * d.rowp + lo] = v[it];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int it = 0; it < kMaxItems; ++it) {
+        int u = threadIdx.x + it * kThreads;
+        if (u < d.N_t) {
+          uint32_t hi = d.div_out.div((uint32_t)u);
+          uint32_t lo = (uint32_t)u - hi * (uint32_t)d.N_out;
+          v[it] = tile[shi[hi] + slo[lo]];
+        }
+      }
+#pragma unroll
+      for (int it = 0; it < kMaxItems; ++it) {
+        int u = threadIdx.x + it * kThreads;
+        if (u < d.N_t) {
+          uint32_t hi = d.div_out.div((uint32_t)u);
+          uint32_t lo = (uint32_t)u - hi * (uint32_t)d.N_out;
+          o[outhi[hi] + lo] = v[it];
+        }
+      }
+      __syncthreads();
+    } else {
+      // boundary tile: per-element validity on the (at most two) split axes
+      for (int t = threadIdx.x; t < d.N_t; t += kThreads) {
+        bool ok = true;
+        if (d.a_in >= 0) {
+          int a = d.a_in;
+          uint32_t q = d.tsi_div[a].div((uint32_t)t);
+          uint32_t dig = q - d.ext_div[a].div(q) * d.ext[a];
+          ok = ok && (int)dig < lim_in;
+        }
+        if (d.a_out >= 0) {
+          int a = d.a_out;
+          uint32_t q = d.tsi_div[a].div((uint32_t)t);
+          uint32_t dig = q - d.ext_div[a].div(q) * d.ext[a];
+          ok = ok && (int)dig < lim_out;
+        }
+        if (ok) {
+          uint32_t hi = d.div_in.div((uint32_t)t);
+          uint32_t lo = (uint32_t)t - hi * (uint32_t)d.N_in;
+          tile[hi * d.rowp + lo] = __ldg(s + inhi[hi] + lo);
+        }
+      }
+      __syncthreads();
+      for (int u = threadIdx.x; u < d.N_t; u += kThreads) {
+        bool ok = true;
+        if (d.a_in >= 0) {
+          int a = d.a_in;
+          uint32_t q = d.tso_div[a].div((uint32_t)u);
+          uint32_t dig = q - d.ext_div[a].div(q) * d.ext[a];
+          ok = ok && (int)dig < lim_in;
+        }
+        if (d.a_out >= 0) {
+          int a = d.a_out;
+          uint32_t q = d.tso_div[a].div((uint32_t)u);
+          uint32_t dig = q - d.ext_div[a].div(q) * d.ext[a];
+          ok = ok && (int)dig < lim_out;
+        }
+        if (ok) {
+          uint32_t hi = d.div_out.div((uint32_t)u);
+          uint32_t lo = (uint32_t)u - hi * (uint32_t)d.N_out;
+          o[outhi[hi] + lo] = tile[shi[hi] + slo[lo]];
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fast path 1 -- shared innermost axis (after merging, the storage-innermost
+// axis is also the output-innermost axis): the permute is a gather of
+// contiguous rows of L elements. Work unit = (row, 2 KB chunk); each lane moves
+// 16-byte vectors, four in flight.
+struct RowDesc {
+  int64_t L;          // row length (elements)
+  int64_t rows;
+  int64_t chunks;     // chunks per row
+  int nb;             // other axes, output order (outer -> inner)
+  int64_t bdim[kMaxR];
+  int64_t bistr[kMaxR];
+  FastDiv bdiv[kMaxR];
+  FastDiv chunk_div;
+  int vec;            // 1: 16-byte vectors usable (aligned rows), 0: element copies
+};
+
+template <int ES>
+__global__ void __launch_bounds__(256) permute_rows_kernel(const unsigned char* __restrict__ src,
+                                                           unsigned char* __restrict__ dst, const RowDesc d) {
+  using T = typename Word<ES>::T;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t units = d.rows * d.chunks;
+  constexpr int kChunkBytes = 2048;
+  for (int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < units; u += warps) {
+    uint32_t row = d.chunk_div.div((uint32_t)u);
+    int64_t chunk = u - (int64_t)row * d.chunks;
+    int64_t in_off = 0;
+    uint32_t rem = row;
+    for (int q = d.nb - 1; q >= 0; --q) {
+      uint32_t quo = d.bdiv[q].div(rem);
+      in_off += (int64_t)(rem - quo * (uint32_t)d.bdim[q]) * d.bistr[q];
+      rem = quo;
+    }
+    const int64_t row_bytes = d.L * ES;
+    const int64_t b0 = chunk * kChunkBytes;
+    const int64_t nbytes = min((int64_t)kChunkBytes, row_bytes - b0);
+    const unsigned char* s = src + in_off * ES + b0;
+    unsigned char* o = dst + (int64_t)row * row_bytes + b0;
+    if (d.vec) {
+      const uint4* s4 = reinterpret_cast<const uint4*>(s);
+      uint4* o4 = reinterpret_cast<uint4*>(o);
+      const int nv = (int)(nbytes >> 4);
+      uint4 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (lane + 32 * k < nv) v[k] = __ldcs(s4 + lane + 32 * k);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (lane + 32 * k < nv) __stcs(o4 + lane + 32 * k, v[k]);
+    } else {
+      const T* st = reinterpret_cast<const T*>(s);
+      T* ot = reinterpret_cast<T*>(o);
+      const int ne = (int)(nbytes / ES);
+      for (int e = lane; e < ne; e += 32) ot[e] = st[e];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fast path 2 -- 2-D transpose with batch: the storage-innermost axis (i, dim Di)
+// and the output-innermost axis (j, dim Do) differ. One warp owns a T x T tile:
+// it reads T rows of j (each a contiguous run of T i-elements, 256 B), stages
+// them in a padded per-warp shared tile, and writes T rows of i (contiguous
+// runs of T j-elements). No block barriers; T*T/32 loads in flight per lane.
+struct T2Desc {
+  int64_t Di, Do;      // extents of the i / j axes
+  int64_t sj;          // input stride of j
+  int64_t si;          // output stride of i
+  int64_t ti, tj;      // tiles along i / j
+  int64_t ntiles;      // batch * ti * tj
+  int nb;              // batch axes, output order (outer -> inner)
+  int64_t bdim[kMaxR];
+  int64_t bistr[kMaxR];
+  int64_t bostr[kMaxR];
+  FastDiv bdiv[kMaxR];
+  FastDiv ti_div, tj_div;
+};
+
+template <int ES, int T>
+__global__ void __launch_bounds__(256) permute_t2d_kernel(const typename Word<ES>::T* __restrict__ src,
+                                                          typename Word<ES>::T* __restrict__ dst, const T2Desc d) {
+  using W = typename Word<ES>::T;
+  constexpr int RPI = 32 / T;      // rows per warp instruction
+  constexpr int NI = T / RPI;      // instructions per tile side
+  constexpr int LD = T + 1;        // padded smem row
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  W* tile = reinterpret_cast<W*>(smem_raw) + warp * T * LD;
+  const int r0 = lane / T, c = lane % T;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; t < d.ntiles; t += nwarps) {
+    uint32_t q = (uint32_t)t;
+    uint32_t qi = d.ti_div.div(q);
+    const int64_t it = q - qi * (uint32_t)d.ti;
+    uint32_t qj = d.tj_div.div(qi);
+    const int64_t jt = qi - qj * (uint32_t)d.tj;
+    int64_t bin = 0, bout = 0;
+    uint32_t rem = qj;
+    for (int k = d.nb - 1; k >= 0; --k) {
+      uint32_t quo = d.bdiv[k].div(rem);
+      int64_t dig = rem - quo * (uint32_t)d.bdim[k];
+      rem = quo;
+      bin += dig * d.bistr[k];
+      bout += dig * d.bostr[k];
+    }
+    const int64_t i0 = it * T, j0 = jt * T;
+    const bool full = (i0 + T <= d.Di) && (j0 + T <= d.Do);
+    const W* s = src + bin + i0 + j0 * d.sj;
+    W* o = dst + bout + j0 + i0 * d.si;
+    W v[NI];
+    if (full) {
+#pragma unroll
+      for (int k = 0; k < NI; ++k) v[k] = __ldcs(s + c + (int64_t)(k * RPI + r0) * d.sj);
+#pragma unroll
+      for (int k = 0; k < NI; ++k) tile[(k * RPI + r0) * LD + c] = v[k];
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < NI; ++k) v[k] = tile[c * LD + k * RPI + r0];
+#pragma unroll
+      for (int k = 0; k < NI; ++k) __stcs(o + c + (int64_t)(k * RPI + r0) * d.si, v[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < NI; ++k) {
+        const int j = k * RPI + r0;
+        if (i0 + c < d.Di && j0 + j < d.Do) tile[j * LD + c] = s[c + (int64_t)j * d.sj];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < NI; ++k) {
+        const int i = k * RPI + r0;
+        if (j0 + c < d.Do && i0 + i < d.Di) o[c + (int64_t)i * d.si] = tile[c * LD + i];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+
+struct Plan {
+  bool identity = false;
+  int64_t nelem = 0;
+  int kind = 0;  // 0 generic tiled, 1 rows, 2 transpose2d
+  int t2d_T = 0;
+  PermDesc d;
+  RowDesc rd;
+  T2Desc td;
+  size_t smem = 0;
+};
+
+int make_plan(int es, int rank, const int64_t* shape, const int32_t* perm, Plan& p) {
+  if (rank < 0 || rank > kMaxR) return fail(TNB_EINVAL, "permute: rank out of range");
+  int64_t n = 1;
+  std::vector<int> seen(rank, 0);
+  for (int k = 0; k < rank; ++k) {
+    if (shape[k] < 0) return fail(TNB_EINVAL, "permute: negative dimension");
+    n *= shape[k];
+    if (perm[k] < 0 || perm[k] >= rank || seen[perm[k]]) return fail(TNB_EINVAL, "permute: invalid permutation");
+    seen[perm[k]] = 1;
+  }
+  p.nelem = n;
+  if (n <= 1) { p.identity = true; return TNB_OK; }
+  // storage strides
+  std::vector<int64_t> sstride(rank, 1);
+  for (int a = rank - 2; a >= 0; --a) sstride[a] = sstride[a + 1] * shape[a + 1];
+  // logical axes (output order), dropping unit dims
+  std::vector<int> lax;
+  for (int k = 0; k < rank; ++k)
+    if (shape[perm[k]] != 1) lax.push_back(perm[k]);
+  // merge logical neighbours that are storage neighbours (storage axis a followed by a+1,
+  // ignoring unit storage axes in between)
+  struct Ax { int64_t dim, istride; int skey; };
+  std::vector<Ax> out_axes;  // output order
+  for (size_t i = 0; i < lax.size(); ++i) {
+    int a = lax[i];
+    if (!out_axes.empty()) {
+      Ax& prev = out_axes.back();
+      if (prev.istride == shape[a] * sstride[a]) {  // prev is directly outside a in storage
+        prev.dim *= shape[a];
+        prev.istride = sstride[a];
+        prev.skey = a;
+        continue;
+      }
+    }
+    out_axes.push_back({shape[a], sstride[a], a});
+  }
+  int r = (int)out_axes.size();
+  // storage order of merged axes: sort by istride descending
+  std::vector<int> sorder(r);
+  for (int i = 0; i < r; ++i) sorder[i] = i;
+  std::sort(sorder.begin(), sorder.end(), [&](int x, int y) { return out_axes[x].istride > out_axes[y].istride; });
+  bool ident = true;
+  for (int i = 0; i < r; ++i) ident = ident && (sorder[i] == i);
+  if (ident) { p.identity = true; return TNB_OK; }
+  if (n >= (int64_t(1) << 62)) return fail(TNB_EINVAL, "permute: tensor too large");
+
+  PermDesc& d = p.d;
+  memset(&d, 0, sizeof(d));
+  d.r = r;
+  // index merged axes by STORAGE position a = 0..r-1 (outer->inner)
+  std::vector<int> s2o(r);  // storage pos -> output pos
+  for (int a = 0; a < r; ++a) s2o[a] = sorder[a];
+  std::vector<int> o2s(r);
+  for (int a = 0; a < r; ++a) o2s[sorder[a]] = a;
+  {
+    // merged axes by storage position: dims / strides (input) and output strides
+    std::vector<int64_t> mdim(r), mis(r), mos(r);
+    std::vector<int64_t> ostr_k(r, 1);
+    for (int k = r - 2; k >= 0; --k) ostr_k[k] = ostr_k[k + 1] * out_axes[k + 1].dim;
+    for (int a = 0; a < r; ++a) {
+      mdim[a] = out_axes[s2o[a]].dim;
+      mis[a] = out_axes[s2o[a]].istride;
+      mos[a] = ostr_k[s2o[a]];
+    }
+    const int a_si = r - 1, a_so = o2s[r - 1];
+    if (a_si == a_so && mdim[a_si] * es >= 64 && n / mdim[a_si] < (int64_t(1) << 31)) {
+      RowDesc& rd = p.rd;
+      memset(&rd, 0, sizeof(rd));
+      rd.L = mdim[a_si];
+      rd.rows = n / rd.L;
+      rd.chunks = (rd.L * es + 2047) / 2048;
+      if (rd.rows * rd.chunks >= (int64_t(1) << 31)) return fail(TNB_EUNSUP, "permute: too many rows");
+      rd.chunk_div = FastDiv((uint32_t)rd.chunks);
+      for (int k = 0; k < r - 1; ++k) {
+        int a = o2s[k];
+        rd.bdim[rd.nb] = mdim[a];
+        rd.bistr[rd.nb] = mis[a];
+        rd.bdiv[rd.nb] = FastDiv((uint32_t)mdim[a]);
+        rd.nb++;
+      }
+      rd.vec = ((rd.L * es) % 16 == 0) ? 1 : 0;
+      p.kind = 1;
+      return TNB_OK;
+    }
+    if (a_si != a_so && mdim[a_si] * es >= 64 && mdim[a_so] * es >= 64 && (es == 8 || es == 16)) {
+      T2Desc& td = p.td;
+      memset(&td, 0, sizeof(td));
+      int T = (es == 8) ? ((mdim[a_si] >= 32 && mdim[a_so] >= 32) ? 32 : 16) : 16;
+      if (es == 16 && (mdim[a_si] < 16 || mdim[a_so] < 16)) T = 8;
+      td.Di = mdim[a_si];
+      td.Do = mdim[a_so];
+      td.sj = mis[a_so];
+      td.si = mos[a_si];
+      td.ti = (td.Di + T - 1) / T;
+      td.tj = (td.Do + T - 1) / T;
+      int64_t nbatch = n / (td.Di * td.Do);
+      td.ntiles = nbatch * td.ti * td.tj;
+      if (td.ntiles < (int64_t(1) << 31)) {
+        td.ti_div = FastDiv((uint32_t)td.ti);
+        td.tj_div = FastDiv((uint32_t)td.tj);
+        for (int k = 0; k < r; ++k) {
+          int a = o2s[k];
+          if (a == a_si || a == a_so) continue;
+          td.bdim[td.nb] = mdim[a];
+          td.bistr[td.nb] = mis[a];
+          td.bostr[td.nb] = mos[a];
+          td.bdiv[td.nb] = FastDiv((uint32_t)mdim[a]);
+          td.nb++;
+        }
+        p.kind = 2;
+        p.t2d_T = T;
+        return TNB_OK;
+      }
+    }
+  }
+  std::vector<int64_t> ostr(r, 1);  // output stride by output position
+  for (int k = r - 2; k >= 0; --k) ostr[k] = ostr[k + 1] * out_axes[k + 1].dim;
+  for (int a = 0; a < r; ++a) {
+    int k = s2o[a];
+    d.dim[a] = out_axes[k].dim;
+    d.istride[a] = out_axes[k].istride;
+    d.ostride[a] = ostr[k];
+    d.ext[a] = 1;
+  }
+  // ---- tile selection ----
+  const int run_lo = std::max(1, 256 / es);     // >= 256 B contiguous per run
+  const int tmax = (es == 16) ? 2048 : 4096;  // <= 32 KB of data per tile
+  std::vector<int> inU(r, 0);
+  // G_in: storage suffix
+  int64_t prod = 1;
+  int gin = 0;
+  d.a_in = -1;
+  for (int a = r - 1; a >= 0 && prod < run_lo; --a) {
+    int64_t need = (run_lo + prod - 1) / prod;
+    if (d.dim[a] <= need || d.dim[a] * prod <= 2 * run_lo) {
+      d.ext[a] = (int32_t)d.dim[a];
+    } else {
+      int64_t e = need;
+      // prefer a divisor of dim in [need, 2*need]
+      for (int64_t c = need; c <= 2 * need; ++c)
+        if (d.dim[a] % c == 0) { e = c; break; }
+      d.ext[a] = (int32_t)e;
+      d.a_in = a;
+    }
+    prod *= d.ext[a];
+    inU[a] = 1;
+    ++gin;
+  }
+  int N_in = (int)prod;
+  // G_out: output suffix
+  int64_t tprod = prod;  // tile size so far
+  int64_t oprod = 1;
+  int gout = 0;
+  d.a_out = -1;
+  for (int k = r - 1; k >= 0; --k) {
+    int a = o2s[k];
+    bool need_more = (oprod < run_lo) || (tprod < 1024 && oprod * 2 <= tmax);
+    if (!need_more) break;
+    if (inU[a]) {
+      if (a == d.a_in && d.ext[a] != d.dim[a]) {  // partial axis: must be G_out's top
+        oprod *= d.ext[a];
+        ++gout;
+        break;
+      }
+      oprod *= d.ext[a];
+      ++gout;
+      continue;
+    }
+    int64_t room = tmax / tprod;
+    if (room < 2) break;
+    int64_t want = (oprod < run_lo) ? (run_lo + oprod - 1) / oprod : std::max<int64_t>(2, 1024 / tprod);
+    want = std::min(want, room);
+    if (d.dim[a] <= want) {
+      d.ext[a] = (int32_t)d.dim[a];
+      inU[a] = 1;
+      oprod *= d.ext[a];
+      tprod *= d.ext[a];
+      ++gout;
+      continue;
+    }
+    int64_t e = want;
+    for (int64_t c = want; c >= std::max<int64_t>(1, want / 2); --c)
+      if (d.dim[a] % c == 0) { e = c; break; }
+    d.ext[a] = (int32_t)e;
+    d.a_out = a;
+    inU[a] = 1;
+    oprod *= e;
+    tprod *= e;
+    ++gout;
+    break;
+  }
+  // G_out must be an output suffix of U with only its top axis partial; fold any U axis
+  // that sits inside it (can only be full G_in axes) -- already counted above.
+  int N_t = (int)tprod;
+  int N_out = (int)oprod;
+  // U in storage order and output order
+  d.nuin = 0;
+  for (int a = 0; a < r; ++a)
+    if (inU[a]) d.uin[d.nuin++] = a;
+  d.nuout = 0;
+  for (int k = 0; k < r; ++k)
+    if (inU[o2s[k]]) d.uout[d.nuout++] = o2s[k];
+  d.gin = gin;
+  d.gout = gout;
+  // sanity: G_out are the innermost gout axes of uout
+  d.N_t = N_t;
+  d.N_in = N_in;
+  d.N_out = N_out;
+  // one 8-byte (or one 16-byte element) pad per input run breaks the power-of-two
+  // row stride that the output-order (column) reads of a 2-D transpose would hit
+  const int pad = (es <= 8) ? 8 / es : 1;
+  d.rowp = N_in + ((N_t / N_in > 1) ? pad : 0);
+  d.n_hi_in = N_t / N_in;
+  d.n_hi_out = N_t / N_out;
+  // tile strides
+  {
+    int32_t acc = 1;
+    for (int q = d.nuin - 1; q >= 0; --q) {
+      int a = d.uin[q];
+      d.tsi[a] = acc;
+      if (q >= d.nuin - gin) d.pts[a] = acc;
+      else d.pts[a] = (acc / N_in) * d.rowp;
+      acc *= d.ext[a];
+    }
+    acc = 1;
+    for (int q = d.nuout - 1; q >= 0; --q) {
+      int a = d.uout[q];
+      d.tso[a] = acc;
+      acc *= d.ext[a];
+    }
+    for (int a = 0; a < r; ++a) {
+      if (inU[a]) {
+        d.tsi_div[a] = FastDiv((uint32_t)d.tsi[a]);
+        d.tso_div[a] = FastDiv((uint32_t)d.tso[a]);
+        d.ext_div[a] = FastDiv((uint32_t)d.ext[a]);
+      }
+    }
+  }
+  d.div_in = FastDiv((uint32_t)N_in);
+  d.div_out = FastDiv((uint32_t)N_out);
+  // batch axes in output order (outer -> inner), tiles along each
+  d.nb = 0;
+  int64_t ntiles = 1;
+  for (int k = 0; k < r; ++k) {
+    int a = o2s[k];
+    int64_t nt = (d.dim[a] + d.ext[a] - 1) / d.ext[a];
+    if (nt > 1) {
+      d.bax[d.nb] = a;
+      d.bnt[d.nb] = (uint32_t)nt;
+      d.bdiv[d.nb] = FastDiv((uint32_t)nt);
+      ++d.nb;
+      ntiles *= nt;
+    }
+  }
+  if (ntiles >= (int64_t(1) << 31)) return fail(TNB_EUNSUP, "permute: too many tiles (tensor too large)");
+  d.ntiles = ntiles;
+  size_t data_bytes = ((size_t)d.n_hi_in * d.rowp * es + 15) & ~(size_t)15;
+  p.smem = data_bytes + (size_t)(d.n_hi_in + d.n_hi_out) * 8 + (size_t)(d.n_hi_out + d.N_out) * 4;
+  if (N_t > kThreads * 8) return fail(TNB_EINVAL, "permute: internal tile too large");
+  return TNB_OK;
+}
+
+template <int ES, int T>
+int launch_t2d(const void* src, void* dst, const Plan& p, cudaStream_t st) {
+  using W = typename Word<ES>::T;
+  auto kern = permute_t2d_kernel<ES, T>;
+  const size_t smem = (size_t)8 * T * (T + 1) * ES;
+  static bool configured = false;
+  if (!configured) {
+    TNB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    TNB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    if (per_sm < 1) per_sm = 1;
+  }
+  int64_t grid = std::min<int64_t>((p.td.ntiles + 7) / 8, (int64_t)sm_count() * per_sm);
+  kern<<<(unsigned)grid, 256, smem, st>>>(static_cast<const W*>(src), static_cast<W*>(dst), p.td);
+  count_launch();
+  TNB_CUDA_CHECK(cudaGetLastError());
+  return TNB_OK;
+}
+
+template <int ES>
+int launch_rows(const void* src, void* dst, const Plan& p, cudaStream_t st) {
+  auto kern = permute_rows_kernel<ES>;
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    TNB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    if (per_sm < 1) per_sm = 1;
+  }
+  int64_t units = p.rd.rows * p.rd.chunks;
+  int64_t grid = std::min<int64_t>((units + 7) / 8, (int64_t)sm_count() * per_sm);
+  RowDesc rd = p.rd;
+  if (rd.vec && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)) rd.vec = 0;
+  kern<<<(unsigned)grid, 256, 0, st>>>(static_cast<const unsigned char*>(src), static_cast<unsigned char*>(dst), rd);
+  count_launch();
+  TNB_CUDA_CHECK(cudaGetLastError());
+  return TNB_OK;
+}
+
+template <int ES>
+int launch(const void* src, void* dst, const Plan& p, cudaStream_t st) {
+  if (p.kind == 1) return launch_rows<ES>(src, dst, p, st);
+  if (p.kind == 2) {
+    if constexpr (ES == 8) {
+      if (p.t2d_T == 32) return launch_t2d<8, 32>(src, dst, p, st);
+      return launch_t2d<8, 16>(src, dst, p, st);
+    }
+    if constexpr (ES == 16) {
+      if (p.t2d_T == 16) return launch_t2d<16, 16>(src, dst, p, st);
+      return launch_t2d<16, 8>(src, dst, p, st);
+    }
+  }
+  using T = typename Word<ES>::T;
+  auto kern = permute_tiled_kernel<ES>;
+  static int configured_smem[1] = {0};
+  if ((int)p.smem > 48 * 1024 && configured_smem[0] < (int)p.smem) {
+    TNB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    configured_smem[0] = (int)p.smem;
+  }
+  int per_sm = 0;
+  TNB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, p.smem));
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = std::min<int64_t>(p.d.ntiles, (int64_t)sm_count() * per_sm);
+  kern<<<(unsigned)grid, kThreads, p.smem, st>>>(static_cast<const T*>(src), static_cast<T*>(dst), p.d);
+  count_launch();
+  TNB_CUDA_CHECK(cudaGetLastError());
+  return TNB_OK;
+}
+
+}  // namespace
+
+int permute_device(const void* src, void* dst, int es, int rank, const int64_t* shape, const int32_t* perm,
+                   cudaStream_t st) {
+  Plan p;
+  int rc = make_plan(es, rank, shape, perm, p);
+  if (rc) return rc;
+  if (p.nelem == 0) return TNB_OK;
+  if (p.identity) {
+    TNB_CUDA_CHECK(cudaMemcpyAsync(dst, src, (size_t)p.nelem * es, cudaMemcpyDeviceToDevice, st));
+    return TNB_OK;
+  }
+  switch (es) {
+    case 1: return launch<1>(src, dst, p, st);
+    case 2: return launch<2>(src, dst, p, st);
+    case 4: return launch<4>(src, dst, p, st);
+    case 8: return launch<8>(src, dst, p, st);
+    case 16: return launch<16>(src, dst, p, st);
+    default: return fail(TNB_EINVAL, "permute: elem_size must be 1, 2, 4, 8 or 16");
+  }
+}
+
+}  // namespace tnb
+
+extern "C" int tnb_permute(const void* src, void* dst, int elem_size, int rank, const int64_t* shape,
+                           const int32_t* perm, void* stream) {
+  int rc = tnb::require_device();
+  if (rc) return rc;
+  if (rank > 0 && (!shape || !perm)) return tnb::fail(TNB_EINVAL, "permute: shape/perm is NULL");
+  if (elem_size != 1 && elem_size != 2 && elem_size != 4 && elem_size != 8 && elem_size != 16)
+    return tnb::fail(TNB_EINVAL, "permute: elem_size must be 1, 2, 4, 8 or 16");
+  return tnb::permute_device(src, dst, elem_size, rank, shape, perm, (cudaStream_t)stream);
+}

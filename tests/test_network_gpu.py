@@ -1,0 +1,143 @@
+"""a16/a17: Network.launch on device tensors vs reference golden launches and the
+oracle; reuse, rebinding, TOUT verbatim, order policy, validation."""
+import numpy as np
+import pytest
+
+import tnkit_np as oracle
+from tnb_testutil import load, rel_fro
+
+import paper_2401_01921_b200 as tnb
+from paper_2401_01921_b200 import IN, Bond, Network, Symmetry, UniTensor, contract_pair, storage
+
+pytestmark = pytest.mark.gpu
+
+MATMUL = ["M1:  i, j", "M2:  j, k", "TOUT: i, k"]
+THREE = ["M1: i, j", "M2: j, k", "M3: k, l", "TOUT: i, l", "ORDER: ((M1,M2),M3)"]
+
+
+def test_golden_network_launches(cuda):
+    z, meta = load("network.npz")
+    for k in range(3):
+        c = meta["cases"][k]
+        net = Network(c["net"])
+        for nm in c["names"]:
+            arr = z[f"n{k}_{nm}"]
+            labels = [f"{nm}{i}" for i in range(arr.ndim)]
+            net.put_tensor(nm, UniTensor(storage.from_numpy(arr), labels=labels), labels)
+        net.set_order(optimal=True)
+        out = net.launch()
+        assert net.get_order() == c["order"] and out.labels == c["labels"] and out.rowrank == c["rowrank"]
+        assert np.max(np.abs(out.numpy() - z[f"n{k}_out"])) <= 1e-12
+    c = meta["cases"][3]
+    net = Network(c["net"])
+    for nm, s in c["shapes"].items():
+        net.put_tensor(nm, UniTensor.ones(s, labels=[f"x{i}" for i in range(len(s))]))
+    out = net.launch()
+    assert out.rank == 0 and out.item() == 4096.0
+    c = meta["cases"][4]
+    net = Network(c["net"])
+    for nm in c["names"]:
+        arr = z[f"n3_{nm}"]
+        net.put_tensor(nm, UniTensor(storage.from_numpy(arr), labels=[f"x{j}" for j in range(arr.ndim)]))
+    net.set_order(optimal=True)
+    val = net.launch().item()
+    assert net.get_order() == c["order"]
+    assert abs(val - c["scalar"]) <= 1e-10 * max(1.0, abs(c["scalar"]))
+    c = meta["cases"][5]
+    net = Network(c["net"])
+    net.put_tensor("A", UniTensor(storage.arange(24).reshape(2, 3, 4), labels=["p", "q", "r"]), ["p", "q", "r"])
+    out = net.launch()
+    assert out.labels == c["labels"] == ["z", "x", "y"] and out.shape == (4, 2, 3) and out.rowrank == 2
+    assert np.array_equal(out.numpy(), z["n5_out"])
+
+
+def test_matmul_reuse_and_rebinding(cuda):
+    net = Network(MATMUL)
+    a = UniTensor.ones([2, 2], labels=["a", "b"], name="A")
+    b = UniTensor(storage.arange(4).reshape(2, 2), labels=["a", "b"], name="B")
+    net.put_tensor("M1", a, ["a", "b"])
+    net.put_tensor("M2", b, ["a", "b"])
+    ab = net.launch()
+    assert ab.labels == ["i", "k"] and ab.rowrank == 1
+    assert np.allclose(ab.numpy(), np.ones((2, 2)) @ np.arange(4).reshape(2, 2))
+    net.put_tensor("M1", b, ["a", "b"])
+    net.put_tensor("M2", a, ["a", "b"])
+    assert np.allclose(net.launch().numpy(), np.arange(4).reshape(2, 2) @ np.ones((2, 2)))
+    assert a.labels == ["a", "b"]  # user tensors keep their labels
+    z0 = UniTensor.zeros([2, 2], labels=["a", "b"])
+    net.put_tensor("M1", z0)
+    assert net.launch().norm() == 0.0
+
+
+def test_launch_validation_messages(cuda):
+    net = Network(MATMUL)
+    net.put_tensor("M1", UniTensor.ones([2, 3], labels=["a", "b"]))
+    with pytest.raises(ValueError, match="M2"):
+        net.launch()
+    net.put_tensor("M2", UniTensor.ones([2, 2], labels=["a", "b"]))
+    with pytest.raises(ValueError, match="j"):
+        net.launch()
+    with pytest.raises(ValueError):
+        net.put_tensor("M9", UniTensor.ones([2, 2], labels=["a", "b"]))
+    with pytest.raises(ValueError):
+        net.put_tensor("M1", UniTensor.ones([2, 2], labels=["a", "b"]), ["a", "zz"])
+    u1 = Symmetry.u1()
+    bi = Bond(btype=IN, sectors=[(1, 1), (-1, 1)], syms=[u1])
+    s = UniTensor([bi, bi.redirect()], labels=["x", "y"])
+    net = Network(MATMUL)
+    net.put_tensor("M1", s, ["x", "y"])
+    net.put_tensor("M2", s, ["x", "y"])
+    net.launch()
+    net.put_tensor("M2", s, ["y", "x"])
+    with pytest.raises(ValueError, match="direction"):
+        net.launch()
+
+
+def test_optimal_order_recomputed_each_launch(cuda):
+    net = Network(THREE)
+    net.set_order(optimal=True)
+    net.put_tensor("M1", UniTensor.ones([2, 20], labels=["a", "b"]), ["a", "b"])
+    net.put_tensor("M2", UniTensor.ones([20, 20], labels=["a", "b"]), ["a", "b"])
+    net.put_tensor("M3", UniTensor.ones([20, 2], labels=["a", "b"]), ["a", "b"])
+    net.launch()
+    assert net.get_order() == "((M1,M2),M3)"
+    net.put_tensor("M1", UniTensor.ones([20, 20], labels=["a", "b"]), ["a", "b"])
+    net.launch()
+    assert net.get_order() == "((M2,M3),M1)"
+
+
+@pytest.mark.parametrize("chi,dtype", [(128, np.float64), (64, np.complex128)])
+def test_lawr_matvec_vs_oracle(cuda, chi, dtype):
+    """BASELINE config C1 (chi=128 f64) and a complex variant against the oracle."""
+    inp = oracle.lawr_inputs(chi, dtype=dtype, seed=31)
+    want, tree = oracle.launch(oracle.lawr_slots(), "b, q, b2", inp)
+    net = Network(oracle.LAWR_NET)
+    for nm, arr in inp.items():
+        t = UniTensor(storage.from_numpy(arr), labels=[f"{nm}{i}" for i in range(arr.ndim)])
+        net.put_tensor(nm, t, t.labels)
+    net.set_order(optimal=True)
+    out = net.launch()
+    assert net.get_order() == oracle.render_order(tree) == "(((A,L),W),R)"
+    assert rel_fro(out.numpy(), want) <= 1e-12
+
+
+def test_peps_small_vs_left_fold(cuda):
+    """PEPS reading A at small size: optimal launch equals a pairwise left fold."""
+    _, meta = load("network.npz")
+    lines = meta["cases"][4]["net"]
+    chi, D, d = 6, 3, 2
+    shp = {"C0": [chi, chi], "C1": [chi, chi], "C2": [chi, chi], "C3": [chi, chi],
+           "T0": [chi, D, D, chi], "T1": [chi, D, D, chi], "T2": [chi, D, D, chi], "T3": [chi, D, D, chi],
+           "a": [D, D, D, D, d], "a*": [D, D, D, D, d]}
+    net = Network(lines)
+    rel = []
+    for i, (nm, s) in enumerate(shp.items()):
+        t = UniTensor(storage.from_numpy(oracle.normal(s, seed=50 + i)), labels=[f"x{j}" for j in range(len(s))])
+        net.put_tensor(nm, t)
+    net.set_order(optimal=True)
+    val = net.launch().item()
+    net2 = Network(lines)
+    for nm in shp:
+        net2.put_tensor(nm, net._bindings[nm][0])
+    ref = net2.launch().item()  # appearance-order fold
+    assert abs(val - ref) <= 1e-10 * max(1.0, abs(ref))

@@ -1,0 +1,45 @@
+"""Small driver for ncu captures: one workload, a few iterations (dev aid)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+import numpy as np
+import torch
+
+import tnkit_np as oracle
+import paper_2401_01921_b200 as tnb
+from paper_2401_01921_b200 import Network, UniTensor, storage
+
+
+def lawr(chi, dt, iters):
+    inp = oracle.lawr_inputs(chi, dtype=dt, seed=3)
+    net = Network(oracle.LAWR_NET)
+    for nm, arr in inp.items():
+        t = UniTensor(storage.from_numpy(arr), labels=[f"{nm}{i}" for i in range(arr.ndim)])
+        net.put_tensor(nm, t, t.labels)
+    net.set_order(optimal=True)
+    for _ in range(iters):
+        net.launch()
+    torch.cuda.synchronize()
+
+
+def permute(shape, dt, perms, iters):
+    src = storage.uniform(list(shape), dtype=dt, seed=1)
+    for _ in range(iters):
+        for p in perms:
+            src.permute(*p).contiguous()
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    torch.cuda.set_device(0)
+    what = sys.argv[1]
+    if what == "lawr":
+        lawr(int(sys.argv[2]), np.complex128 if sys.argv[3] == "c128" else np.float64, int(sys.argv[4]))
+    elif what == "permute":
+        perms = [tuple(int(c) for c in p) for p in sys.argv[4].split(",")]
+        permute(tuple(int(x) for x in sys.argv[2].split("x")), np.complex128 if sys.argv[3] == "c128" else np.float64,
+                perms, int(sys.argv[5]))
+    print("done")
