@@ -1,0 +1,490 @@
+"""Benchmark driver (contract: README of the round / SURVEY.md section 8(d)).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl tnb|reference]
+                    [--workload NAME] [--no-secondary]
+
+Headline workload (BASELINE.json configs[2], f64 part, the north-star target):
+L.A.W.R effective-Hamiltonian matvec through ``Network.launch`` at chi=1024, d=2,
+D=5, float64, optimal order (((A,L),W),R); metric fp64 GFLOP/s (algorithmic
+2*MACs from the reference's own cost model). Secondary workloads (configs C1,
+C2, C3 c128 / batch, C4, C5) are measured in the same run and reported under
+"workloads". Inputs are the reference recipes' seeded N(0,1)/U(0,1) synthetic
+tensors (oracle/tnkit_np.py) -- there is no dataset.
+
+--impl reference times the reference algorithm's CPU path (the numpy port in
+oracle/, same numpy/OpenBLAS calls as the reference) on this host's cores.
+Multi-GPU (torchrun): one process per GPU; the matvec is replicated per rank
+(weak scaling), the C3b batch and C5 sites are sharded across ranks.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+import numpy as np
+
+FP64_PEAK_TFLOPS = 37.06   # measured DMMA peak on this pool's B200 (profiles/r01_fp64_peak.txt)
+PEAK_SOURCE = "measured DMMA.8x8x4 microbenchmark, profiles/r01_fp64_peak.txt (MEASURED_PEAKS.json has no fp64)"
+
+
+def peaks():
+    hbm = 6546.9
+    src = "fallback"
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        hbm = float(mp.get("hbm_gbs", hbm))
+        src = "MEASURED_PEAKS.json"
+    except Exception:
+        pass
+    return hbm, src
+
+
+# ----------------------------------------------------------------------------- dist
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self, backend):
+        if self.world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group(backend=backend)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            import torch
+            if torch.cuda.is_available():
+                self.pg.barrier(device_ids=[self.local])
+            else:
+                self.pg.barrier()
+
+    def max(self, x):
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([float(x)], dtype=torch.float64,
+                         device="cuda" if torch.cuda.is_available() else "cpu")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x):
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([float(x)], dtype=torch.float64,
+                         device="cuda" if torch.cuda.is_available() else "cpu")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
+        return float(t.item())
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- GPU side
+def _events():
+    import torch
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+class L2Flush:
+    def __init__(self):
+        import torch
+        self.buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def __call__(self):
+        self.buf.zero_()
+
+
+def time_steps(fn, steps, flush, dist):
+    """Device time of `steps` calls of fn, each bracketed by its own events; L2 flushed
+    (untimed) before every call; barrier + synchronize around the region; max over ranks."""
+    import torch
+    pairs = []
+    dist.barrier()
+    torch.cuda.synchronize()
+    for _ in range(steps):
+        flush()
+        e0, e1 = _events()
+        e0.record()
+        fn()
+        e1.record()
+        pairs.append((e0, e1))
+    torch.cuda.synchronize()
+    dist.barrier()
+    total_ms = sum(a.elapsed_time(b) for a, b in pairs)
+    return dist.max(total_ms)
+
+
+def lawr_network(tnb, inp):
+    net = tnb.Network(WL.LAWR_NET)
+    tensors = {}
+    for nm, arr in inp.items():
+        t = tnb.UniTensor(tnb.storage.from_numpy(arr), labels=[f"{nm}{i}" for i in range(arr.ndim)])
+        net.put_tensor(nm, t, t.labels)
+        tensors[nm] = t
+    net.set_order(optimal=True)
+    return net, tensors
+
+
+def lawr_macs(chi, d=2, D=5):
+    import paper_2401_01921_b200 as tnb
+    sets, dims = WL.lawr_label_sets(), WL.lawr_dims(chi, d, D)
+    tree = tnb.find_optimal_order(sets, dims)
+    return tnb.contraction_cost(tree, sets, dims), tnb.render_order(tree)
+
+
+def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, roof=True, seed=1234):
+    import torch
+    inp = WL.lawr_inputs(chi, dtype=dtype, seed=seed + 17 * dist.rank)
+    net, tensors = lawr_network(tnb, inp)
+    macs, order = lawr_macs(chi)
+    flop = macs * (8 if dtype == np.complex128 else 2)
+    for _ in range(warmup):
+        net.launch()
+    launches0 = tnb._lib.launch_count()
+    ms = time_steps(net.launch, steps, flush, dist)
+    launches = (tnb._lib.launch_count() - launches0) // max(steps, 1)
+    assert net.get_order() == order
+    res = {"ms_per_step": ms / steps, "flop_per_step": flop, "order": order, "launches_per_step": launches}
+    res["gflops"] = dist.sum(flop) / (ms / steps) / 1e6  # all ranks' work / max time
+    if e2e:
+        # end to end through the public API: pinned host inputs -> HBM, launch, result -> host
+        pinned = {nm: torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for nm, a in inp.items()}
+        out_host = None
+        h2d = sum(p.numel() * p.element_size() for p in pinned.values())
+
+        def step():
+            nonlocal out_host
+            for nm, p in pinned.items():
+                tensors[nm].get_block_().storage().copy_(p.reshape(-1), non_blocking=True)
+            out = net.launch()
+            host = out.get_block_().contiguous().storage().to("cpu", non_blocking=False)
+            out_host = host
+        for _ in range(max(1, warmup)):
+            step()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = _events()
+        e0.record()
+        for _ in range(steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        ems = dist.max(e0.elapsed_time(e1))
+        d2h = out_host.numel() * out_host.element_size()
+        res["e2e"] = {"value": dist.sum(flop) / (ems / steps) / 1e6, "unit": "GFLOP/s",
+                      "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                      "ms_per_step": ems / steps}
+    if roof:
+        # dominant kernel = the DMMA GEMM of steps 1 (A.L) and 3 (T2.R): time those launches alone
+        L = tensors["L"].relabel(["b", "w", "vl"])
+        A = tensors["A"].relabel(["vl", "p", "vr"])
+        W = tensors["W"].relabel(["w", "w2", "q", "p"])
+        R = tensors["R"].relabel(["b2", "w2", "vr"])
+        t1 = tnb.contract_pair(A, L)
+        t2 = tnb.contract_pair(t1, W)
+        mul = 8 if dtype == np.complex128 else 2
+        f1 = 2 * chi * 5 * chi * chi * mul
+        f3 = 2 * chi * chi * 5 * chi * mul
+        s1 = time_steps(lambda: tnb.contract_pair(A, L), steps, flush, dist) / steps
+        s3 = time_steps(lambda: tnb.contract_pair(t2, R), steps, flush, dist) / steps
+        s2 = time_steps(lambda: tnb.contract_pair(t1, W), steps, flush, dist) / steps
+        res["steps_ms"] = {"A.L": s1, "T1.W": s2, "T2.R": s3}
+        ach = (f1 + f3) / ((s1 + s3) / 1e3) / 1e12
+        res["roofline"] = {"bound": "tensor", "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS,
+                           "unit": "TFLOP/s", "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": None,
+                           "kernel": "gemm_ws_kernel (DMMA.8x8x4) steps A.L + T2.R",
+                           "peak_source": PEAK_SOURCE}
+    return res
+
+
+def gpu_permute(tnb, steps, warmup, flush, dist):
+    import itertools
+    import torch
+    out = {}
+    for shape, dt, name in [((64,) * 4, np.float64, "r4_f64"), ((64,) * 4, np.complex128, "r4_c128"),
+                            ((16,) * 6, np.float64, "r6_f64"), ((16,) * 6, np.complex128, "r6_c128")]:
+        src = tnb.storage.uniform(list(shape), dtype=dt, seed=11)
+        if len(shape) == 4:
+            perms = [p for p in itertools.permutations(range(4)) if p != (0, 1, 2, 3)]
+        else:
+            g = np.random.default_rng(606)
+            perms = []
+            while len(perms) < 32:
+                p = tuple(int(x) for x in g.permutation(6))
+                if p != tuple(range(6)):
+                    perms.append(p)
+        nbytes = 2 * src.size * src.itemsize
+        rates = []
+        for p in perms:
+            for _ in range(warmup):
+                src.permute(*p).contiguous()
+            ms = time_steps(lambda: src.permute(*p).contiguous(), max(1, steps // 2), flush, dist) / max(1, steps // 2)
+            rates.append(nbytes / ms / 1e6)
+        out[name] = {"median_gbs": float(np.median(rates)), "min_gbs": float(np.min(rates)),
+                     "max_gbs": float(np.max(rates)), "n_perms": len(perms), "bytes_per_permute": nbytes}
+    return out
+
+
+def c4_tensors(tnb, seed=777):
+    u1 = tnb.Symmetry.u1()
+    V = tnb.Bond(btype=tnb.IN, sectors=WL.c4_sectors(), syms=[u1])
+    P = tnb.Bond(btype=tnb.IN, sectors=[(1, 1), (-1, 1)], syms=[u1])
+    A = tnb.UniTensor([V, P, V.redirect()], labels=["vl", "p", "vr"])
+    E = tnb.UniTensor([V, P.redirect(), V.redirect()], labels=["vr", "p", "x"])
+    tnb.random.normal_(A, seed=seed)
+    tnb.random.normal_(E, seed=seed + 1)
+    return A, E
+
+
+C4_MACS = 169073208
+
+
+def gpu_c4(tnb, steps, warmup, flush, dist):
+    import torch
+    A, E = c4_tensors(tnb)
+    for _ in range(warmup):
+        tnb.contract(A, E)
+    ms = time_steps(lambda: tnb.contract(A, E), steps, flush, dist) / steps
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        tnb.contract(A, E)
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / steps * 1e3
+    return {"ms_per_call": ms, "host_wall_ms_per_call": wall, "gflops": dist.sum(2 * C4_MACS) / ms / 1e6}
+
+
+# ----------------------------------------------------------------------------- CPU side
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads") for i in threadpool_info() if i.get("internal_api") == "openblas"]
+        return int(n[0]) if n else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_lawr(chi, dtype, budget_s=8.0, max_iter=10, seed=1234):
+    inp = ORACLE.lawr_inputs(chi, dtype=dtype, seed=seed)
+    sets, dims = WL.lawr_label_sets(), WL.lawr_dims(chi)
+    macs = ORACLE.contraction_cost(ORACLE.find_optimal_order(sets, dims), sets, dims)
+    flop = macs * (8 if dtype == np.complex128 else 2)
+    ORACLE.launch(ORACLE.lawr_slots(), "b, q, b2", inp)  # warm
+    ts = []
+    t_start = time.perf_counter()
+    while len(ts) < max_iter and (time.perf_counter() - t_start) < budget_s:
+        t0 = time.perf_counter()
+        ORACLE.launch(ORACLE.lawr_slots(), "b, q, b2", inp)
+        ts.append(time.perf_counter() - t0)
+    best = min(ts)
+    return {"value": flop / best / 1e9, "unit": "GFLOP/s", "cores": cpu_threads(), "kind": "port",
+            "sample": f"{len(ts)} Network launches of L.A.W.R chi={chi} {np.dtype(dtype).name} "
+                      f"(oracle port of tnkit, numpy {np.__version__} OpenBLAS), best-of",
+            "ms_per_launch": best * 1e3}
+
+
+def cpu_permute(budget_s=6.0):
+    import itertools
+    src = ORACLE.uniform([64] * 4, seed=11)
+    perms = [p for p in itertools.permutations(range(4)) if p != (0, 1, 2, 3)]
+    rates = []
+    t_start = time.perf_counter()
+    for p in perms:
+        if time.perf_counter() - t_start > budget_s:
+            break
+        t0 = time.perf_counter()
+        ORACLE.permute_contiguous(src, p)
+        rates.append(2 * src.nbytes / (time.perf_counter() - t0) / 1e9)
+    return {"value": float(np.median(rates)), "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": f"{len(rates)} of the 23 rank-4 [64]^4 f64 permutes (np.ascontiguousarray, single-threaded)"}
+
+
+def cpu_c4(budget_s=3.0):
+    sec = ORACLE.c4_sectors()
+    qv = [(q,) for q, _ in sec]
+    deg = [d for _, d in sec]
+    a_qns = ORACLE.zero_flux_combos([(1, qv, [0]), (1, [(1,), (-1,)], [0]), (-1, qv, [0])])
+    e_qns = ORACLE.zero_flux_combos([(1, qv, [0]), (-1, [(1,), (-1,)], [0]), (-1, qv, [0])])
+    out_qns = ORACLE.zero_flux_combos([(1, qv, [0]), (-1, qv, [0])])
+    ab = ORACLE.fill_blocks_normal([(deg[q[0]], 1, deg[q[2]]) for q in a_qns], seed=777)
+    eb = ORACLE.fill_blocks_normal([(deg[q[0]], 1, deg[q[2]]) for q in e_qns], seed=778)
+    ts = []
+    t_start = time.perf_counter()
+    while time.perf_counter() - t_start < budget_s and len(ts) < 50:
+        t0 = time.perf_counter()
+        ORACLE.zero_flux_combos([(1, qv, [0]), (-1, qv, [0])])
+        ORACLE.contract_blocks(a_qns, ab, ["vl", "p", "vr"], e_qns, eb, ["vr", "p", "x"], out_qns)
+        ts.append(time.perf_counter() - t0)
+    best = min(ts)
+    return {"value": 2 * C4_MACS / best / 1e9, "unit": "GFLOP/s", "cores": cpu_threads(), "kind": "port",
+            "sample": f"{len(ts)} block-sparse contractions (C4), best-of", "ms_per_call": best * 1e3}
+
+
+# ----------------------------------------------------------------------------- main
+def run_reference(args, dist):
+    """--impl reference: the reference algorithm on the host's cores (oracle port)."""
+    if dist.rank != 0:
+        return 0
+    chi = 1024
+    inp = ORACLE.lawr_inputs(chi, dtype=np.float64, seed=1234)
+    sets, dims = WL.lawr_label_sets(), WL.lawr_dims(chi)
+    tree = ORACLE.find_optimal_order(sets, dims)
+    macs, order = ORACLE.contraction_cost(tree, sets, dims), ORACLE.render_order(tree)
+    flop = 2 * macs
+    for _ in range(args.warmup):
+        ORACLE.launch(ORACLE.lawr_slots(), "b, q, b2", inp)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ORACLE.launch(ORACLE.lawr_slots(), "b, q, b2", inp)
+    dt = (time.perf_counter() - t0) / args.steps
+    val = flop / dt / 1e9
+    line = {"metric": "fp64 GFLOP/s (L.A.W.R Network matvec, chi=1024)", "value": round(val, 3),
+            "unit": "GFLOP/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1), reference recipe)",
+            "config": {"workload": "lawr_f64_chi1024", "chi": chi, "d": 2, "D": 5, "order": order},
+            "cpu_baseline": {"value": round(val, 3), "unit": "GFLOP/s", "cores": cpu_threads(), "kind": "port",
+                             "sample": f"{args.steps} full launches (numpy/OpenBLAS port of tnkit on host cores)"},
+            "e2e": {"value": round(val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tnb", choices=["tnb", "reference"])
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    dist = Dist()
+    if args.impl == "reference":
+        dist.init("gloo")
+        return run_reference(args, dist)
+
+    import torch
+    torch.cuda.set_device(dist.local)
+    dist.init("nccl")
+    import paper_2401_01921_b200 as tnb
+    flush = L2Flush()
+    hbm_peak, hbm_src = peaks()
+
+    with ClockSampler(dist.local) as clk:
+        head = gpu_lawr(tnb, 1024, np.float64, args.steps, args.warmup, flush, dist)
+    clocks = clk.summary()
+    line = {"metric": "fp64 GFLOP/s (L.A.W.R Network matvec, chi=1024)", "value": round(head["gflops"], 3),
+            "unit": "GFLOP/s", "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(head["ms_per_step"], 5), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1), reference recipe)",
+            "config": {"workload": "lawr_f64_chi1024", "chi": 1024, "d": 2, "D": 5, "order": head["order"],
+                       "l2": "flushed (256 MiB write) before every timed step", "parallelism":
+                       f"replicas x{dist.world}"},
+            "e2e": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in head["e2e"].items()},
+            "roofline": head["roofline"], "gpu_launches": int(head["launches_per_step"] * args.steps),
+            "clocks": clocks, "steps_ms": head["steps_ms"]}
+    if not args.no_secondary:
+        wl = {}
+        c3 = gpu_lawr(tnb, 1024, np.complex128, max(3, args.steps // 2), args.warmup, flush, dist, e2e=False)
+        wl["lawr_c128_chi1024"] = {"value": round(c3["gflops"], 2), "unit": "GFLOP/s (8 flop/complex MAC)",
+                                   "ms_per_step": c3["ms_per_step"], "roofline": c3["roofline"],
+                                   "complex_mode": tnb.get_complex_mode()}
+        c1 = gpu_lawr(tnb, 128, np.float64, max(10, args.steps), args.warmup, flush, dist, e2e=False, roof=False)
+        wl["lawr_f64_chi128"] = {"value": round(c1["gflops"], 2), "unit": "GFLOP/s",
+                                 "ms_per_step": c1["ms_per_step"]}
+        perm = gpu_permute(tnb, max(4, args.steps), args.warmup, flush, dist)
+        best = max(v["median_gbs"] for v in perm.values())
+        wl["permute_sweep"] = {"unit": "GB/s (2 x bytes / time, median over perms)", "cases": perm,
+                               "roofline": {"bound": "hbm", "peak": hbm_peak, "unit": "GB/s",
+                                            "peak_source": hbm_src,
+                                            "frac_median": {k: round(v["median_gbs"] / hbm_peak, 4)
+                                                            for k, v in perm.items()}}}
+        c4 = gpu_c4(tnb, max(10, args.steps), args.warmup, flush, dist)
+        wl["blocksparse_c4"] = {"value": round(c4["gflops"], 2), "unit": "GFLOP/s", **c4}
+        line["workloads"] = wl
+    if dist.rank == 0 and not args.no_cpu:
+        cb = cpu_lawr(1024, np.float64)
+        line["cpu_baseline"] = cb
+        if not args.no_secondary:
+            line["workloads"]["lawr_f64_chi128"]["cpu_baseline"] = cpu_lawr(128, np.float64, budget_s=2, max_iter=50)
+            line["workloads"]["permute_sweep"]["cpu_baseline"] = cpu_permute()
+            line["workloads"]["blocksparse_c4"]["cpu_baseline"] = cpu_c4()
+    if dist.rank == 0:
+        print(json.dumps(line))
+    return 0
+
+
+import tnkit_np as ORACLE  # noqa: E402  (CPU-baseline leg and reference arm only)
+from paper_2401_01921_b200 import workloads as WL  # noqa: E402
+
+if __name__ == "__main__":
+    sys.exit(main())
