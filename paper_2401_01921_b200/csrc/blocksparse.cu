@@ -155,7 +155,7 @@ template <int MODE>
 struct BsCfg<true, MODE> { using Core = TileCore<true, MODE, 64, 64, 8, 2, 2, 3>; };
 
 template <bool CPLX, int MODE>
-__global__ void __launch_bounds__(128, 2) bs_gemm_kernel(const BsMeta m) {
+__global__ void __launch_bounds__(128, 2) bs_gemm_kernel(const __grid_constant__ BsMeta m) {
   using Core = typename BsCfg<CPLX, MODE>::Core;
   using T = typename Core::T;
   extern __shared__ __align__(16) unsigned char smem[];

@@ -24,7 +24,7 @@
 #include <cstring>
 #include <vector>
 
-#include "gemm_core.cuh"
+#include "gemm_sk.cuh"
 
 namespace tnb {
 
@@ -33,21 +33,13 @@ int permute_device(const void* src, void* dst, int es, int rank, const int64_t* 
 
 namespace {
 
-struct GemmDesc {
-  int M, N, K;
-  int tiles_m, tiles_n, splitk;
-  int k_per_split;  // multiple of BK
-  int a_mfast, b_nfast;
-  int out_ld;       // = N
-  KAffine kaff;
-  Group rowA, kA, kB, colB;
-};
+
 
 // Warp-specialised dense tile GEMM (producer warpgroup + DMMA warps).
 template <bool CPLX, int MODE, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
 __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32 + 128, 1)
     gemm_ws_kernel(const typename Elem<CPLX>::T* __restrict__ A, const typename Elem<CPLX>::T* __restrict__ B,
-                   typename Elem<CPLX>::T* __restrict__ C, const GemmDesc d) {
+                   typename Elem<CPLX>::T* __restrict__ C, const __grid_constant__ GemmDesc d) {
   using Core = TileCoreWS<CPLX, MODE, BM, BN, BK, WARPS_M, WARPS_N, STAGES, 0, 0>;
   extern __shared__ __align__(16) unsigned char smem[];
   int bid = blockIdx.x;
@@ -69,9 +61,25 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32 + 128, 1)
   const int kend = min(d.K, kbeg + d.k_per_split);
   typename Core::Acc acc;
   Core::zero(acc);
-  if (Core::run(smem, A, B, d.rowA, d.kA, d.kB, d.colB, m0, n0, d.M, d.N, kbeg, kend, d.a_mfast != 0,
-                d.b_nfast != 0, d.kaff, acc))
+  bool math;
+  if (d.a_mfast) {
+    if (d.b_nfast) math = Core::template run<true, true>(smem, A, B, d.rowA, d.kA, d.kB, d.colB, m0, n0, d.M, d.N, kbeg, kend, d.kaff, acc);
+    else math = Core::template run<true, false>(smem, A, B, d.rowA, d.kA, d.kB, d.colB, m0, n0, d.M, d.N, kbeg, kend, d.kaff, acc);
+  } else {
+    if (d.b_nfast) math = Core::template run<false, true>(smem, A, B, d.rowA, d.kA, d.kB, d.colB, m0, n0, d.M, d.N, kbeg, kend, d.kaff, acc);
+    else math = Core::template run<false, false>(smem, A, B, d.rowA, d.kA, d.kB, d.colB, m0, n0, d.M, d.N, kbeg, kend, d.kaff, acc);
+  }
+  if (math)
     Core::store(C + (size_t)split * (size_t)d.M * (size_t)d.out_ld, d.out_ld, m0, n0, d.M, d.N, acc);
+}
+
+// Persistent stream-K warp-specialised GEMM (SKCore): the dense contraction path.
+template <bool CPLX, int MODE, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool AMF, bool BNF>
+__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32 + 128, 1)
+    gemm_sk_kernel(const typename Elem<CPLX>::T* __restrict__ A, const typename Elem<CPLX>::T* __restrict__ B,
+                   typename Elem<CPLX>::T* __restrict__ C, const __grid_constant__ GemmDesc d, const SKParams sk) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  SKCore<CPLX, MODE, BM, BN, BK, WARPS_M, WARPS_N, STAGES>::template run<AMF, BNF>(smem, A, B, C, d, sk);
 }
 
 // Dense tile GEMM: one CTA per (tile, K split); tile raster in groups of 8
@@ -79,7 +87,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32 + 128, 1)
 template <bool CPLX, int MODE, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB>
 __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
     gemm_kernel(const typename Elem<CPLX>::T* __restrict__ A, const typename Elem<CPLX>::T* __restrict__ B,
-                typename Elem<CPLX>::T* __restrict__ C, const GemmDesc d) {
+                typename Elem<CPLX>::T* __restrict__ C, const __grid_constant__ GemmDesc d) {
   using Core = TileCore<CPLX, MODE, BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
   extern __shared__ __align__(16) unsigned char smem[];
   int bid = blockIdx.x;
@@ -137,7 +145,7 @@ __global__ void splitk_reduce_kernel(const typename Elem<CPLX>::T* __restrict__ 
 template <bool CPLX>
 __global__ void __launch_bounds__(256) skinny_kernel(const typename Elem<CPLX>::T* __restrict__ A,
                                                      const typename Elem<CPLX>::T* __restrict__ B,
-                                                     typename Elem<CPLX>::T* __restrict__ C, const GemmDesc d) {
+                                                     typename Elem<CPLX>::T* __restrict__ C, const __grid_constant__ GemmDesc d) {
   using T = typename Elem<CPLX>::T;
   constexpr int RM = 128;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -346,6 +354,52 @@ struct Tiled {
   }
 };
 
+// Host side of the stream-K kernel: one CTA per SM, workspace for split tiles.
+template <bool CPLX, int MODE, int BM, int BN, int BK, int WM, int WN, int ST>
+struct StreamK {
+  using Core = SKCore<CPLX, MODE, BM, BN, BK, WM, WN, ST>;
+  using T = typename Elem<CPLX>::T;
+  template <bool AMF, bool BNF>
+  static int launch_one(const void* A, const void* B, void* C, const GemmDesc& d, const SKParams& sk, cudaStream_t st) {
+    auto kern = gemm_sk_kernel<CPLX, MODE, BM, BN, BK, WM, WN, ST, AMF, BNF>;
+    static bool configured = false;
+    if (!configured) {
+      TNB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Core::kSmem));
+      configured = true;
+    }
+    kern<<<sk.G, Core::NT, Core::kSmem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B), static_cast<T*>(C),
+                                              d, sk);
+    count_launch();
+    TNB_CUDA_CHECK(cudaGetLastError());
+    return TNB_OK;
+  }
+  static int run(const void* A, const void* B, void* C, GemmDesc d, cudaStream_t st) {
+    d.tiles_m = (d.M + BM - 1) / BM;
+    d.tiles_n = (d.N + BN - 1) / BN;
+    d.splitk = 1;
+    SKParams sk;
+    sk.KT = (d.K + BK - 1) / BK;
+    sk.total = (int64_t)d.tiles_m * d.tiles_n * sk.KT;
+    if ((int64_t)d.tiles_m * d.tiles_n >= (1ll << 31)) return fail(TNB_EUNSUP, "contract: too many tiles");
+    // >= 4 k-tiles per CTA: tiny problems do not pay for many partial hand-offs
+    sk.G = (int)std::max<int64_t>(1, std::min<int64_t>(sk.total / 4, sms()));
+    size_t ws_bytes = (size_t)sk.G * Core::ACCN * Core::NMATH * 8;
+    void* mem = nullptr;
+    TNB_CUDA_CHECK(cudaMallocAsync(&mem, ws_bytes + (size_t)sk.G * 4 + 64, st));
+    sk.ws = static_cast<double*>(mem);
+    sk.flags = reinterpret_cast<int*>(static_cast<char*>(mem) + ws_bytes);
+    cudaError_t e = cudaMemsetAsync(sk.flags, 0, (size_t)sk.G * 4, st);
+    int rc = TNB_OK;
+    if (e != cudaSuccess) rc = cuda_fail(e, "contract: workspace memset");
+    else if (d.a_mfast && d.b_nfast) rc = launch_one<true, true>(A, B, C, d, sk, st);
+    else if (d.a_mfast) rc = launch_one<true, false>(A, B, C, d, sk, st);
+    else if (d.b_nfast) rc = launch_one<false, true>(A, B, C, d, sk, st);
+    else rc = launch_one<false, false>(A, B, C, d, sk, st);
+    cudaFreeAsync(mem, st);
+    return rc;
+  }
+};
+
 template <bool CPLX>
 size_t skinny_smem(const GemmDesc& d);
 
@@ -377,21 +431,9 @@ template <bool CPLX, int MODE>
 int dispatch(const void* A, const void* B, void* C, GemmDesc& d, cudaStream_t st) {
   if (d.N <= 64 && d.K <= 64 && d.M >= 4096 && skinny_smem<CPLX>(d) <= 160 * 1024)
     return run_skinny<CPLX>(A, B, C, d, st);
-  if constexpr (!CPLX) {
-    using Big = Tiled<false, 0, 128, 128, 16, 4, 4, 4, 1, 1>;
-    using Small = Tiled<false, 0, 64, 64, 16, 2, 2, 3, 2>;
-    int sb = 1, ss = 1;
-    double tb = Big::plan(d, sb, 1.0), ts = Small::plan(d, ss, 1.15);
-    if (tb <= ts) return Big::run(A, B, C, d, sb, st);
-    return Small::run(A, B, C, d, ss, st);
-  } else {
-    using Big = Tiled<true, MODE, 64, (MODE == 1 ? 64 : 128), 8, 4, 4, 4, 1, 1>;
-    using Small = Tiled<true, MODE, 64, 64, 8, 2, 2, 3, 2>;
-    int sb = 1, ss = 1;
-    double tb = Big::plan(d, sb, 1.0), ts = Small::plan(d, ss, 1.1);
-    if (tb <= ts) return Big::run(A, B, C, d, sb, st);
-    return Small::run(A, B, C, d, ss, st);
-  }
+  if constexpr (!CPLX) return StreamK<false, 0, 128, 128, 16, 4, 4, 4>::run(A, B, C, d, st);
+  else if constexpr (MODE == 0) return StreamK<true, 0, 64, 128, 8, 4, 4, 4>::run(A, B, C, d, st);
+  else return StreamK<true, 1, 64, 64, 8, 4, 4, 4>::run(A, B, C, d, st);
 }
 
 // f64 -> c128 widening (mixed-dtype contraction promotes like np.result_type)

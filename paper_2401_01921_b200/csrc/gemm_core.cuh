@@ -359,10 +359,12 @@ struct TileCoreWS {
   __device__ static void zero(Acc& acc) { TileCore<CPLX, MODE, BM, BN, BK, WARPS_M, WARPS_N, STAGES>::zero(acc); }
 
   // Returns true in math threads (acc valid); producers return false after the last stage.
+  // AMF / BNF: operand A is M-fast (else K-fast), operand B is N-fast (else K-fast).
+  template <bool AMF, bool BNF>
   __device__ static bool run(unsigned char* smem, const T* __restrict__ A, const T* __restrict__ B,
                              const Group& rowA, const Group& kA, const Group& kB, const Group& colB, int m0, int n0,
-                             int M, int N, int kbeg, int kend, bool a_mfast, bool b_nfast, const KAffine& kaff,
-                             Acc& acc) {
+                             int M, int N, int kbeg, int kend, const KAffine& kaff, Acc& acc) {
+    constexpr bool a_mfast = AMF, b_nfast = BNF;
     T* As = reinterpret_cast<T*>(smem);
     T* Bs = As + STAGES * BK * LDA;
     int64_t* rowOffA = reinterpret_cast<int64_t*>(Bs + STAGES * BK * LDB);
@@ -388,61 +390,110 @@ struct TileCoreWS {
       for (int i = p; i < BM; i += NPROD) rowOffA[i] = (m0 + i < M) ? group_offset(rowA, m0 + i) : -1;
       for (int i = p; i < BN; i += NPROD) colOffB[i] = (n0 + i < N) ? group_offset(colB, n0 + i) : -1;
       detail::named_sync(1, NPROD);
+      constexpr int EA = (BM * BK) / NPROD, EB = (BN * BK) / NPROD;
+      // element e of this thread -> (row, kk) of the tile (same mapping for every k-tile)
+      auto mapA = [&](int i, int& m, int& kk) {
+        const int e = p + i * NPROD;
+        if (a_mfast) { m = e % BM; kk = e / BM; }
+        else { kk = (e & 3) + 4 * (e / (4 * BM)); m = (e >> 2) % BM; }
+      };
+      auto mapB = [&](int i, int& n, int& kk) {
+        const int e = p + i * NPROD;
+        if (b_nfast) { n = e % BN; kk = e / BN; }
+        else { kk = (e & 3) + 4 * (e / (4 * BN)); n = (e >> 2) % BN; }
+      };
+      // affine fast path: per-element offsets rowOff + kk*ks live in registers for the
+      // whole tile; per k-tile one group_offset per operand and one 64-bit add per element
+      const bool all_affine = kaff.ok && ((kend - kbeg) % BK == 0);
+      if (all_affine) {
+        // distinct rows / cols touched by this thread (compile-time structure of the
+        // mapping): M-fast -> one row, K-fast -> 4 rows (one per i % 4)
+        constexpr int RA = AMF ? 1 : 4, RB = BNF ? 1 : 4;
+        int64_t rA[RA], rB[RB];
+#pragma unroll
+        for (int j = 0; j < RA; ++j) {
+          int m, kk;
+          mapA(j, m, kk);
+          rA[j] = rowOffA[m];
+        }
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+          int n, kk;
+          mapB(j, n, kk);
+          rB[j] = colOffB[n];
+        }
+        const uint32_t sAbase = smem_u32(As), sBbase = smem_u32(Bs);
+        constexpr uint32_t stA = BK * LDA * ES, stB = BK * LDB * ES;
+        for (int kt = 0; kt < KT; ++kt) {
+          const int s = kt % STAGES;
+          const int k0 = kbeg + kt * BK;
+          const T* pa = A + group_offset(kA, k0);
+          const T* pb = B + group_offset(kB, k0);
+          if (kt >= STAGES) detail::mbar_wait(&empty[s], ((kt / STAGES) & 1) ^ 1);
+#pragma unroll
+          for (int i = 0; i < EA; ++i) {
+            int m, kk;
+            mapA(i, m, kk);
+            const int64_t ro = rA[i % RA];
+            const bool v = ro >= 0;
+            const T* src = v ? pa + ro + (int64_t)kk * kaff.ksA : A;
+            const uint32_t dst = sAbase + s * stA + (uint32_t)(kk * LDA + m) * ES;
+            if constexpr (CPLX)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
+            else
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0));
+          }
+#pragma unroll
+          for (int i = 0; i < EB; ++i) {
+            int n, kk;
+            mapB(i, n, kk);
+            const int64_t co = rB[i % RB];
+            const bool v = co >= 0;
+            const T* src = v ? pb + co + (int64_t)kk * kaff.ksB : B;
+            const uint32_t dst = sBbase + s * stB + (uint32_t)(kk * LDB + n) * ES;
+            if constexpr (CPLX)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
+            else
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0));
+          }
+          detail::cp_async_mbar_arrive_noinc(&full[s]);
+        }
+        cp_async_wait<0>();
+        return false;
+      }
       for (int kt = 0; kt < KT; ++kt) {
         const int s = kt % STAGES;
         const int k0 = kbeg + kt * BK;
-        int64_t baseA = 0, baseB = 0;
         const int64_t* ka = kOffA + (kt & 1) * BK;
         const int64_t* kb = kOffB + (kt & 1) * BK;
-        const bool full_tile = (k0 + BK <= kend);
-        const bool affine = kaff.ok && full_tile;
-        if (affine) {
-          baseA = group_offset(kA, k0);
-          baseB = group_offset(kB, k0);
-        } else {
-          // per-k offsets for this tile in a producer-private double buffer
-          for (int i = p; i < 2 * BK; i += NPROD) {
-            const int kk = i % BK, k = k0 + kk;
-            const bool v = k < kend;
-            if (i < BK) kOffA[(kt & 1) * BK + kk] = v ? group_offset(kA, k) : -1;
-            else kOffB[(kt & 1) * BK + kk] = v ? group_offset(kB, k) : -1;
-          }
-          detail::named_sync(1, NPROD);
+        // per-k offsets for this tile in a producer-private double buffer
+        for (int i = p; i < 2 * BK; i += NPROD) {
+          const int kk = i % BK, k = k0 + kk;
+          const bool v = k < kend;
+          if (i < BK) kOffA[(kt & 1) * BK + kk] = v ? group_offset(kA, k) : -1;
+          else kOffB[(kt & 1) * BK + kk] = v ? group_offset(kB, k) : -1;
         }
+        detail::named_sync(1, NPROD);
         if (kt >= STAGES) detail::mbar_wait(&empty[s], ((kt / STAGES) & 1) ^ 1);
         T* as = As + s * BK * LDA;
         T* bs = Bs + s * BK * LDB;
 #pragma unroll
-        for (int i = 0; i < (BM * BK) / NPROD; ++i) {
-          const int e = p + i * NPROD;
+        for (int i = 0; i < EA; ++i) {
           int m, kk;
-          if (a_mfast) {
-            m = e % BM;
-            kk = e / BM;
-          } else {
-            kk = (e & 3) + 4 * (e / (4 * BM));
-            m = (e >> 2) % BM;
-          }
+          mapA(i, m, kk);
           const int64_t ro = rowOffA[m];
-          const int64_t ko = affine ? baseA + kk * kaff.ksA : ka[kk];
+          const int64_t ko = ka[kk];
           const bool v = (ro >= 0) && (ko >= 0);
           const T* src = v ? (A + ro + ko) : A;
           if constexpr (CPLX) cp_async16(as + kk * LDA + m, src, v);
           else cp_async8(as + kk * LDA + m, src, v);
         }
 #pragma unroll
-        for (int i = 0; i < (BN * BK) / NPROD; ++i) {
-          const int e = p + i * NPROD;
+        for (int i = 0; i < EB; ++i) {
           int n, kk;
-          if (b_nfast) {
-            n = e % BN;
-            kk = e / BN;
-          } else {
-            kk = (e & 3) + 4 * (e / (4 * BN));
-            n = (e >> 2) % BN;
-          }
+          mapB(i, n, kk);
           const int64_t co = colOffB[n];
-          const int64_t ko = affine ? baseB + kk * kaff.ksB : kb[kk];
+          const int64_t ko = kb[kk];
           const bool v = (co >= 0) && (ko >= 0);
           const T* src = v ? (B + co + ko) : B;
           if constexpr (CPLX) cp_async16(bs + kk * LDB + n, src, v);

@@ -1,0 +1,347 @@
+// Persistent, warp-specialised, stream-K FP64 DMMA GEMM core (the dense
+// contraction hot loop, a11).
+//
+//  * one CTA per SM; CTA c owns the contiguous k-iteration range
+//    [total*c/G, total*(c+1)/G) of the flattened (tile, k-tile) space, so every SM
+//    gets the same amount of DMMA work whatever the tile count (no wave
+//    quantisation, no split-K reduce pass);
+//  * a producer warpgroup (4 warps) gathers operands for consecutive k-tiles --
+//    across tile boundaries -- into a STAGES-deep ring (cp.async + "full"
+//    mbarriers); 16 math warps (32x32 warp tiles of DMMA.8x8x4) consume and
+//    release stages through "empty" mbarriers; no CTA-wide barrier in the loop;
+//  * a tile split between CTAs is finished by the CTA that computes its last
+//    k-tile ("owner"); earlier CTAs publish register partials to a workspace slot
+//    and a flag; the owner adds them in CTA order (deterministic, no atomics on
+//    data). All G CTAs are co-resident, so the owner's wait always completes.
+#pragma once
+#include "gemm_core.cuh"
+
+namespace tnb {
+
+struct GemmDesc {
+  int M, N, K;
+  int tiles_m, tiles_n, splitk;
+  int k_per_split;
+  int a_mfast, b_nfast;
+  int out_ld;
+  KAffine kaff;
+  Group rowA, kA, kB, colB;
+};
+
+struct SKParams {
+  int KT;          // k-tiles per output tile
+  int G;           // persistent CTAs
+  int64_t total;   // tiles * KT
+  double* ws;      // [G][ACCN][NMATH] register partials
+  int* flags;      // [G], zeroed before the launch
+};
+
+namespace detail {
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__host__ __device__ __forceinline__ int64_t sk_begin(int64_t total, int G, int c) { return total * c / G; }
+__device__ __forceinline__ int sk_cta_of(int64_t total, int G, int64_t x) {
+  int c = (int)((x * G) / total);
+  while (c + 1 < G && sk_begin(total, G, c + 1) <= x) ++c;
+  while (c > 0 && sk_begin(total, G, c) > x) --c;
+  return c;
+}
+}  // namespace detail
+
+template <bool CPLX, int MODE, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
+struct SKCore {
+  using T = typename Elem<CPLX>::T;
+  using Base = TileCore<CPLX, MODE, BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
+  static constexpr int ES = CPLX ? 16 : 8;
+  static constexpr int NMATH = WARPS_M * WARPS_N * 32;
+  static constexpr int NPROD = 128;
+  static constexpr int NT = NMATH + NPROD;
+  static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
+  static constexpr int MF = WTM / 8, NF = WTN / 8;
+  static constexpr int LDA = BM + (CPLX ? 2 : 4);
+  static constexpr int LDB = BN + (CPLX ? 2 : 4);
+  static constexpr int NACC = CPLX ? (MODE == 1 ? 3 : 2) : 1;
+  static constexpr int ACCN = NACC * MF * NF * 2;
+  static constexpr int EA = (BM * BK) / NPROD, EB = (BN * BK) / NPROD;
+  static constexpr size_t kSmem = (size_t)STAGES * BK * (LDA + LDB) * ES + (size_t)(BM + BN) * 8 +
+                                  (size_t)2 * 2 * BK * 8 + (size_t)2 * STAGES * 8;
+  static_assert(NMATH % 128 == 0, "math warps must form whole warpgroups");
+  static_assert((BM * BK) % NPROD == 0 && (BN * BK) % NPROD == 0, "tile/producer mismatch");
+  using Acc = typename Base::Acc;
+
+  __device__ static void tile_coords(const GemmDesc& d, int64_t tile, int& m0, int& n0) {
+    const int group = 8;
+    const int per_group = group * d.tiles_n;
+    const int t = (int)tile;
+    const int g = t / per_group;
+    const int first_m = g * group;
+    const int gsz = min(d.tiles_m - first_m, group);
+    const int in_g = t - g * per_group;
+    m0 = (first_m + in_g % gsz) * BM;
+    n0 = (in_g / gsz) * BN;
+  }
+
+  template <bool AMF, bool BNF>
+  __device__ static void run(unsigned char* smem, const T* __restrict__ A, const T* __restrict__ B,
+                             T* __restrict__ C, const GemmDesc& d, const SKParams& sk) {
+    T* As = reinterpret_cast<T*>(smem);
+    T* Bs = As + STAGES * BK * LDA;
+    int64_t* rowOffA = reinterpret_cast<int64_t*>(Bs + STAGES * BK * LDB);
+    int64_t* colOffB = rowOffA + BM;
+    int64_t* kOffA = colOffB + BN;    // [2][BK]
+    int64_t* kOffB = kOffA + 2 * BK;  // [2][BK]
+    uint64_t* full = reinterpret_cast<uint64_t*>(kOffB + 2 * BK);
+    uint64_t* empty = full + STAGES;
+    const int tid = threadIdx.x;
+    const int c = blockIdx.x;
+    const int64_t it0 = detail::sk_begin(sk.total, sk.G, c), it1 = detail::sk_begin(sk.total, sk.G, c + 1);
+    const int KT = sk.KT;
+    if (tid == 0) {
+      for (int s = 0; s < STAGES; ++s) {
+        detail::mbar_init(&full[s], NPROD);
+        detail::mbar_init(&empty[s], NMATH / 32);
+      }
+    }
+    __syncthreads();
+
+    if (tid >= NMATH) {
+      // ================================================================ producer
+      const int p = tid - NMATH;
+      auto mapA = [&](int i, int& m, int& kk) {
+        const int e = p + i * NPROD;
+        if (AMF) { m = e % BM; kk = e / BM; }
+        else { kk = (e & 3) + 4 * (e / (4 * BM)); m = (e >> 2) % BM; }
+      };
+      auto mapB = [&](int i, int& n, int& kk) {
+        const int e = p + i * NPROD;
+        if (BNF) { n = e % BN; kk = e / BN; }
+        else { kk = (e & 3) + 4 * (e / (4 * BN)); n = (e >> 2) % BN; }
+      };
+      constexpr int RA = AMF ? 1 : 4, RB = BNF ? 1 : 4;
+      const uint32_t sAbase = smem_u32(As), sBbase = smem_u32(Bs);
+      constexpr uint32_t stA = BK * LDA * ES, stB = BK * LDB * ES;
+      int64_t gi = 0;
+      // segments in REVERSE range order: a CTA first publishes the partial of the tile it
+      // shares with its successor and finishes (as owner) the tile it shares with its
+      // predecessor last, so no CTA waits on one that is still early in its range
+      for (int64_t e = it1; e > it0;) {
+        const int64_t tile = (e - 1) / KT;
+        const int64_t tstart = tile * KT;
+        const int64_t sb = it0 > tstart ? it0 : tstart;
+        const int kt0 = (int)(sb - tstart);
+        const int kt1 = (int)(e - tstart);
+        int m0, n0;
+        tile_coords(d, tile, m0, n0);
+        detail::named_sync(1, NPROD);  // previous segment's table reads are done
+        for (int i = p; i < BM; i += NPROD) rowOffA[i] = (m0 + i < d.M) ? group_offset(d.rowA, m0 + i) : -1;
+        for (int i = p; i < BN; i += NPROD) colOffB[i] = (n0 + i < d.N) ? group_offset(d.colB, n0 + i) : -1;
+        detail::named_sync(1, NPROD);
+        int64_t rA[RA], rB[RB];
+#pragma unroll
+        for (int j = 0; j < RA; ++j) {
+          int m, kk;
+          mapA(j, m, kk);
+          rA[j] = rowOffA[m];
+        }
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+          int n, kk;
+          mapB(j, n, kk);
+          rB[j] = colOffB[n];
+        }
+        for (int kt = kt0; kt < kt1; ++kt, ++gi) {
+          const int s = (int)(gi % STAGES);
+          const int k0 = kt * BK;
+          if (d.kaff.ok && k0 + BK <= d.K) {
+            const T* pa = A + group_offset(d.kA, k0);
+            const T* pb = B + group_offset(d.kB, k0);
+            if (gi >= STAGES) detail::mbar_wait(&empty[s], (uint32_t)(((gi / STAGES) & 1) ^ 1));
+#pragma unroll
+            for (int i = 0; i < EA; ++i) {
+              int m, kk;
+              mapA(i, m, kk);
+              const int64_t ro = rA[i % RA];
+              const bool v = ro >= 0;
+              const T* src = v ? pa + ro + (int64_t)kk * d.kaff.ksA : A;
+              const uint32_t dst = sAbase + s * stA + (uint32_t)(kk * LDA + m) * ES;
+              if constexpr (CPLX)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
+              else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0));
+            }
+#pragma unroll
+            for (int i = 0; i < EB; ++i) {
+              int n, kk;
+              mapB(i, n, kk);
+              const int64_t co = rB[i % RB];
+              const bool v = co >= 0;
+              const T* src = v ? pb + co + (int64_t)kk * d.kaff.ksB : B;
+              const uint32_t dst = sBbase + s * stB + (uint32_t)(kk * LDB + n) * ES;
+              if constexpr (CPLX)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
+              else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0));
+            }
+          } else {
+            // irregular K group or ragged last k-tile: per-k offsets through a table
+            const int slot = (int)(gi & 1);
+            for (int i = p; i < 2 * BK; i += NPROD) {
+              const int kk = i % BK, k = k0 + kk;
+              const bool v = k < d.K;
+              if (i < BK) kOffA[slot * BK + kk] = v ? group_offset(d.kA, k) : -1;
+              else kOffB[slot * BK + kk] = v ? group_offset(d.kB, k) : -1;
+            }
+            detail::named_sync(1, NPROD);
+            if (gi >= STAGES) detail::mbar_wait(&empty[s], (uint32_t)(((gi / STAGES) & 1) ^ 1));
+            const int64_t* ka = kOffA + slot * BK;
+            const int64_t* kb = kOffB + slot * BK;
+#pragma unroll
+            for (int i = 0; i < EA; ++i) {
+              int m, kk;
+              mapA(i, m, kk);
+              const int64_t ro = rA[i % RA], ko = ka[kk];
+              const bool v = (ro >= 0) && (ko >= 0);
+              const T* src = v ? A + ro + ko : A;
+              const uint32_t dst = sAbase + s * stA + (uint32_t)(kk * LDA + m) * ES;
+              if constexpr (CPLX)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
+              else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0));
+            }
+#pragma unroll
+            for (int i = 0; i < EB; ++i) {
+              int n, kk;
+              mapB(i, n, kk);
+              const int64_t co = rB[i % RB], ko = kb[kk];
+              const bool v = (co >= 0) && (ko >= 0);
+              const T* src = v ? B + co + ko : B;
+              const uint32_t dst = sBbase + s * stB + (uint32_t)(kk * LDB + n) * ES;
+              if constexpr (CPLX)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
+              else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0));
+            }
+          }
+          detail::cp_async_mbar_arrive_noinc(&full[s]);
+        }
+        e = sb;
+      }
+      cp_async_wait<0>();
+      return;
+    }
+
+    // ================================================================== math warps
+    const int lane = tid & 31, warp = tid >> 5;
+    const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+    const int arow = wm * WTM + (lane >> 2);
+    const int bcol = wn * WTN + (lane >> 2);
+    const int kq = lane & 3;
+    int64_t gi = 0;
+    Acc acc;
+    // segments in REVERSE range order: a CTA first publishes the partial of the tile it
+    // shares with its successor and finishes (as owner) the tile it shares with its
+    // predecessor last, so no CTA waits on one that is still early in its range
+    for (int64_t e = it1; e > it0;) {
+      const int64_t tile = (e - 1) / KT;
+      const int64_t tstart = tile * KT;
+      const int64_t sb = it0 > tstart ? it0 : tstart;
+      const int kt0 = (int)(sb - tstart);
+      const int kt1 = (int)(e - tstart);
+      Base::zero(acc);
+      for (int kt = kt0; kt < kt1; ++kt, ++gi) {
+        const int s = (int)(gi % STAGES);
+        detail::mbar_wait(&full[s], (uint32_t)((gi / STAGES) & 1));
+        const T* as = As + s * BK * LDA;
+        const T* bs = Bs + s * BK * LDB;
+#pragma unroll
+        for (int k4 = 0; k4 < BK / 4; ++k4) {
+          const int kr = k4 * 4 + kq;
+          if constexpr (!CPLX) {
+            double af[MF], bf[NF];
+#pragma unroll
+            for (int i = 0; i < MF; ++i) af[i] = as[kr * LDA + arow + i * 8];
+#pragma unroll
+            for (int j = 0; j < NF; ++j) bf[j] = bs[kr * LDB + bcol + j * 8];
+#pragma unroll
+            for (int i = 0; i < MF; ++i)
+#pragma unroll
+              for (int j = 0; j < NF; ++j) dmma(acc[0][i][j][0], acc[0][i][j][1], af[i], bf[j]);
+          } else {
+            double2 af[MF], bf[NF];
+#pragma unroll
+            for (int i = 0; i < MF; ++i) af[i] = as[kr * LDA + arow + i * 8];
+#pragma unroll
+            for (int j = 0; j < NF; ++j) bf[j] = bs[kr * LDB + bcol + j * 8];
+            if constexpr (MODE == 0) {
+#pragma unroll
+              for (int i = 0; i < MF; ++i) {
+                const double ain = dneg(af[i].y);
+#pragma unroll
+                for (int j = 0; j < NF; ++j) {
+                  dmma(acc[0][i][j][0], acc[0][i][j][1], af[i].x, bf[j].x);
+                  dmma(acc[0][i][j][0], acc[0][i][j][1], ain, bf[j].y);
+                  dmma(acc[1][i][j][0], acc[1][i][j][1], af[i].x, bf[j].y);
+                  dmma(acc[1][i][j][0], acc[1][i][j][1], af[i].y, bf[j].x);
+                }
+              }
+            } else {
+              double bsum[NF];
+#pragma unroll
+              for (int j = 0; j < NF; ++j) bsum[j] = bf[j].x + bf[j].y;
+#pragma unroll
+              for (int i = 0; i < MF; ++i) {
+                const double asum = af[i].x + af[i].y;
+#pragma unroll
+                for (int j = 0; j < NF; ++j) {
+                  dmma(acc[0][i][j][0], acc[0][i][j][1], af[i].x, bf[j].x);
+                  dmma(acc[1][i][j][0], acc[1][i][j][1], af[i].y, bf[j].y);
+                  dmma(acc[2][i][j][0], acc[2][i][j][1], asum, bsum[j]);
+                }
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) detail::mbar_arrive(&empty[s]);
+      }
+      // ---- epilogue of this segment
+      int m0, n0;
+      tile_coords(d, tile, m0, n0);
+      double* flat = &acc[0][0][0][0];
+      if (kt1 < KT) {
+        // head/middle of a tile finished by a later CTA: publish the partial
+        double* w = sk.ws + (size_t)c * ACCN * NMATH;
+#pragma unroll
+        for (int r = 0; r < ACCN; ++r) __stcg(w + (size_t)r * NMATH + tid, flat[r]);
+        __threadfence();
+        detail::named_sync(2, NMATH);
+        if (tid == 0) detail::st_release(sk.flags + c, 1);
+      } else {
+        if (kt0 > 0) {
+          // owner: add the partials of the earlier CTAs of this tile in CTA order
+          // (fixed summation order: own k-range, then partials by increasing CTA)
+          const int first = detail::sk_cta_of(sk.total, sk.G, tile * (int64_t)KT);
+          for (int cc = first; cc < c; ++cc) {
+            if (tid == 0)
+              while (detail::ld_acquire(sk.flags + cc) == 0) {
+              }
+            detail::named_sync(2, NMATH);
+            const double* w = sk.ws + (size_t)cc * ACCN * NMATH;
+#pragma unroll
+            for (int r = 0; r < ACCN; ++r) flat[r] += __ldcg(w + (size_t)r * NMATH + tid);
+          }
+        }
+        Base::store(C, d.out_ld, m0, n0, d.M, d.N, acc);
+      }
+      e = sb;
+    }
+  }
+};
+
+}  // namespace tnb

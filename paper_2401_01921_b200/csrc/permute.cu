@@ -67,7 +67,7 @@ struct PermDesc {
 template <int ES>
 __global__ void __launch_bounds__(kThreads, 2) permute_tiled_kernel(
     const typename Word<ES>::T* __restrict__ src, typename Word<ES>::T* __restrict__ dst,
-    const PermDesc d) {
+    const __grid_constant__ PermDesc d) {
   using T = typename Word<ES>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tile = reinterpret_cast<T*>(smem_raw);
@@ -254,7 +254,7 @@ struct RowDesc {
 
 template <int ES>
 __global__ void __launch_bounds__(256) permute_rows_kernel(const unsigned char* __restrict__ src,
-                                                           unsigned char* __restrict__ dst, const RowDesc d) {
+                                                           unsigned char* __restrict__ dst, const __grid_constant__ RowDesc d) {
   using T = typename Word<ES>::T;
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -317,7 +317,7 @@ struct T2Desc {
 
 template <int ES, int T>
 __global__ void __launch_bounds__(256) permute_t2d_kernel(const typename Word<ES>::T* __restrict__ src,
-                                                          typename Word<ES>::T* __restrict__ dst, const T2Desc d) {
+                                                          typename Word<ES>::T* __restrict__ dst, const __grid_constant__ T2Desc d) {
   using W = typename Word<ES>::T;
   constexpr int RPI = 32 / T;      // rows per warp instruction
   constexpr int NI = T / RPI;      // instructions per tile side
