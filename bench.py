@@ -215,16 +215,15 @@ def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, roof=True, s
     if e2e:
         # end to end through the public API: pinned host inputs -> HBM, launch, result -> host
         pinned = {nm: torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for nm, a in inp.items()}
-        out_host = None
         h2d = sum(p.numel() * p.element_size() for p in pinned.values())
+        probe = net.launch().get_block_().contiguous().storage()
+        out_host = torch.empty(probe.shape, dtype=probe.dtype, pin_memory=True)
 
         def step():
-            nonlocal out_host
             for nm, p in pinned.items():
                 tensors[nm].get_block_().storage().copy_(p.reshape(-1), non_blocking=True)
             out = net.launch()
-            host = out.get_block_().contiguous().storage().to("cpu", non_blocking=False)
-            out_host = host
+            out_host.copy_(out.get_block_().contiguous().storage(), non_blocking=True)
         for _ in range(max(1, warmup)):
             step()
         dist.barrier()
@@ -318,7 +317,61 @@ def gpu_c4(tnb, steps, warmup, flush, dist):
         tnb.contract(A, E)
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / steps * 1e3
-    return {"ms_per_call": ms, "host_wall_ms_per_call": wall, "gflops": dist.sum(2 * C4_MACS) / ms / 1e6}
+    # device time of the same call replayed as a CUDA graph (plan cached on device)
+    g = tnb.graphs.capture(lambda: tnb.contract(A, E))
+    gms = time_steps(g.replay, steps, flush, dist) / steps
+    return {"ms_per_call_eager": ms, "host_wall_ms_per_call": wall, "ms_per_call_graph": gms,
+            "gflops_eager": dist.sum(2 * C4_MACS) / ms / 1e6, "gflops": dist.sum(2 * C4_MACS) / gms / 1e6}
+
+
+def gpu_lawr_batch(tnb, n_total, chi, dtype, steps, warmup, flush, dist):
+    """C3b: a batch of independent L.A.W.R matvecs, sharded by instance across ranks."""
+    mine = [i for i in range(n_total) if i % dist.world == dist.rank]
+    nets = []
+    for i in mine:
+        net, _ = lawr_network(tnb, WL.lawr_inputs(chi, dtype=dtype, seed=5000 + 4 * i))
+        nets.append(net)
+    macs, _ = lawr_macs(chi)
+    flop = macs * (8 if dtype == np.complex128 else 2)
+
+    def step():
+        for net in nets:
+            net.launch()
+    for _ in range(warmup):
+        step()
+    ms = time_steps(step, steps, flush, dist) / steps
+    return {"ms_per_step": ms, "instances": n_total, "per_rank": len(mine),
+            "gflops": flop * n_total / ms / 1e6}
+
+
+def gpu_peps(tnb, n_sites, chi, D, d, steps, warmup, flush, dist):
+    """C5 (reading A): PEPS double-layer site networks, optimal order, sharded by site."""
+    mine = [i for i in range(n_sites) if i % dist.world == dist.rank]
+    shapes = WL.peps_shapes(chi, D, d)
+    net = tnb.Network(WL.PEPS_NET)
+    tensors = {}
+    for k, (nm, shp) in enumerate(shapes.items()):
+        t = tnb.UniTensor(tnb.storage.from_numpy(tnb.storage.host_normal(shp, seed=9000 + k)),
+                          labels=[f"x{j}" for j in range(len(shp))])
+        net.put_tensor(nm, t)
+        tensors[nm] = t
+    net.set_order(optimal=True)
+    sets = {n: ls for n, ls in net._slots}
+    dims = {}
+    for nm, ls in net._slots:
+        for l, dd in zip(ls, shapes[nm]):
+            dims[l] = dd
+    tree = tnb.find_optimal_order(sets, dims)
+    flop = 2 * tnb.contraction_cost(tree, sets, dims)
+
+    def step():
+        for _ in mine:  # every site re-launches the blueprint (inputs differ per site in a real sweep)
+            net.launch()
+    for _ in range(max(1, warmup)):
+        net.launch()
+    ms = time_steps(step, steps, flush, dist) / steps
+    return {"ms_per_step": ms, "sites": n_sites, "per_rank": len(mine), "order": tnb.render_order(tree),
+            "flop_per_site": flop, "gflops": flop * n_sites / ms / 1e6}
 
 
 # ----------------------------------------------------------------------------- CPU side
@@ -469,7 +522,14 @@ def main():
                                             "frac_median": {k: round(v["median_gbs"] / hbm_peak, 4)
                                                             for k, v in perm.items()}}}
         c4 = gpu_c4(tnb, max(10, args.steps), args.warmup, flush, dist)
-        wl["blocksparse_c4"] = {"value": round(c4["gflops"], 2), "unit": "GFLOP/s", **c4}
+        wl["blocksparse_c4"] = {"value": round(c4["gflops"], 2), "unit": "GFLOP/s (graph replay; eager in gflops_eager)",
+                                **c4}
+        bt = gpu_lawr_batch(tnb, 64, 512, np.complex128, max(2, args.steps // 4), 1, flush, dist)
+        wl["lawr_batch64_c128_chi512"] = {"value": round(bt["gflops"], 2), "unit": "GFLOP/s (8 flop/complex MAC)",
+                                          "scaling": "strong (64 instances sharded over ranks)", **bt}
+        pe = gpu_peps(tnb, 32, 256, 8, 2, 1, 1, flush, dist)
+        wl["peps_chi256_D8"] = {"value": round(pe["gflops"], 2), "unit": "GFLOP/s",
+                                "scaling": "strong (32 sites sharded over ranks)", **pe}
         line["workloads"] = wl
     if dist.rank == 0 and not args.no_cpu:
         cb = cpu_lawr(1024, np.float64)
