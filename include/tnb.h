@@ -11,7 +11,7 @@
  *   tnb_contract_dense     <- np.tensordot(a.view(), b.view(), axes=(a_pos, b_pos))
  *                             + np.ascontiguousarray(res)
  *                             pkg/src/tnkit/contract.py:127-132 (contract_pair, dense)
- *   tnb_bs_plan / tnb_bs_execute
+ *   tnb_bs_contract[_masked]
  *                          <- _contract_pair_blocks, pkg/src/tnkit/contract.py:137-167
  *                             (b_by_key pairing :148-151, per-pair tensordot :157-158,
  *                              ordered += into the output block :162-164)
@@ -142,6 +142,25 @@ int tnb_bs_contract(int dtype, int na, int nb, int nout,
                     void* const* out_ptrs,
                     int64_t max_pairs, int32_t* pairs_out, int64_t* npairs,
                     void* stream);
+
+/* Multi-GPU partition of a block-sparse contraction: the output is cut into
+ * "panels" of TNB_BS_PANEL_ROWS rows (rows = the a_free part of each output
+ * block), enumerated block by block in output-block order. With panel_mask !=
+ * NULL only panels whose mask byte is non-zero are computed and written (each
+ * panel's full K reduction is local: no cross-GPU reduction); the caller
+ * assembles the rest (parallel.py: NCCL all-gather). npanels must equal the
+ * panel count. Same semantics as tnb_bs_contract otherwise. */
+#define TNB_BS_PANEL_ROWS 64
+int tnb_bs_contract_masked(int dtype, int na, int nb, int nout,
+                           int rank_a, int rank_b,
+                           const int32_t* a_qn, const int64_t* a_shape, const int32_t* a_perm,
+                           const int32_t* b_qn, const int64_t* b_shape, const int32_t* b_perm,
+                           int nc, const int32_t* a_axes, const int32_t* b_axes,
+                           const int32_t* out_qn, const int64_t* out_shape,
+                           const void* const* a_ptrs, const void* const* b_ptrs,
+                           void* const* out_ptrs, int64_t npanels, const uint8_t* panel_mask,
+                           int64_t max_pairs, int32_t* pairs_out, int64_t* npairs,
+                           void* stream);
 
 /* ---- a14: optimal contraction order DP (contract.py:271-343), host only ---
  * n tensors (n <= 16). Labels are interned to ints: nlab[t] labels for tensor

@@ -20,7 +20,7 @@ CPLX_4M, CPLX_3M = 0, 1
 EXPORTS = (
     "tnb_version", "tnb_launch_count", "tnb_last_error", "tnb_device_count", "tnb_set_device",
     "tnb_synchronize", "tnb_permute", "tnb_contract_dense",
-    "tnb_zero_flux_blocks", "tnb_bs_contract", "tnb_optimal_order",
+    "tnb_zero_flux_blocks", "tnb_bs_contract", "tnb_bs_contract_masked", "tnb_optimal_order",
 )
 
 
@@ -61,6 +61,11 @@ def _declare(lib):
                              _pi32, _pi64, _pi32, _pi32, _pi64, _pi32,
                              ctypes.c_int, _pi32, _pi32, _pi32, _pi64,
                              _p, _p, _p, _i64, _pi32, _pi64, _p], ctypes.c_int),
+        "tnb_bs_contract_masked": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_int, ctypes.c_int,
+                                    _pi32, _pi64, _pi32, _pi32, _pi64, _pi32,
+                                    ctypes.c_int, _pi32, _pi32, _pi32, _pi64,
+                                    _p, _p, _p, _i64, _p, _i64, _pi32, _pi64, _p], ctypes.c_int),
         "tnb_optimal_order": ([ctypes.c_int, ctypes.c_char_p, _pi32, _pi32, _pi64,
                                ctypes.c_char_p, _i64, ctypes.c_char_p], ctypes.c_int),
     }
@@ -169,8 +174,11 @@ def zero_flux_blocks(nsec, btype, charges, sym_n):
     return out[:count.value]
 
 
+BS_PANEL_ROWS = 64  # TNB_BS_PANEL_ROWS
+
+
 def bs_contract(dtype, a_qn, a_shapes, a_perm, b_qn, b_shapes, b_perm, a_axes, b_axes,
-                out_qn, out_shapes, a_ptrs, b_ptrs, out_ptrs, stream, want_pairs=False):
+                out_qn, out_shapes, a_ptrs, b_ptrs, out_ptrs, stream, want_pairs=False, panel_mask=None):
     na, nb, nout = len(a_ptrs), len(b_ptrs), len(out_ptrs)
     ra, rb = len(a_perm), len(b_perm)
     aq, paq = _arr32(np.asarray(a_qn, dtype=np.int32).reshape(-1))
@@ -192,11 +200,16 @@ def bs_contract(dtype, a_qn, a_shapes, a_perm, b_qn, b_shapes, b_perm, a_axes, b
     if want_pairs:
         cap = max(na * nb, 1)
         pairs = np.zeros((cap, 3), dtype=np.int32)
-    check(lib().tnb_bs_contract(dtype, na, nb, nout, ra, rb, paq, pash, pap, pbq, pbsh, pbp,
-                                len(a_axes), pxa, pxb, poq, posh,
-                                ctypes.cast(aptr, _p), ctypes.cast(bptr, _p), ctypes.cast(optr, _p),
-                                cap, pairs.ctypes.data_as(_pi32) if want_pairs else None,
-                                ctypes.byref(npairs) if want_pairs else None, stream),
+    mask = None
+    if panel_mask is not None:
+        mask = np.ascontiguousarray(np.asarray(panel_mask, dtype=np.uint8))
+    check(lib().tnb_bs_contract_masked(dtype, na, nb, nout, ra, rb, paq, pash, pap, pbq, pbsh, pbp,
+                                       len(a_axes), pxa, pxb, poq, posh,
+                                       ctypes.cast(aptr, _p), ctypes.cast(bptr, _p), ctypes.cast(optr, _p),
+                                       0 if mask is None else len(mask),
+                                       None if mask is None else mask.ctypes.data_as(_p),
+                                       cap, pairs.ctypes.data_as(_pi32) if want_pairs else None,
+                                       ctypes.byref(npairs) if want_pairs else None, stream),
           "bs_contract")
     if want_pairs:
         return pairs[:npairs.value].copy()

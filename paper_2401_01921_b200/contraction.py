@@ -170,7 +170,7 @@ def _widen(blocks, dt):
     return [b if b.dtype == dt else b.astype(dt) for b in blocks]
 
 
-def _contract_blocks(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds):
+def _contract_blocks(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds, panel_mask=None):
     dt = _result_dtype(a.dtype, b.dtype)
     ablk, aperm = _common_perm(a)
     bblk, bperm = _common_perm(b)
@@ -184,11 +184,13 @@ def _contract_blocks(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds):
     if not qns:
         raise ValueError("no valid blocks: no combination of these bonds' sectors has zero flux")
     shapes = [tuple(x.sectors[k][1] for x, k in zip(out_bonds, qn)) for qn in qns]
-    oblk, _ = _slab_blocks(shapes, dt, zero=False)  # every output block is fully written by the kernel
+    # every output block is fully written by the kernel (with a panel mask: the panels
+    # of this rank; parallel.gather_panels fills the rest)
+    oblk, _ = _slab_blocks(shapes, dt, zero=False)
     _lib.bs_contract(dense.dtype_code(dt), a._qns, [x.storage_shape for x in ablk], aperm,
                      b._qns, [x.storage_shape for x in bblk], bperm, a_pos, b_pos,
                      qns, shapes, [x.data_ptr for x in ablk], [x.data_ptr for x in bblk],
-                     [x.data_ptr for x in oblk], dense.stream_handle())
+                     [x.data_ptr for x in oblk], dense.stream_handle(), panel_mask=panel_mask)
     return UniTensor._assemble(out_bonds, out_labels, len(a_free), "", oblk, qns)
 
 

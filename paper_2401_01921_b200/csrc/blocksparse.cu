@@ -40,7 +40,7 @@ struct BlockDesc {
 };
 
 struct TileRef {
-  int32_t o, m0, n0;
+  int32_t o, m0, n0, panel;  // panel = (o, m0 / TNB_BS_PANEL_ROWS) in output-block order
 };
 
 struct BsMeta {
@@ -61,6 +61,7 @@ struct BsMeta {
   int32_t* out_ptr;   // [nout+1] written by the pairing kernel
   int32_t* pairs;     // [max pairs][2] (i, j) grouped by output block
   int32_t* err;       // [1]
+  const uint8_t* mask;  // per-panel "compute here" flags (multi-GPU partition) or nullptr
   int64_t max_pairs;
 };
 
@@ -169,6 +170,7 @@ __global__ void __launch_bounds__(128, 2) bs_gemm_kernel(const __grid_constant__
   extern __shared__ __align__(16) unsigned char smem[];
   const void* const* ptrs = m.ptrs ? m.ptrs : pt.p;
   const TileRef t = m.tiles[blockIdx.x];
+  if (m.mask && !m.mask[t.panel]) return;  // panel owned by another rank
   const int M = m.out_M[t.o], N = m.out_N[t.o];
   typename Core::Acc acc;
   Core::zero(acc);
@@ -265,12 +267,14 @@ void append(std::string& key, const X* p, size_t n) {
 }  // namespace
 }  // namespace tnb
 
-extern "C" int tnb_bs_contract(int dtype, int na, int nb, int nout, int rank_a, int rank_b, const int32_t* a_qn,
-                               const int64_t* a_shape, const int32_t* a_perm, const int32_t* b_qn,
-                               const int64_t* b_shape, const int32_t* b_perm, int nc, const int32_t* a_axes,
-                               const int32_t* b_axes, const int32_t* out_qn, const int64_t* out_shape,
-                               const void* const* a_ptrs, const void* const* b_ptrs, void* const* out_ptrs,
-                               int64_t max_pairs, int32_t* pairs_out, int64_t* npairs, void* stream) {
+extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int rank_a, int rank_b,
+                                      const int32_t* a_qn, const int64_t* a_shape, const int32_t* a_perm,
+                                      const int32_t* b_qn, const int64_t* b_shape, const int32_t* b_perm, int nc,
+                                      const int32_t* a_axes, const int32_t* b_axes, const int32_t* out_qn,
+                                      const int64_t* out_shape, const void* const* a_ptrs,
+                                      const void* const* b_ptrs, void* const* out_ptrs, int64_t npanels,
+                                      const uint8_t* panel_mask, int64_t max_pairs, int32_t* pairs_out,
+                                      int64_t* npairs, void* stream) {
   using namespace tnb;
   int rc = require_device();
   if (rc) return rc;
@@ -297,6 +301,10 @@ extern "C" int tnb_bs_contract(int dtype, int na, int nb, int nout, int rank_a, 
     append(key, b_axes, (size_t)nc);
     append(key, out_qn, (size_t)nout * ro);
     append(key, out_shape, (size_t)nout * ro);
+    if (panel_mask && npanels > 0) {
+      key.push_back('M');
+      append(key, panel_mask, (size_t)npanels);
+    }
   }
   std::lock_guard<std::mutex> lock(g_cache.mu);
   int dev = 0;
@@ -370,6 +378,8 @@ extern "C" int tnb_bs_contract(int dtype, int na, int nb, int nout, int rank_a, 
     const int BM = 64, BN = 64;
     std::vector<int32_t> oM(nout), oN(nout);
     std::vector<TileRef> tiles;
+    int32_t panel = 0;
+    static_assert(TNB_BS_PANEL_ROWS % 64 == 0, "panels must hold whole 64-row tiles");
     for (int o = 0; o < nout; ++o) {
       int64_t Mo = 1, No = 1;
       for (int f = 0; f < meta.nfa; ++f) Mo *= out_shape[(int64_t)o * ro + f];
@@ -377,9 +387,13 @@ extern "C" int tnb_bs_contract(int dtype, int na, int nb, int nout, int rank_a, 
       if (Mo >= (1ll << 31) || No >= (1ll << 31)) return fail(TNB_EUNSUP, "bs_contract: output block too large");
       oM[o] = (int32_t)Mo;
       oN[o] = (int32_t)No;
-      for (int64_t m0 = 0; m0 < Mo; m0 += BM)
-        for (int64_t n0 = 0; n0 < No; n0 += BN) tiles.push_back({o, (int32_t)m0, (int32_t)n0});
+      for (int64_t m0 = 0; m0 < Mo; m0 += BM) {
+        const int32_t pnl = panel + (int32_t)(m0 / TNB_BS_PANEL_ROWS);
+        for (int64_t n0 = 0; n0 < No; n0 += BN) tiles.push_back({o, (int32_t)m0, (int32_t)n0, pnl});
+      }
+      panel += (int32_t)((Mo + TNB_BS_PANEL_ROWS - 1) / TNB_BS_PANEL_ROWS);
     }
+    if (panel_mask && npanels != panel) return fail(TNB_EINVAL, "bs_contract: panel mask has the wrong length");
     if (tiles.size() >= (1u << 31)) return fail(TNB_EUNSUP, "bs_contract: too many tiles");
     meta.ntiles = (int)tiles.size();
     // exact pair count from a key histogram (O(na + nb)) sizes the device pair table;
@@ -408,7 +422,8 @@ extern "C" int tnb_bs_contract(int dtype, int na, int nb, int nout, int rank_a, 
     const size_t o_aqn = take((size_t)na * rank_a * 4), o_bqn = take((size_t)nb * rank_b * 4),
                  o_oqn = take((size_t)nout * ro * 4), o_oM = take((size_t)nout * 4), o_oN = take((size_t)nout * 4),
                  o_da = take(sizeof(BlockDesc) * na), o_db = take(sizeof(BlockDesc) * nb),
-                 o_tiles = take(sizeof(TileRef) * tiles.size());
+                 o_tiles = take(sizeof(TileRef) * tiles.size()),
+                 o_mask = take(panel_mask ? (size_t)npanels : 0);
     const size_t upload = off;
     const size_t o_optr = take((size_t)(nout + 1) * 4), o_err = take(16), o_pairs = take((size_t)meta.max_pairs * 8);
     const size_t total = off;
@@ -421,6 +436,7 @@ extern "C" int tnb_bs_contract(int dtype, int na, int nb, int nout, int rank_a, 
     memcpy(h.data() + o_da, da.data(), sizeof(BlockDesc) * na);
     memcpy(h.data() + o_db, db.data(), sizeof(BlockDesc) * nb);
     memcpy(h.data() + o_tiles, tiles.data(), sizeof(TileRef) * tiles.size());
+    if (panel_mask) memcpy(h.data() + o_mask, panel_mask, (size_t)npanels);
     TNB_CUDA_CHECK(cudaMalloc((void**)&plan.dblob, total));
     unsigned char* dblob = plan.dblob;
     TNB_CUDA_CHECK(cudaMemcpyAsync(dblob, h.data(), upload, cudaMemcpyHostToDevice, st));  // staged, then returns
@@ -436,6 +452,7 @@ extern "C" int tnb_bs_contract(int dtype, int na, int nb, int nout, int rank_a, 
     meta.out_ptr = reinterpret_cast<int32_t*>(dblob + o_optr);
     meta.err = reinterpret_cast<int32_t*>(dblob + o_err);
     meta.pairs = reinterpret_cast<int32_t*>(dblob + o_pairs);
+    meta.mask = panel_mask ? reinterpret_cast<const uint8_t*>(dblob + o_mask) : nullptr;
     meta.ptrs = nullptr;
     bs_pair_kernel<<<1, 1024, 0, st>>>(meta);
     count_launch();
@@ -509,4 +526,15 @@ extern "C" int tnb_bs_contract(int dtype, int na, int nb, int nout, int rank_a, 
     if (npairs) *npairs = np;
   }
   return TNB_OK;
+}
+
+extern "C" int tnb_bs_contract(int dtype, int na, int nb, int nout, int rank_a, int rank_b, const int32_t* a_qn,
+                               const int64_t* a_shape, const int32_t* a_perm, const int32_t* b_qn,
+                               const int64_t* b_shape, const int32_t* b_perm, int nc, const int32_t* a_axes,
+                               const int32_t* b_axes, const int32_t* out_qn, const int64_t* out_shape,
+                               const void* const* a_ptrs, const void* const* b_ptrs, void* const* out_ptrs,
+                               int64_t max_pairs, int32_t* pairs_out, int64_t* npairs, void* stream) {
+  return tnb_bs_contract_masked(dtype, na, nb, nout, rank_a, rank_b, a_qn, a_shape, a_perm, b_qn, b_shape, b_perm, nc,
+                                a_axes, b_axes, out_qn, out_shape, a_ptrs, b_ptrs, out_ptrs, 0, nullptr, max_pairs,
+                                pairs_out, npairs, stream);
 }

@@ -137,6 +137,100 @@ __global__ void splitk_reduce_kernel(const typename Elem<CPLX>::T* __restrict__ 
   }
 }
 
+// ------------------------------------------------------------------ narrow kernel
+// C[M, N] for N <= 16, K <= 32 (the T1.W step of L.A.W.R: N = K = 10): HBM-bound.
+// One warp owns 32 consecutive rows (one per lane): a lane issues all K gathered
+// loads of its row before any FMA (K loads in flight per lane, no block barrier),
+// multiplies by B held in shared memory (broadcast reads), stages the 32 x N
+// outputs -- one contiguous run of C -- in a per-warp smem tile and writes them
+// with consecutive lanes on consecutive addresses.
+template <bool CPLX, int NMAX, int KMAX, int WARPS = (CPLX ? 4 : 8)>
+__global__ void __launch_bounds__(WARPS * 32) narrow_kernel(const typename Elem<CPLX>::T* __restrict__ A,
+                                                     const typename Elem<CPLX>::T* __restrict__ B,
+                                                     typename Elem<CPLX>::T* __restrict__ C,
+                                                     const __grid_constant__ GemmDesc d) {
+  using T = typename Elem<CPLX>::T;
+  __shared__ T Bs[KMAX * NMAX];
+  __shared__ int64_t kA[KMAX];
+  __shared__ T stage[WARPS][32 * NMAX + 1];
+  const int K = d.K, N = d.N;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) kA[i] = group_offset(d.kA, i);
+  for (int i = threadIdx.x; i < K * N; i += blockDim.x) {
+    const int k = i / N, n = i - k * N;
+    Bs[k * NMAX + n] = B[group_offset(d.kB, k) + group_offset(d.colB, n)];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T* st = stage[warp];
+  const int64_t nchunks = ((int64_t)d.M + 31) / 32;
+  for (int64_t ch = (int64_t)blockIdx.x * WARPS + warp; ch < nchunks; ch += (int64_t)gridDim.x * WARPS) {
+    const int64_t r0 = ch * 32;
+    const int64_t r = r0 + lane;
+    const int rows = (int)(d.M - r0 < 32 ? d.M - r0 : 32);
+    T a[KMAX];
+    if (r < d.M) {
+      const int64_t ro = group_offset(d.rowA, (uint32_t)r);
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k < K) a[k] = __ldcs(A + ro + kA[k]);
+    }
+    if constexpr (!CPLX) {
+      double acc[NMAX];
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n) acc[n] = 0.0;
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k < K)
+#pragma unroll
+          for (int n = 0; n < NMAX; ++n) acc[n] = fma(a[k], Bs[k * NMAX + n], acc[n]);
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n)
+        if (n < N) st[lane * N + n] = acc[n];
+    } else {
+      double ar[NMAX], ai[NMAX];
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n) ar[n] = ai[n] = 0.0;
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k < K)
+#pragma unroll
+          for (int n = 0; n < NMAX; ++n) {
+            const double2 b = Bs[k * NMAX + n];
+            ar[n] = fma(a[k].x, b.x, ar[n]);
+            ar[n] = fma(-a[k].y, b.y, ar[n]);
+            ai[n] = fma(a[k].x, b.y, ai[n]);
+            ai[n] = fma(a[k].y, b.x, ai[n]);
+          }
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n)
+        if (n < N) st[lane * N + n] = make_double2(ar[n], ai[n]);
+    }
+    __syncwarp();
+    T* out = C + r0 * N;
+    const int tot = rows * N;
+    for (int i = lane; i < tot; i += 32) __stcs(out + i, st[i]);
+    __syncwarp();
+  }
+}
+
+template <bool CPLX, int NMAX, int KMAX>
+int run_narrow(const void* A, const void* B, void* C, const GemmDesc& d, cudaStream_t st) {
+  using T = typename Elem<CPLX>::T;
+  constexpr int WARPS = CPLX ? 4 : 8;
+  auto kern = narrow_kernel<CPLX, NMAX, KMAX, WARPS>;
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    TNB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, 0));
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int64_t chunks = ((int64_t)d.M + 31) / 32;
+  const int64_t grid = std::min<int64_t>((chunks + WARPS - 1) / WARPS, (int64_t)sm_count() * per_sm);
+  kern<<<(unsigned)grid, WARPS * 32, 0, st>>>(static_cast<const T*>(A), static_cast<const T*>(B), static_cast<T*>(C), d);
+  count_launch();
+  TNB_CUDA_CHECK(cudaGetLastError());
+  return TNB_OK;
+}
+
 // ------------------------------------------------------------------ skinny kernel
 // C[M, N] with N <= 64 and K <= 64: memory-bound. Each CTA stages a 128-row
 // panel of A (gathered through the offset groups) and all of B in shared
@@ -429,6 +523,9 @@ size_t skinny_smem(const GemmDesc& d) {
 
 template <bool CPLX, int MODE>
 int dispatch(const void* A, const void* B, void* C, GemmDesc& d, cudaStream_t st) {
+  if (d.N <= 16 && d.K <= 16 && d.M >= 4096) return run_narrow<CPLX, 16, 16>(A, B, C, d, st);
+  if constexpr (!CPLX)
+    if (d.N <= 16 && d.K <= 32 && d.M >= 4096) return run_narrow<CPLX, 16, 32>(A, B, C, d, st);
   if (d.N <= 64 && d.K <= 64 && d.M >= 4096 && skinny_smem<CPLX>(d) <= 160 * 1024)
     return run_skinny<CPLX>(A, B, C, d, st);
   if constexpr (!CPLX) return StreamK<false, 0, 128, 128, 16, 4, 4, 4>::run(A, B, C, d, st);
