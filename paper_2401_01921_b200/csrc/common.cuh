@@ -28,6 +28,8 @@ int sm_count();
 // Counts every kernel this library launches (tnb_launch_count); bench.py reports it.
 void count_launch(int n = 1);
 
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
 // Unsigned 32-bit division by a runtime-invariant divisor via multiply-high
 // (Granlund-Montgomery). Valid for 0 <= n < 2^31 and 1 <= d < 2^31.
 struct FastDiv {

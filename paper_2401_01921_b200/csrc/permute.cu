@@ -250,49 +250,203 @@ struct RowDesc {
   FastDiv bdiv[kMaxR];
   FastDiv chunk_div;
   int vec;            // 1: 16-byte vectors usable (aligned rows), 0: element copies
+  int bulk;           // 1: TMA bulk-copy path (rows 16-byte aligned, long enough)
+  int64_t bchunks;    // 8 KB chunks per row (bulk path)
+  FastDiv bchunk_div;
+  FastDiv vdiv;       // by 16-byte vectors per unit row (rows kernel)
 };
 
+// Unit = R consecutive OUTPUT rows (R <= 32, R * row_bytes <= 8 KB; these are one
+// contiguous output run) or an 8 KB chunk of one long row. Lane j computes the
+// input offset of row j of the unit once and shares it by warp shuffle; every lane
+// then issues up to 16 independent 16-byte loads before its 16 stores (8 KB in
+// flight per warp).
 template <int ES>
 __global__ void __launch_bounds__(256) permute_rows_kernel(const unsigned char* __restrict__ src,
-                                                           unsigned char* __restrict__ dst, const __grid_constant__ RowDesc d) {
+                                                           unsigned char* __restrict__ dst,
+                                                           const __grid_constant__ RowDesc d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t row_bytes = d.L * ES;
+  const bool grouped = row_bytes <= 8192;
+  const int R = grouped ? (int)min64(32, 8192 / row_bytes) : 1;
+  const int V = grouped ? (int)(row_bytes >> 4) : 512;  // 16-byte vectors per row (per chunk)
+  const FastDiv& vdiv = d.vdiv;
+  const int64_t units = grouped ? (d.rows + R - 1) / R : d.rows * d.chunks;
+  for (int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < units; u += warps) {
+    int64_t r0, b0 = 0;
+    int nr, nvec;
+    if (grouped) {
+      r0 = u * R;
+      nr = (int)min64(R, d.rows - r0);
+      nvec = nr * V;
+    } else {
+      const uint32_t row = d.chunk_div.div((uint32_t)u);
+      r0 = row;
+      nr = 1;
+      b0 = (u - (int64_t)row * d.chunks) * 8192;
+      nvec = (int)(min64(8192, row_bytes - b0) >> 4);
+    }
+    int64_t my_src = 0;
+    if (lane < nr) {
+      uint32_t rem = (uint32_t)(r0 + lane);
+      for (int q = d.nb - 1; q >= 0; --q) {
+        uint32_t quo = d.bdiv[q].div(rem);
+        my_src += (int64_t)(rem - quo * (uint32_t)d.bdim[q]) * d.bistr[q];
+        rem = quo;
+      }
+      my_src = my_src * ES + b0;
+    }
+    uint4 v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int i = lane + 32 * k;
+      const uint32_t row = vdiv.div((uint32_t)i);
+      const int64_t rs = __shfl_sync(0xffffffffu, my_src, (int)(row & 31));
+      if (i < nvec) v[k] = __ldcs(reinterpret_cast<const uint4*>(src + rs + (int64_t)(i - (int)row * V) * 16));
+    }
+    uint4* o = reinterpret_cast<uint4*>(dst + r0 * row_bytes + b0);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int i = lane + 32 * k;
+      if (i < nvec) __stcs(o + i, v[k]);
+    }
+  }
+}
+
+// element-wise fallback for rows that are not 16-byte multiples
+template <int ES>
+__global__ void __launch_bounds__(256) permute_rows_scalar_kernel(const unsigned char* __restrict__ src,
+                                                                  unsigned char* __restrict__ dst,
+                                                                  const __grid_constant__ RowDesc d) {
   using T = typename Word<ES>::T;
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t units = d.rows * d.chunks;
-  constexpr int kChunkBytes = 2048;
-  for (int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < units; u += warps) {
-    uint32_t row = d.chunk_div.div((uint32_t)u);
-    int64_t chunk = u - (int64_t)row * d.chunks;
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < d.rows; row += warps) {
     int64_t in_off = 0;
-    uint32_t rem = row;
+    uint32_t rem = (uint32_t)row;
     for (int q = d.nb - 1; q >= 0; --q) {
       uint32_t quo = d.bdiv[q].div(rem);
       in_off += (int64_t)(rem - quo * (uint32_t)d.bdim[q]) * d.bistr[q];
       rem = quo;
     }
-    const int64_t row_bytes = d.L * ES;
-    const int64_t b0 = chunk * kChunkBytes;
-    const int64_t nbytes = min((int64_t)kChunkBytes, row_bytes - b0);
-    const unsigned char* s = src + in_off * ES + b0;
-    unsigned char* o = dst + (int64_t)row * row_bytes + b0;
-    if (d.vec) {
-      const uint4* s4 = reinterpret_cast<const uint4*>(s);
-      uint4* o4 = reinterpret_cast<uint4*>(o);
-      const int nv = (int)(nbytes >> 4);
-      uint4 v[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (lane + 32 * k < nv) v[k] = __ldcs(s4 + lane + 32 * k);
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (lane + 32 * k < nv) __stcs(o4 + lane + 32 * k, v[k]);
-    } else {
-      const T* st = reinterpret_cast<const T*>(s);
-      T* ot = reinterpret_cast<T*>(o);
-      const int ne = (int)(nbytes / ES);
-      for (int e = lane; e < ne; e += 32) ot[e] = st[e];
-    }
+    const T* s = reinterpret_cast<const T*>(src) + in_off;
+    T* o = reinterpret_cast<T*>(dst) + row * d.L;
+    for (int64_t e = lane; e < d.L; e += 32) o[e] = s[e];
   }
+}
+
+// ---------------------------------------------------------------------------
+// Fast path 1b -- the same row gather with the TMA bulk-copy engine
+// (cp.async.bulk global->shared, shared->global) when rows are 16-byte aligned.
+// A "unit" is either a group of consecutive OUTPUT rows (short rows: R loads, one
+// contiguous store) or a 8 KB chunk of one long row. One elected lane per warp
+// drives a 4-stage ring of 8 KB shared buffers: stage i+3 is being loaded while
+// unit i is stored, ~24 KB of reads in flight per warp with no per-element
+// instructions at all.
+constexpr int kBulkStage = 8192;
+constexpr int kBulkStages = 4;
+constexpr int kBulkWarps = 2;
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(src), "r"(bytes)
+               : "memory");
+}
+
+template <int ES>
+__global__ void __launch_bounds__(kBulkWarps * 32) permute_rows_bulk_kernel(const unsigned char* __restrict__ src,
+                                                                             unsigned char* __restrict__ dst,
+                                                                             const __grid_constant__ RowDesc d) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t mbar[kBulkWarps][kBulkStages];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane != 0) return;
+  unsigned char* ring = smem_raw + (size_t)warp * kBulkStages * kBulkStage;
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+  uint32_t mb[kBulkStages];
+  for (int s = 0; s < kBulkStages; ++s) {
+    mb[s] = (uint32_t)__cvta_generic_to_shared(&mbar[warp][s]);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb[s]));
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  const int64_t row_bytes = d.L * ES;
+  const bool grouped = row_bytes <= kBulkStage;
+  const int64_t R = grouped ? (kBulkStage / row_bytes) : 1;  // rows per unit
+  const int64_t units = grouped ? (d.rows + R - 1) / R : d.rows * d.bchunks;
+  const int64_t wstride = (int64_t)gridDim.x * kBulkWarps;
+  const int64_t first = (int64_t)blockIdx.x * kBulkWarps + warp;
+  // input byte offset of output row r
+  auto row_src = [&](int64_t r) -> int64_t {
+    int64_t off = 0;
+    uint32_t rem = (uint32_t)r;
+    for (int q = d.nb - 1; q >= 0; --q) {
+      uint32_t quo = d.bdiv[q].div(rem);
+      off += (int64_t)(rem - quo * (uint32_t)d.bdim[q]) * d.bistr[q];
+      rem = quo;
+    }
+    return off * ES;
+  };
+  auto issue_load = [&](int64_t u, int s) -> void {
+    if (grouped) {
+      const int64_t r0 = u * R;
+      const int64_t nr = (r0 + R <= d.rows) ? R : d.rows - r0;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb[s]),
+                   "r"((uint32_t)(nr * row_bytes)));
+      for (int64_t j = 0; j < nr; ++j)
+        bulk_g2s(ring_s + s * kBulkStage + (uint32_t)(j * row_bytes), src + row_src(r0 + j), (uint32_t)row_bytes,
+                 mb[s]);
+    } else {
+      const uint32_t row = d.bchunk_div.div((uint32_t)u);
+      const int64_t ch = u - (int64_t)row * d.bchunks;
+      const int64_t b0 = ch * kBulkStage;
+      const uint32_t nbytes = (uint32_t)((row_bytes - b0 < kBulkStage) ? row_bytes - b0 : kBulkStage);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb[s]), "r"(nbytes));
+      bulk_g2s(ring_s + s * kBulkStage, src + row_src(row) + b0, nbytes, mb[s]);
+    }
+  };
+  auto issue_store = [&](int64_t u, int s) -> void {
+    int64_t off, nbytes;
+    if (grouped) {
+      const int64_t r0 = u * R;
+      const int64_t nr = (r0 + R <= d.rows) ? R : d.rows - r0;
+      off = r0 * row_bytes;
+      nbytes = nr * row_bytes;
+    } else {
+      const uint32_t row = d.bchunk_div.div((uint32_t)u);
+      const int64_t ch = u - (int64_t)row * d.bchunks;
+      const int64_t b0 = ch * kBulkStage;
+      off = (int64_t)row * row_bytes + b0;
+      nbytes = (row_bytes - b0 < kBulkStage) ? row_bytes - b0 : kBulkStage;
+    }
+    bulk_s2g(dst + off, ring_s + s * kBulkStage, (uint32_t)nbytes);
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+  };
+  const int64_t mine = (first < units) ? (units - first + wstride - 1) / wstride : 0;
+  // prologue: S-1 loads in flight
+  for (int64_t i = 0; i < kBulkStages - 1 && i < mine; ++i) issue_load(first + i * wstride, (int)i);
+  for (int64_t i = 0; i < mine; ++i) {
+    const int s = (int)(i % kBulkStages);
+    const int64_t nxt = i + kBulkStages - 1;
+    if (nxt < mine) {
+      // its stage was last read by the store of unit i-1: wait for that smem read
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      issue_load(first + nxt * wstride, (int)(nxt % kBulkStages));
+    }
+    const uint32_t parity = (uint32_t)((i / kBulkStages) & 1);
+    asm volatile(
+        "{\n.reg .pred P1;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n}\n" ::"r"(mb[s]),
+        "r"(parity)
+        : "memory");
+    issue_store(first + i * wstride, s);
+  }
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -456,7 +610,7 @@ int make_plan(int es, int rank, const int64_t* shape, const int32_t* perm, Plan&
       memset(&rd, 0, sizeof(rd));
       rd.L = mdim[a_si];
       rd.rows = n / rd.L;
-      rd.chunks = (rd.L * es + 2047) / 2048;
+      rd.chunks = (rd.L * es + 8191) / 8192;
       if (rd.rows * rd.chunks >= (int64_t(1) << 31)) return fail(TNB_EUNSUP, "permute: too many rows");
       rd.chunk_div = FastDiv((uint32_t)rd.chunks);
       for (int k = 0; k < r - 1; ++k) {
@@ -467,6 +621,15 @@ int make_plan(int es, int rank, const int64_t* shape, const int32_t* perm, Plan&
         rd.nb++;
       }
       rd.vec = ((rd.L * es) % 16 == 0) ? 1 : 0;
+      rd.vdiv = FastDiv((uint32_t)(rd.L * es <= 8192 ? (rd.L * es) / 16 : 512));
+      // bulk copies: 16-byte granularity; the input row strides are multiples of L
+      rd.bulk = (rd.vec && rd.L * es >= 8192) ? 1 : 0;  // long rows: TMA bulk copies
+      if (rd.bulk) {
+        const int64_t rb = rd.L * es;
+        rd.bchunks = (rb + kBulkStage - 1) / kBulkStage;
+        rd.bchunk_div = FastDiv((uint32_t)rd.bchunks);
+        if (rd.rows * rd.bchunks >= (int64_t(1) << 31)) rd.bulk = 0;
+      }
       p.kind = 1;
       return TNB_OK;
     }
@@ -671,18 +834,47 @@ int launch_t2d(const void* src, void* dst, const Plan& p, cudaStream_t st) {
 }
 
 template <int ES>
-int launch_rows(const void* src, void* dst, const Plan& p, cudaStream_t st) {
-  auto kern = permute_rows_kernel<ES>;
+int launch_rows_bulk(const void* src, void* dst, const Plan& p, cudaStream_t st) {
+  auto kern = permute_rows_bulk_kernel<ES>;
+  const size_t smem = (size_t)kBulkWarps * kBulkStages * kBulkStage;
   static int per_sm = 0;
   if (per_sm == 0) {
-    TNB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    TNB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TNB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBulkWarps * 32, smem));
     if (per_sm < 1) per_sm = 1;
   }
-  int64_t units = p.rd.rows * p.rd.chunks;
-  int64_t grid = std::min<int64_t>((units + 7) / 8, (int64_t)sm_count() * per_sm);
-  RowDesc rd = p.rd;
-  if (rd.vec && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)) rd.vec = 0;
-  kern<<<(unsigned)grid, 256, 0, st>>>(static_cast<const unsigned char*>(src), static_cast<unsigned char*>(dst), rd);
+  const int64_t row_bytes = p.rd.L * ES;
+  const int64_t units = row_bytes <= kBulkStage ? (p.rd.rows + (kBulkStage / row_bytes) - 1) / (kBulkStage / row_bytes)
+                                                : p.rd.rows * p.rd.bchunks;
+  const int64_t grid = std::min<int64_t>((units + kBulkWarps - 1) / kBulkWarps, (int64_t)sm_count() * per_sm);
+  kern<<<(unsigned)grid, kBulkWarps * 32, smem, st>>>(static_cast<const unsigned char*>(src),
+                                                       static_cast<unsigned char*>(dst), p.rd);
+  count_launch();
+  TNB_CUDA_CHECK(cudaGetLastError());
+  return TNB_OK;
+}
+
+template <int ES>
+int launch_rows(const void* src, void* dst, const Plan& p, cudaStream_t st) {
+  const bool aligned = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  if (p.rd.bulk && aligned) return launch_rows_bulk<ES>(src, dst, p, st);
+  const bool vec = p.rd.vec && aligned;
+  auto kern = vec ? permute_rows_kernel<ES> : permute_rows_scalar_kernel<ES>;
+  static int per_sm[2] = {0, 0};
+  int& psm = per_sm[vec ? 1 : 0];
+  if (psm == 0) {
+    TNB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&psm, kern, 256, 0));
+    if (psm < 1) psm = 1;
+  }
+  const int64_t row_bytes = p.rd.L * ES;
+  int64_t units = p.rd.rows;
+  if (vec) {
+    const int64_t R = row_bytes <= 8192 ? std::min<int64_t>(32, 8192 / row_bytes) : 1;
+    units = row_bytes <= 8192 ? (p.rd.rows + R - 1) / R : p.rd.rows * p.rd.chunks;
+  }
+  const int64_t grid = std::min<int64_t>((units + 7) / 8, (int64_t)sm_count() * psm);
+  kern<<<(unsigned)grid, 256, 0, st>>>(static_cast<const unsigned char*>(src), static_cast<unsigned char*>(dst),
+                                       p.rd);
   count_launch();
   TNB_CUDA_CHECK(cudaGetLastError());
   return TNB_OK;
