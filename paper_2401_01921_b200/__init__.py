@@ -11,7 +11,7 @@ Tensors live in HBM; the Python layer keeps the reference's labels / bonds /
 qnums / Network semantics and calls libtnb.so through a C ABI (include/tnb.h).
 There is no CPU fallback.
 """
-from . import graphs, parallel, random, workloads
+from . import eig, graphs, parallel, random, workloads
 from . import dense as storage
 from ._lib import EngineError, EngineUnavailable
 from .blueprint import Network
@@ -33,5 +33,5 @@ __all__ = [
     "Int64", "Network", "Symmetry", "UniTensor", "EngineError", "EngineUnavailable", "arange", "block_pairs",
     "brute_force_order", "contract", "Contract", "contract_pair", "contraction_cost", "execute_tree", "eye",
     "find_optimal_order", "from_numpy", "get_complex_mode", "kron", "normal", "ones", "parse_order", "random",
-    "render_order", "set_complex_mode", "storage", "tree_leaves", "uniform", "zeros", "graphs", "parallel", "workloads",
+    "render_order", "set_complex_mode", "storage", "tree_leaves", "uniform", "zeros", "eig", "graphs", "parallel", "workloads",
 ]
