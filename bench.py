@@ -47,6 +47,18 @@ def peaks():
     return hbm, src
 
 
+def traffic_per_launch(kernel, dtype):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed `ncu --set full`
+    capture of this workload (profiles/r01_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            tr = json.load(f)
+        key = f"{kernel}:{np.dtype(dtype).name}"
+        return tr[key]["bytes_per_launch"] if key in tr else None
+    except Exception:
+        return None
+
+
 # ----------------------------------------------------------------------------- dist
 class Dist:
     def __init__(self):
@@ -245,24 +257,25 @@ def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, roof=True, s
                       "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                       "ms_per_step": ems / steps}
     if roof:
-        # dominant kernel = the DMMA GEMM of steps 1 (A.L) and 3 (T2.R): time those launches alone
-        L = tensors["L"].relabel(["b", "w", "vl"])
-        A = tensors["A"].relabel(["vl", "p", "vr"])
-        W = tensors["W"].relabel(["w", "w2", "q", "p"])
-        R = tensors["R"].relabel(["b2", "w2", "vr"])
-        t1 = tnb.contract_pair(A, L)
-        t2 = tnb.contract_pair(t1, W)
-        mul = 8 if dtype == np.complex128 else 2
-        f1 = 2 * chi * 5 * chi * chi * mul
-        f3 = 2 * chi * chi * 5 * chi * mul
-        s1 = time_steps(lambda: tnb.contract_pair(A, L), steps, flush, dist) / steps
-        s3 = time_steps(lambda: tnb.contract_pair(t2, R), steps, flush, dist) / steps
-        s2 = time_steps(lambda: tnb.contract_pair(t1, W), steps, flush, dist) / steps
-        res["steps_ms"] = {"A.L": s1, "T1.W": s2, "T2.R": s3}
-        ach = (f1 + f3) / ((s1 + s3) / 1e3) / 1e12
+        # dominant kernel = the stream-K DMMA GEMM (steps A.L and T2.R): the library's kernel
+        # timer records a CUDA event pair around each of its launches ON THE LAUNCHING STREAM;
+        # this pass repeats the timed region (same flush, same K steps) with the timer on.
+        tnb._lib.ktimer_reset()
+        tnb._lib.ktimer_enable(True)
+        time_steps(net.launch, steps, flush, dist)
+        tnb._lib.ktimer_enable(False)
+        n_g, ms_g, fl_g = tnb._lib.ktimer_read(tnb._lib.KF_GEMM)
+        n_s, ms_s, _ = tnb._lib.ktimer_read(tnb._lib.KF_GEMM_SKINNY)
+        tnb._lib.ktimer_reset()
+        ach = fl_g / (dist.max(ms_g) / 1e3) / 1e12 if n_g else 0.0  # per GPU (slowest rank)
+        res["steps_ms"] = {"gemm (A.L + T2.R)": ms_g / steps, "skinny (T1.W)": ms_s / steps,
+                           "gemm_launches_per_step": n_g / steps, "gemm_share_of_step": ms_g / ms}
         res["roofline"] = {"bound": "tensor", "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS,
-                           "unit": "TFLOP/s", "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": None,
-                           "kernel": "gemm_ws_kernel (DMMA.8x8x4) steps A.L + T2.R",
+                           "unit": "TFLOP/s", "frac": round(ach / FP64_PEAK_TFLOPS, 4),
+                           "traffic": traffic_per_launch("gemm_sk_kernel", dtype),
+                           "kernel": "gemm_sk_kernel (stream-K DMMA.8x8x4), steps A.L + T2.R",
+                           "achieved_how": "algorithmic flop of the GEMM launches / their summed CUDA-event "
+                                           "durations on the launching stream, over the K timed steps",
                            "peak_source": PEAK_SOURCE}
     return res
 
@@ -331,7 +344,15 @@ def gpu_c4(tnb, steps, warmup, flush, dist):
     # device time of the same call replayed as a CUDA graph (plan cached on device)
     g = tnb.graphs.capture(lambda: tnb.contract(A, E))
     gms = time_steps(g.replay, steps, flush, dist) / steps
+    tnb._lib.ktimer_reset()
+    tnb._lib.ktimer_enable(True)
+    time_steps(lambda: tnb.contract(A, E), steps, flush, dist)
+    tnb._lib.ktimer_enable(False)
+    n_k, ms_k, _ = tnb._lib.ktimer_read(tnb._lib.KF_BS_GEMM)
+    tnb._lib.ktimer_reset()
+    kms = ms_k / max(n_k, 1)
     return {"ms_per_call_eager": ms, "host_wall_ms_per_call": wall, "ms_per_call_graph": gms,
+            "bs_gemm_kernel_ms": kms, "bs_gemm_kernel_tflops": 2 * C4_MACS / kms / 1e9,
             "gflops_eager": dist.sum(2 * C4_MACS) / ms / 1e6, "gflops": dist.sum(2 * C4_MACS) / gms / 1e6}
 
 

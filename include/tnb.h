@@ -71,6 +71,23 @@ int tnb_device_count(int* count);            /* 0 devices is not an error */
 int tnb_set_device(int device);
 int tnb_synchronize(void* stream);           /* waits; surfaces async faults */
 
+/* ---- kernel timer (measurement; bench.py's roofline) ----------------------
+ * While enabled, every libtnb kernel launch outside stream capture records a
+ * CUDA event pair on the stream it is launched on, plus its algorithmic work
+ * (flop for contractions: 2 per real MAC, 8 per complex MAC; bytes read +
+ * written for permutes; 0 where the host does not know it).
+ * tnb_ktimer_read sums launches, device milliseconds and work of one family
+ * since the last reset (it waits for the recorded events). */
+#define TNB_KF_GEMM 0        /* stream-K DMMA GEMM (dense contraction)        */
+#define TNB_KF_GEMM_SKINNY 1 /* memory-bound narrow/skinny contraction kernels */
+#define TNB_KF_PERMUTE 2     /* permute materialisation kernels              */
+#define TNB_KF_BS_GEMM 3     /* block-sparse grouped GEMM                    */
+#define TNB_KF_BS_PAIR 4     /* block-sparse device pairing                  */
+#define TNB_KF_OTHER 5       /* widening, split-K reduce, ...                */
+int tnb_ktimer_enable(int on);
+int tnb_ktimer_reset(void);
+int tnb_ktimer_read(int family, int64_t* launches, double* ms, double* work);
+
 /* ---- a7: permute materialisation (storage.py:114-144) ---------------------
  * dst[row-major over logical shape] = src viewed with storage shape `shape`
  * and logical permutation `perm`; bit-exact data movement for element sizes

@@ -21,7 +21,11 @@ EXPORTS = (
     "tnb_version", "tnb_launch_count", "tnb_last_error", "tnb_device_count", "tnb_set_device",
     "tnb_synchronize", "tnb_permute", "tnb_contract_dense",
     "tnb_zero_flux_blocks", "tnb_bs_contract", "tnb_bs_contract_masked", "tnb_optimal_order",
+    "tnb_ktimer_enable", "tnb_ktimer_reset", "tnb_ktimer_read",
 )
+
+# kernel families of the kernel timer (TNB_KF_* in include/tnb.h)
+KF_GEMM, KF_GEMM_SKINNY, KF_PERMUTE, KF_BS_GEMM, KF_BS_PAIR, KF_OTHER = 0, 1, 2, 3, 4, 5
 
 
 class EngineError(RuntimeError):
@@ -50,6 +54,10 @@ def _declare(lib):
         "tnb_device_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
         "tnb_set_device": ([ctypes.c_int], ctypes.c_int),
         "tnb_synchronize": ([_p], ctypes.c_int),
+        "tnb_ktimer_enable": ([ctypes.c_int], ctypes.c_int),
+        "tnb_ktimer_reset": ([], ctypes.c_int),
+        "tnb_ktimer_read": ([ctypes.c_int, _pi64, ctypes.POINTER(ctypes.c_double),
+                             ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
         "tnb_permute": ([_p, _p, ctypes.c_int, ctypes.c_int, _pi64, _pi32, _p], ctypes.c_int),
         "tnb_contract_dense": ([_p, ctypes.c_int, ctypes.c_int, _pi64, _pi32,
                                 _p, ctypes.c_int, ctypes.c_int, _pi64, _pi32,
@@ -99,6 +107,22 @@ def lib():
 def launch_count():
     """Number of kernels libtnb has launched in this process."""
     return int(lib().tnb_launch_count())
+
+
+def ktimer_enable(on=True):
+    """Record a CUDA event pair around every libtnb kernel launch (outside graph capture)."""
+    check(lib().tnb_ktimer_enable(1 if on else 0), "ktimer_enable")
+
+
+def ktimer_reset():
+    check(lib().tnb_ktimer_reset(), "ktimer_reset")
+
+
+def ktimer_read(family):
+    """(launches, device ms, algorithmic work) of one kernel family since the last reset."""
+    n, ms, w = ctypes.c_int64(0), ctypes.c_double(0.0), ctypes.c_double(0.0)
+    check(lib().tnb_ktimer_read(int(family), ctypes.byref(n), ctypes.byref(ms), ctypes.byref(w)), "ktimer_read")
+    return int(n.value), float(ms.value), float(w.value)
 
 
 def last_error():

@@ -10,15 +10,26 @@
 //
 // B200 design:
 //   1. One H2D copy of all block metadata (qn tuples, per-block address groups,
-//      output tile list) from a pinned staging buffer.
-//   2. pairing kernel (ON DEVICE, one CTA): thread per output block o finds its
-//      contributing pairs (i asc, j asc) -- exactly the reference's accumulation
-//      order restricted to o -- and writes a CSR (out_ptr, pair list).
-//   3. grouped GEMM kernel: one CTA per output tile; it loops over its output
-//      block's pairs in that order, accumulating all of them in registers
-//      (deterministic, no atomics), then stores the tile once. Tiles of blocks
-//      with no pair store zeros.
+//      output tile list) from a pinned staging buffer, once per block STRUCTURE
+//      (plans are cached on the device).
+//   2. pairing kernel (ON DEVICE, one CTA, qn tables staged in shared memory):
+//      thread per output block o finds its contributing pairs (i asc, j asc) --
+//      exactly the reference's accumulation order restricted to o -- and writes
+//      a CSR (out_ptr, pair list); then the per-tile k-iteration counts
+//      (sum over the tile's pairs of ceil(K_i / BK)) are scanned into tile_kbeg.
+//   3. grouped stream-K GEMM (one persistent CTA per SM, warp-specialised like
+//      the dense path, gemm_sk.cuh): the k-iterations of ALL output tiles -- each
+//      tile's pairs concatenated in reference order -- form one flat iteration
+//      space split evenly over the CTAs, so the few large sectors no longer set
+//      the critical path. A producer warpgroup gathers A/B k-tiles pair by pair
+//      (index groups per block, cp.async into an mbarrier ring); 16 math warps
+//      only do LDS + DMMA. A tile split across CTAs is finished by the CTA that
+//      holds its last k-iteration, adding the earlier CTAs' partials in CTA
+//      order (deterministic, no data atomics; flags self-reset for the next
+//      launch). Tiles of blocks without pairs are stored as zeros.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <array>
 #include <map>
 #include <cstring>
@@ -27,12 +38,12 @@
 #include <unordered_map>
 #include <vector>
 
-#include "gemm_core.cuh"
+#include "gemm_sk.cuh"
 
 namespace tnb {
 namespace {
 
-struct BlockDesc {
+struct alignas(16) BlockDesc {
   Group free_g;  // A: rows (a_free), B: cols (b_free)
   Group k_g;     // contracted axes, in shared-label order (not merged; consistent across A/B)
   int32_t F;     // product of free dims
@@ -62,21 +73,37 @@ struct BsMeta {
   int32_t* pairs;     // [max pairs][2] (i, j) grouped by output block
   int32_t* err;       // [1]
   const uint8_t* mask;  // per-panel "compute here" flags (multi-GPU partition) or nullptr
+  int32_t* tile_kbeg;   // [ntiles+1] prefix sums of per-tile k-iterations, in SCHEDULE order
+  int32_t* tile_cnt;    // [ntiles] scratch: k-iterations per tile in list order
+  TileRef* stiles;      // [ntiles] the tiles in schedule order (written by the pairing kernel)
   int64_t max_pairs;
+  int bk;               // k-tile depth of the GEMM (per-tile iteration counts)
+  int qn_smem;          // qn tables fit in the pairing kernel's shared memory
+  int sched_smem;       // bytes of schedule tables the GEMM stages in shared memory (0 = read from global)
+  int desc_smem;        // the GEMM also stages the block descriptors (da, db) in shared memory
 };
 
+// Schedule tables the grouped GEMM reads on every segment / pair switch (dependent
+// loads): staged once per CTA in shared memory, right after the GEMM's own buffers.
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) / 16 * 16; }
+__host__ __device__ inline size_t sched_bytes(int ntiles, int nout, int64_t npairs) {
+  return al16((size_t)(ntiles + 1) * 4) + (size_t)ntiles * 16 + al16((size_t)(nout + 1) * 4) +
+         al16((size_t)npairs * 8) + 2 * al16((size_t)nout * 4);
+}
+
 // ---- pairing: one CTA; thread per output block -----------------------------
-__device__ __forceinline__ bool a_matches(const BsMeta& m, int i, int o) {
-  const int32_t* aq = m.a_qn + (int64_t)i * m.ra;
-  const int32_t* oq = m.out_qn + (int64_t)o * m.ro;
+__device__ __forceinline__ bool a_matches(const BsMeta& m, const int32_t* aqn, const int32_t* oqn, int i, int o) {
+  const int32_t* aq = aqn + (int64_t)i * m.ra;
+  const int32_t* oq = oqn + (int64_t)o * m.ro;
   for (int f = 0; f < m.nfa; ++f)
     if (aq[m.a_free[f]] != oq[f]) return false;
   return true;
 }
-__device__ __forceinline__ bool b_matches(const BsMeta& m, int i, int j, int o) {
-  const int32_t* aq = m.a_qn + (int64_t)i * m.ra;
-  const int32_t* bq = m.b_qn + (int64_t)j * m.rb;
-  const int32_t* oq = m.out_qn + (int64_t)o * m.ro + m.nfa;
+__device__ __forceinline__ bool b_matches(const BsMeta& m, const int32_t* aqn, const int32_t* bqn,
+                                          const int32_t* oqn, int i, int j, int o) {
+  const int32_t* aq = aqn + (int64_t)i * m.ra;
+  const int32_t* bq = bqn + (int64_t)j * m.rb;
+  const int32_t* oq = oqn + (int64_t)o * m.ro + m.nfa;
   for (int c = 0; c < m.nc; ++c)
     if (aq[m.a_axes[c]] != bq[m.b_axes[c]]) return false;
   for (int f = 0; f < m.nfb; ++f)
@@ -84,29 +111,16 @@ __device__ __forceinline__ bool b_matches(const BsMeta& m, int i, int j, int o) 
   return true;
 }
 
-__global__ void __launch_bounds__(1024) bs_pair_kernel(const BsMeta m) {
+// In place: a[0..n) := inclusive prefix sums (one CTA, blockDim a multiple of 32).
+__device__ void cta_inclusive_scan(int32_t* a, int n) {
   __shared__ int32_t carry;
   __shared__ int32_t wsum[32];
-  int32_t* cnt = m.out_ptr + 1;  // counts first, then scanned in place
-  for (int o = threadIdx.x; o < m.nout; o += blockDim.x) {
-    int c = 0;
-    for (int i = 0; i < m.na; ++i) {
-      if (!a_matches(m, i, o)) continue;
-      for (int j = 0; j < m.nb; ++j) c += b_matches(m, i, j, o) ? 1 : 0;
-    }
-    cnt[o] = c;
-  }
-  __syncthreads();
-  // inclusive scan of cnt[0..nout) in chunks of blockDim
-  if (threadIdx.x == 0) {
-    carry = 0;
-    m.out_ptr[0] = 0;
-  }
+  if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int base = 0; base < m.nout; base += blockDim.x) {
-    int o = base + threadIdx.x;
-    int v = (o < m.nout) ? cnt[o] : 0;
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int o = base + threadIdx.x;
+    int v = (o < n) ? a[o] : 0;
     for (int s = 1; s < 32; s <<= 1) {
       int t = __shfl_up_sync(0xffffffffu, v, s);
       if (lane >= s) v += t;
@@ -122,12 +136,42 @@ __global__ void __launch_bounds__(1024) bs_pair_kernel(const BsMeta m) {
       wsum[lane] = w;
     }
     __syncthreads();
-    int incl = v + (warp > 0 ? wsum[warp - 1] : 0) + carry;
+    const int incl = v + (warp > 0 ? wsum[warp - 1] : 0) + carry;
     __syncthreads();
-    if (o < m.nout) cnt[o] = incl;
+    if (o < n) a[o] = incl;
     if (threadIdx.x == blockDim.x - 1) carry = incl;
     __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(1024) bs_pair_kernel(const BsMeta m) {
+  extern __shared__ int32_t qsm[];
+  // the qn tables are re-read O(nout * (na + pairs * nb)) times: stage them on chip
+  const int32_t* aqn = m.a_qn;
+  const int32_t* bqn = m.b_qn;
+  const int32_t* oqn = m.out_qn;
+  if (m.qn_smem) {
+    const int na_ = m.na * m.ra, nb_ = m.nb * m.rb, no_ = m.nout * m.ro;
+    for (int x = threadIdx.x; x < na_; x += blockDim.x) qsm[x] = m.a_qn[x];
+    for (int x = threadIdx.x; x < nb_; x += blockDim.x) qsm[na_ + x] = m.b_qn[x];
+    for (int x = threadIdx.x; x < no_; x += blockDim.x) qsm[na_ + nb_ + x] = m.out_qn[x];
+    aqn = qsm;
+    bqn = qsm + na_;
+    oqn = qsm + na_ + nb_;
+    __syncthreads();
+  }
+  int32_t* cnt = m.out_ptr + 1;  // counts first, then scanned in place
+  for (int o = threadIdx.x; o < m.nout; o += blockDim.x) {
+    int c = 0;
+    for (int i = 0; i < m.na; ++i) {
+      if (!a_matches(m, aqn, oqn, i, o)) continue;
+      for (int j = 0; j < m.nb; ++j) c += b_matches(m, aqn, bqn, oqn, i, j, o) ? 1 : 0;
+    }
+    cnt[o] = c;
+  }
+  if (threadIdx.x == 0) m.out_ptr[0] = 0;
+  __syncthreads();
+  cta_inclusive_scan(cnt, m.nout);
   // write pairs of each output block in reference order (i asc, j asc)
   if (m.out_ptr[m.nout] > m.max_pairs) {
     if (threadIdx.x == 0) m.err[0] = 1;
@@ -136,24 +180,57 @@ __global__ void __launch_bounds__(1024) bs_pair_kernel(const BsMeta m) {
   for (int o = threadIdx.x; o < m.nout; o += blockDim.x) {
     int p = m.out_ptr[o];
     for (int i = 0; i < m.na; ++i) {
-      if (!a_matches(m, i, o)) continue;
+      if (!a_matches(m, aqn, oqn, i, o)) continue;
       for (int j = 0; j < m.nb; ++j)
-        if (b_matches(m, i, j, o)) {
+        if (b_matches(m, aqn, bqn, oqn, i, j, o)) {
           m.pairs[2 * p] = i;
           m.pairs[2 * p + 1] = j;
           ++p;
         }
     }
   }
+  __syncthreads();
+  // k-iterations per output tile (0 for tiles of other ranks' panels)
+  for (int t = threadIdx.x; t < m.ntiles; t += blockDim.x) {
+    const TileRef tr = m.tiles[t];
+    int c = 0;
+    if (!m.mask || m.mask[tr.panel])
+      for (int p = m.out_ptr[tr.o]; p < m.out_ptr[tr.o + 1]; ++p) c += (m.da[m.pairs[2 * p]].K + m.bk - 1) / m.bk;
+    m.tile_cnt[t] = c;
+  }
+  __syncthreads();
+  // schedule order: tiles ranked by k-iterations (descending, stable), laid out
+  // big, small, big, small, ... so that every stream-K range holds at most a few
+  // short segments (each segment / pair switch has a fixed gather set-up latency)
+  const bool reorder = m.ntiles <= 4096;
+  for (int t = threadIdx.x; t < m.ntiles; t += blockDim.x) {
+    int pos = t;
+    if (reorder) {
+      const int ct = m.tile_cnt[t];
+      int r = 0;
+      for (int u = 0; u < m.ntiles; ++u) {
+        const int cu = m.tile_cnt[u];
+        r += (cu > ct || (cu == ct && u < t)) ? 1 : 0;
+      }
+      const int half = (m.ntiles + 1) / 2;
+      pos = r < half ? 2 * r : 2 * (m.ntiles - 1 - r) + 1;
+    }
+    m.stiles[pos] = m.tiles[t];
+    m.tile_kbeg[pos + 1] = m.tile_cnt[t];
+  }
+  if (threadIdx.x == 0) m.tile_kbeg[0] = 0;
+  __syncthreads();
+  cta_inclusive_scan(m.tile_kbeg + 1, m.ntiles);
 }
 
-// ---- grouped GEMM: one CTA per output tile ------------------------------------
+// ---- grouped stream-K GEMM --------------------------------------------------
 template <bool CPLX, int MODE>
-struct BsCfg;
-template <int MODE>
-struct BsCfg<false, MODE> { using Core = TileCore<false, 0, 64, 64, 16, 2, 2, 3>; };
-template <int MODE>
-struct BsCfg<true, MODE> { using Core = TileCore<true, MODE, 64, 64, 8, 2, 2, 3>; };
+struct BsCfg {
+  // 64x64 tiles suit the sector sizes; at this tile size the gather rate, not the DMMA
+  // rate, is the limit, so two producer warpgroups feed the 16 math warps
+  static constexpr int BM = 64, BN = 64, BK = CPLX ? 8 : 16, WM = 4, WN = 4, STAGES = 8, NPROD = 256;
+  using Core = SKCore<CPLX, MODE, BM, BN, BK, WM, WN, STAGES, NPROD>;
+};
 
 // Per-call data pointers (A blocks, B blocks, output blocks) travel as a kernel
 // parameter when they fit, so a cached plan needs no per-call H2D copy.
@@ -162,31 +239,325 @@ struct PtrTable {
   const void* p[kInlinePtrs];
 };
 
-template <bool CPLX, int MODE>
-__global__ void __launch_bounds__(128, 2) bs_gemm_kernel(const __grid_constant__ BsMeta m,
-                                                         const __grid_constant__ PtrTable pt) {
-  using Core = typename BsCfg<CPLX, MODE>::Core;
+struct BsSK {
+  double* ws;  // [G][ACCN][NMATH] register partials
+  int* flags;  // [G], zero between launches (consumers reset them)
+  // dev instrumentation (TNB_BS_TRACE=file): per CTA [kTraceW] int64 of %globaltimer stamps
+  long long* trace;
+};
+constexpr int kTraceW = 64;
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <bool CPLX, int MODE, bool AMF, bool BNF>
+__global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
+    bs_sk_kernel(const __grid_constant__ BsMeta m, const __grid_constant__ PtrTable pt, const BsSK sk) {
+  using Cfg = BsCfg<CPLX, MODE>;
+  using Core = typename Cfg::Core;
+  using Base = typename Core::Base;
   using T = typename Core::T;
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
+  constexpr int NMATH = Core::NMATH, NPROD = Core::NPROD, ES = Core::ES;
+  constexpr int LDA = Core::LDA, LDB = Core::LDB, EA = Core::EA, EB = Core::EB;
   extern __shared__ __align__(16) unsigned char smem[];
+  T* As = reinterpret_cast<T*>(smem);
+  T* Bs = As + STAGES * BK * LDA;
+  int64_t* rowOffA = reinterpret_cast<int64_t*>(Bs + STAGES * BK * LDB);
+  int64_t* colOffB = rowOffA + BM;
+  int64_t* kOffA = colOffB + BN;    // [2][BK]
+  int64_t* kOffB = kOffA + 2 * BK;  // [2][BK]
+  uint64_t* full = reinterpret_cast<uint64_t*>(kOffB + 2 * BK);
+  uint64_t* empty = full + STAGES;
+
   const void* const* ptrs = m.ptrs ? m.ptrs : pt.p;
-  const TileRef t = m.tiles[blockIdx.x];
-  if (m.mask && !m.mask[t.panel]) return;  // panel owned by another rank
-  const int M = m.out_M[t.o], N = m.out_N[t.o];
-  typename Core::Acc acc;
-  Core::zero(acc);
-  const int p0 = m.out_ptr[t.o], p1 = m.out_ptr[t.o + 1];
-  for (int p = p0; p < p1; ++p) {
-    const int i = m.pairs[2 * p], j = m.pairs[2 * p + 1];
-    const BlockDesc& da = m.da[i];
-    const BlockDesc& db = m.db[j];
-    const T* A = static_cast<const T*>(ptrs[i]);
-    const T* B = static_cast<const T*>(ptrs[m.na + j]);
-    const bool a_mfast = da.free_g.n > 0 && da.free_g.stride[da.free_g.n - 1] == 1;
-    const bool b_nfast = db.free_g.n > 0 && db.free_g.stride[db.free_g.n - 1] == 1;
-    Core::mainloop(smem, A, B, da.free_g, da.k_g, db.k_g, db.free_g, t.m0, t.n0, M, N, 0, da.K, a_mfast, b_nfast,
-                   acc);
+  const int tid = threadIdx.x;
+  const int c = blockIdx.x;
+  const int* kbeg = m.tile_kbeg;
+  const TileRef* tiles = m.stiles;
+  const BlockDesc* DA = m.da;
+  const BlockDesc* DB = m.db;
+  const int32_t* optr = m.out_ptr;
+  const int32_t* pairs = m.pairs;
+  const int32_t* oM = m.out_M;
+  const int32_t* oN = m.out_N;
+  if (m.sched_smem) {
+    // one round of independent loads instead of a chain of dependent ones per segment
+    unsigned char* q = smem + al16(Core::kSmem);
+    int32_t* s_kbeg = reinterpret_cast<int32_t*>(q);
+    q += al16((size_t)(m.ntiles + 1) * 4);
+    TileRef* s_tiles = reinterpret_cast<TileRef*>(q);
+    q += (size_t)m.ntiles * 16;
+    int32_t* s_optr = reinterpret_cast<int32_t*>(q);
+    q += al16((size_t)(m.nout + 1) * 4);
+    int32_t* s_pairs = reinterpret_cast<int32_t*>(q);
+    q += al16((size_t)m.max_pairs * 8);
+    int32_t* s_oM = reinterpret_cast<int32_t*>(q);
+    q += al16((size_t)m.nout * 4);
+    int32_t* s_oN = reinterpret_cast<int32_t*>(q);
+    for (int x = tid; x <= m.ntiles; x += blockDim.x) s_kbeg[x] = kbeg[x];
+    for (int x = tid; x < m.ntiles; x += blockDim.x) s_tiles[x] = tiles[x];
+    for (int x = tid; x <= m.nout; x += blockDim.x) s_optr[x] = optr[x];
+    for (int x = tid; x < 2 * m.max_pairs; x += blockDim.x) s_pairs[x] = pairs[x];
+    for (int x = tid; x < m.nout; x += blockDim.x) {
+      s_oM[x] = oM[x];
+      s_oN[x] = oN[x];
+    }
+    if (m.desc_smem) {
+      // block descriptors: read on every pair switch by the producers
+      q += al16((size_t)m.nout * 4);
+      uint4* s_d = reinterpret_cast<uint4*>(q);
+      const int na16 = (int)(sizeof(BlockDesc) * m.na / 16), nb16 = (int)(sizeof(BlockDesc) * m.nb / 16);
+      const uint4* ga = reinterpret_cast<const uint4*>(m.da);
+      const uint4* gb = reinterpret_cast<const uint4*>(m.db);
+      for (int x = tid; x < na16 + nb16; x += blockDim.x) s_d[x] = x < na16 ? ga[x] : gb[x - na16];
+      DA = reinterpret_cast<const BlockDesc*>(s_d);
+      DB = reinterpret_cast<const BlockDesc*>(s_d + na16);
+    }
+    kbeg = s_kbeg;
+    tiles = s_tiles;
+    optr = s_optr;
+    pairs = s_pairs;
+    oM = s_oM;
+    oN = s_oN;
   }
-  Core::store(static_cast<T*>(const_cast<void*>(ptrs[m.na + m.nb + t.o])), N, t.m0, t.n0, M, N, acc);
+  __syncthreads();
+  const int64_t total = kbeg[m.ntiles];
+  // stream-K participants: >= 4 k-iterations each, so no participant has an empty range
+  // (an owner waits on EVERY participant between a tile's first CTA and itself)
+  const int G = (int)min((int64_t)gridDim.x, max(total / 4, (int64_t)1));
+  const int64_t it0 = c < G ? detail::sk_begin(total, G, c) : 0;
+  const int64_t it1 = c < G ? detail::sk_begin(total, G, c + 1) : 0;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      detail::mbar_init(&full[s], NPROD);
+      detail::mbar_init(&empty[s], NMATH / 32);
+    }
+  }
+  __syncthreads();
+  // largest tile t with kbeg[t] <= x (skips empty tiles, whose kbeg equals the next one's)
+  auto tile_of = [&](int64_t x) {
+    int lo = 0, hi = m.ntiles - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (kbeg[mid] <= x) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
+  };
+
+  if (tid >= NMATH) {
+    // ================================================================ producer
+    const int p = tid - NMATH;
+    auto mapA = [&](int i, int& mm, int& kk) {
+      const int e = p + i * NPROD;
+      if (AMF) { mm = e % BM; kk = e / BM; }
+      else { kk = (e & 3) + 4 * (e / (4 * BM)); mm = (e >> 2) % BM; }
+    };
+    auto mapB = [&](int i, int& nn, int& kk) {
+      const int e = p + i * NPROD;
+      if (BNF) { nn = e % BN; kk = e / BN; }
+      else { kk = (e & 3) + 4 * (e / (4 * BN)); nn = (e >> 2) % BN; }
+    };
+    constexpr int RA = AMF ? 1 : 4, RB = BNF ? 1 : 4;
+    const uint32_t sAbase = smem_u32(As), sBbase = smem_u32(Bs);
+    constexpr uint32_t stA = BK * LDA * ES, stB = BK * LDB * ES;
+    int64_t gi = 0;
+    for (int64_t e = it1; e > it0;) {
+      const int t = tile_of(e - 1);
+      const int64_t tstart = kbeg[t];
+      const int64_t sb = it0 > tstart ? it0 : tstart;
+      const TileRef tr = tiles[t];
+      const int M = oM[tr.o], N = oN[tr.o];
+      // walk the tile's pairs (reference order) over local k-iterations [sb, e) - tstart
+      int64_t kt = sb - tstart;
+      const int64_t kend = e - tstart;
+      int64_t pbase = 0;
+      for (int q = optr[tr.o]; q < optr[tr.o + 1] && kt < kend; ++q) {
+        const int i = pairs[2 * q], j = pairs[2 * q + 1];
+        const BlockDesc& da = DA[i];
+        const BlockDesc& db = DB[j];
+        const int nkt = (da.K + BK - 1) / BK;
+        if (kt >= pbase + nkt) {
+          pbase += nkt;
+          continue;
+        }
+        const T* A = static_cast<const T*>(ptrs[i]);
+        const T* B = static_cast<const T*>(ptrs[m.na + j]);
+        detail::named_sync(1, NPROD);  // previous pair's table reads are done
+        for (int x = p; x < BM + BN; x += NPROD) {
+          if (x < BM) rowOffA[x] = (tr.m0 + x < M) ? group_offset(da.free_g, tr.m0 + x) : -1;
+          else colOffB[x - BM] = (tr.n0 + x - BM < N) ? group_offset(db.free_g, tr.n0 + x - BM) : -1;
+        }
+        detail::named_sync(1, NPROD);
+        // affine k-tiles (K group of one digit, or an innermost digit that BK divides):
+        // offset(k0 + kk) = offset(k0) + kk * stride_inner -- no per-k table, no barrier
+        const int nA = da.k_g.n, nB = db.k_g.n;
+        const bool aff = (nA <= 1 || da.k_g.dim[nA - 1] % BK == 0) && (nB <= 1 || db.k_g.dim[nB - 1] % BK == 0);
+        const int64_t ksA = nA ? da.k_g.stride[nA - 1] : 0, ksB = nB ? db.k_g.stride[nB - 1] : 0;
+        const int Kp = da.K;
+        int64_t rA[RA], rB[RB];
+#pragma unroll
+        for (int jj = 0; jj < RA; ++jj) {
+          int mm, kk;
+          mapA(jj, mm, kk);
+          rA[jj] = rowOffA[mm];
+        }
+#pragma unroll
+        for (int jj = 0; jj < RB; ++jj) {
+          int nn, kk;
+          mapB(jj, nn, kk);
+          rB[jj] = colOffB[nn];
+        }
+        // this thread's gather sources for the whole pair (nullptr = padding row/col);
+        // per k-tile only the k offset moves
+        const T* pA[EA];
+        const T* pB[EB];
+#pragma unroll
+        for (int x = 0; x < EA; ++x) {
+          int mm, kk;
+          mapA(x, mm, kk);
+          const int64_t ro = rA[x % RA];
+          pA[x] = ro >= 0 ? A + (ro + (int64_t)kk * ksA) : nullptr;
+        }
+#pragma unroll
+        for (int x = 0; x < EB; ++x) {
+          int nn, kk;
+          mapB(x, nn, kk);
+          const int64_t co = rB[x % RB];
+          pB[x] = co >= 0 ? B + (co + (int64_t)kk * ksB) : nullptr;
+        }
+        const int64_t lend = (kend - pbase) < nkt ? (kend - pbase) : nkt;
+        for (int64_t lk = kt - pbase; lk < lend; ++lk, ++gi) {
+          const int s = (int)(gi % STAGES);
+          const int k0 = (int)lk * BK;
+          if (aff) {
+            // per-element base addresses are fixed for the whole pair; only the k offset moves
+            const int64_t koA = nA == 0 ? 0 : (nA == 1 ? (int64_t)k0 * ksA : group_offset(da.k_g, k0));
+            const int64_t koB = nB == 0 ? 0 : (nB == 1 ? (int64_t)k0 * ksB : group_offset(db.k_g, k0));
+            const int krem = Kp - k0;  // >= BK: whole k-tile
+            if (gi >= STAGES) detail::mbar_wait(&empty[s], (uint32_t)(((gi / STAGES) & 1) ^ 1));
+            const uint32_t sa = sAbase + s * stA, sbb = sBbase + s * stB;
+#pragma unroll
+            for (int x = 0; x < EA; ++x) {
+              int mm, kk;
+              mapA(x, mm, kk);
+              const bool v = pA[x] != nullptr && kk < krem;
+              const T* src = v ? pA[x] + koA : A;
+              const uint32_t dst = sa + (uint32_t)(kk * LDA + mm) * ES;
+              if constexpr (CPLX)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
+              else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0));
+            }
+#pragma unroll
+            for (int x = 0; x < EB; ++x) {
+              int nn, kk;
+              mapB(x, nn, kk);
+              const bool v = pB[x] != nullptr && kk < krem;
+              const T* src = v ? pB[x] + koB : B;
+              const uint32_t dst = sbb + (uint32_t)(kk * LDB + nn) * ES;
+              if constexpr (CPLX)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
+              else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0));
+            }
+            detail::cp_async_mbar_arrive_noinc(&full[s]);
+            continue;
+          }
+          const int slot = (int)(gi & 1);
+          for (int x = p; x < 2 * BK; x += NPROD) {
+            const int kk = x % BK, k = k0 + kk;
+            const bool v = k < da.K;
+            if (x < BK) kOffA[slot * BK + kk] = v ? group_offset(da.k_g, k) : -1;
+            else kOffB[slot * BK + kk] = v ? group_offset(db.k_g, k) : -1;
+          }
+          detail::named_sync(1, NPROD);
+          if (gi >= STAGES) detail::mbar_wait(&empty[s], (uint32_t)(((gi / STAGES) & 1) ^ 1));
+          const int64_t* ka = kOffA + slot * BK;
+          const int64_t* kb = kOffB + slot * BK;
+#pragma unroll
+          for (int x = 0; x < EA; ++x) {
+            int mm, kk;
+            mapA(x, mm, kk);
+            const int64_t ro = rA[x % RA], ko = ka[kk];
+            const bool v = (ro >= 0) && (ko >= 0);
+            const T* src = v ? A + ro + ko : A;
+            const uint32_t dst = sAbase + s * stA + (uint32_t)(kk * LDA + mm) * ES;
+            if constexpr (CPLX)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
+            else
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0));
+          }
+#pragma unroll
+          for (int x = 0; x < EB; ++x) {
+            int nn, kk;
+            mapB(x, nn, kk);
+            const int64_t co = rB[x % RB], ko = kb[kk];
+            const bool v = (co >= 0) && (ko >= 0);
+            const T* src = v ? B + co + ko : B;
+            const uint32_t dst = sBbase + s * stB + (uint32_t)(kk * LDB + nn) * ES;
+            if constexpr (CPLX)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
+            else
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0));
+          }
+          detail::cp_async_mbar_arrive_noinc(&full[s]);
+        }
+        kt = pbase + lend;
+        pbase += nkt;
+      }
+      e = sb;
+    }
+    cp_async_wait<0>();
+    return;
+  }
+
+  // ================================================================== math warps
+  typename Core::Acc acc;
+  // tiles whose output block has no pair (or whose rank owns them but K is empty) are zeros
+  Base::zero(acc);
+  for (int t = c; t < m.ntiles; t += gridDim.x) {
+    if (kbeg[t + 1] != kbeg[t]) continue;
+    const TileRef tr = tiles[t];
+    if (m.mask && !m.mask[tr.panel]) continue;
+    const int M = oM[tr.o], N = oN[tr.o];
+    Base::store(static_cast<T*>(const_cast<void*>(ptrs[m.na + m.nb + tr.o])), N, tr.m0, tr.n0, M, N, acc);
+  }
+  int64_t gi = 0;
+  long long* tr_ = (sk.trace && tid == 0) ? sk.trace + (size_t)c * kTraceW : nullptr;
+  int nseg = 0;
+  if (tr_) tr_[0] = gtimer();
+  for (int64_t e = it1; e > it0;) {
+    const int t = tile_of(e - 1);
+    const int64_t tstart = kbeg[t], tend = kbeg[t + 1];
+    const int64_t sb = it0 > tstart ? it0 : tstart;
+    Base::zero(acc);
+    Core::consume(As, Bs, full, empty, gi, (int)(e - sb), acc);
+    if (tr_ && nseg < 15) tr_[4 + 4 * nseg] = gtimer();
+    if (e < tend) {
+      Core::publish(sk.ws, sk.flags, c, acc);
+    } else {
+      if (sb > tstart) Core::absorb(sk.ws, sk.flags, detail::sk_cta_of(total, G, tstart), c, acc, true);
+      const TileRef tr = tiles[t];
+      const int M = oM[tr.o], N = oN[tr.o];
+      Base::store(static_cast<T*>(const_cast<void*>(ptrs[m.na + m.nb + tr.o])), N, tr.m0, tr.n0, M, N, acc);
+    }
+    if (tr_ && nseg < 15) {
+      tr_[5 + 4 * nseg] = gtimer();
+      tr_[6 + 4 * nseg] = t;
+      tr_[7 + 4 * nseg] = e - sb;
+    }
+    ++nseg;
+    e = sb;
+  }
+  if (tr_) {
+    tr_[1] = gtimer();
+    tr_[2] = nseg;
+    tr_[3] = it1 - it0;
+  }
 }
 
 // ---- host ---------------------------------------------------------------------
@@ -230,6 +601,7 @@ struct Plan {
   int64_t npairs = 0;
   size_t o_optr = 0, o_pairs = 0;
   int dtype = 0;
+  bool amf = true, bnf = true;  // operand gather orientation (coalescing only)
 };
 
 struct PlanCache {
@@ -239,22 +611,91 @@ struct PlanCache {
   void* stage = nullptr;  // pinned staging for large pointer tables
   size_t stage_cap = 0;
   cudaEvent_t stage_ev = nullptr;
+  // stream-K partials + flags, shared by all plans of this device. Launches are
+  // serialised through ws_ev when they come from different streams.
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  cudaEvent_t ws_ev = nullptr;
+  cudaStream_t ws_stream = nullptr;
 };
 PlanCache g_cache;
 
-template <bool CPLX, int MODE>
-int launch_bs(const BsMeta& meta, const PtrTable* pt, cudaStream_t st) {
+template <bool CPLX, int MODE, bool AMF, bool BNF>
+int launch_bs_one(const BsMeta& meta, const PtrTable* pt, const BsSK& sk, int G, cudaStream_t st) {
   using Core = typename BsCfg<CPLX, MODE>::Core;
-  auto kern = bs_gemm_kernel<CPLX, MODE>;
-  static bool configured = false;
-  if (!configured) {
-    TNB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Core::kSmem));
-    configured = true;
+  auto kern = bs_sk_kernel<CPLX, MODE, AMF, BNF>;
+  const size_t smem = al16(Core::kSmem) + (size_t)meta.sched_smem;
+  static size_t configured = 0;
+  if (configured < smem) {
+    TNB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
   }
-  if (meta.ntiles > 0) {
-    kern<<<meta.ntiles, Core::NT, Core::kSmem, st>>>(meta, *pt);
-    count_launch();
-    TNB_CUDA_CHECK(cudaGetLastError());
+  {
+    KTimer kt(TNB_KF_BS_GEMM, st, 0.0);
+    kern<<<G, Core::NT, smem, st>>>(meta, *pt, sk);
+  }
+  count_launch();
+  TNB_CUDA_CHECK(cudaGetLastError());
+  return TNB_OK;
+}
+
+// Caller holds g_cache.mu.
+template <bool CPLX, int MODE>
+int launch_bs(const Plan& plan, const BsMeta& meta, const PtrTable* pt, cudaStream_t st) {
+  using Core = typename BsCfg<CPLX, MODE>::Core;
+  if (meta.ntiles == 0) return TNB_OK;
+  const int G = sm_count();  // one persistent CTA per SM (all co-resident: stream-K hand-offs)
+  const size_t ws_need = (size_t)G * Core::ACCN * Core::NMATH * 8;
+  const size_t need = ws_need + (size_t)G * 4 + 64;
+  if (g_cache.ws_bytes < need) {
+    if (g_cache.ws) {
+      TNB_CUDA_CHECK(cudaDeviceSynchronize());
+      cudaFree(g_cache.ws);
+      g_cache.ws = nullptr;
+      g_cache.ws_bytes = 0;
+    }
+    // sized for the larger (complex) accumulator set so both dtypes share it
+    using CCore = typename BsCfg<true, 0>::Core;
+    const size_t want = std::max(need, (size_t)G * CCore::ACCN * CCore::NMATH * 8 + (size_t)G * 4 + 64);
+    TNB_CUDA_CHECK(cudaMalloc(&g_cache.ws, want));
+    TNB_CUDA_CHECK(cudaMemset(g_cache.ws, 0, want));
+    g_cache.ws_bytes = want;
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  TNB_CUDA_CHECK(cudaStreamIsCapturing(st, &cs));
+  const bool capturing = cs != cudaStreamCaptureStatusNone;
+  if (!capturing && g_cache.ws_ev && g_cache.ws_stream != st) TNB_CUDA_CHECK(cudaStreamWaitEvent(st, g_cache.ws_ev, 0));
+  BsSK sk;
+  sk.ws = static_cast<double*>(g_cache.ws);
+  // flags live after the largest partial area (fixed offset for both dtypes)
+  using CCore = typename BsCfg<true, 0>::Core;
+  sk.flags = reinterpret_cast<int*>(static_cast<char*>(g_cache.ws) + (size_t)G * CCore::ACCN * CCore::NMATH * 8);
+  sk.trace = nullptr;
+  static const char* trace_path = getenv("TNB_BS_TRACE");
+  if (trace_path && !capturing) {
+    TNB_CUDA_CHECK(cudaMallocAsync((void**)&sk.trace, (size_t)G * kTraceW * 8, st));
+    TNB_CUDA_CHECK(cudaMemsetAsync(sk.trace, 0, (size_t)G * kTraceW * 8, st));
+  }
+  int rc;
+  if (plan.amf && plan.bnf) rc = launch_bs_one<CPLX, MODE, true, true>(meta, pt, sk, G, st);
+  else if (plan.amf) rc = launch_bs_one<CPLX, MODE, true, false>(meta, pt, sk, G, st);
+  else if (plan.bnf) rc = launch_bs_one<CPLX, MODE, false, true>(meta, pt, sk, G, st);
+  else rc = launch_bs_one<CPLX, MODE, false, false>(meta, pt, sk, G, st);
+  if (rc) return rc;
+  if (sk.trace) {
+    std::vector<long long> h((size_t)G * kTraceW);
+    TNB_CUDA_CHECK(cudaMemcpyAsync(h.data(), sk.trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    TNB_CUDA_CHECK(cudaStreamSynchronize(st));
+    cudaFreeAsync(sk.trace, st);
+    if (FILE* f = fopen(trace_path, "ab")) {
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+  }
+  if (!capturing) {
+    if (!g_cache.ws_ev) TNB_CUDA_CHECK(cudaEventCreateWithFlags(&g_cache.ws_ev, cudaEventDisableTiming));
+    TNB_CUDA_CHECK(cudaEventRecord(g_cache.ws_ev, st));
+    g_cache.ws_stream = st;
   }
   return TNB_OK;
 }
@@ -375,7 +816,28 @@ extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int r
     for (int j = 0; j < nb; ++j)
       if (!block_desc(rank_b, b_shape + (int64_t)j * rank_b, b_perm, bcon.data(), b_axes, db[j]))
         return fail(TNB_EUNSUP, "bs_contract: block index group too large");
+    // gather orientation (the dense rule of gemm.cu per block), majority by block work
+    {
+      double wa[2] = {0, 0}, wb[2] = {0, 0};
+      for (int i = 0; i < na; ++i) {
+        const Group& f = da[i].free_g;
+        const Group& k = da[i].k_g;
+        const bool fast = (f.n > 0 && f.stride[f.n - 1] == 1 && f.dim[f.n - 1] >= 4) ||
+                          !(k.n > 0 && k.stride[k.n - 1] == 1);
+        wa[fast ? 1 : 0] += (double)da[i].F * da[i].K;
+      }
+      for (int j = 0; j < nb; ++j) {
+        const Group& f = db[j].free_g;
+        const Group& k = db[j].k_g;
+        const bool fast = (f.n > 0 && f.stride[f.n - 1] == 1 && f.dim[f.n - 1] >= 4) ||
+                          !(k.n > 0 && k.stride[k.n - 1] == 1);
+        wb[fast ? 1 : 0] += (double)db[j].F * db[j].K;
+      }
+      plan.amf = wa[1] >= wa[0];
+      plan.bnf = wb[1] >= wb[0];
+    }
     const int BM = 64, BN = 64;
+    meta.bk = (dtype == TNB_C128) ? BsCfg<true, 0>::BK : BsCfg<false, 0>::BK;
     std::vector<int32_t> oM(nout), oN(nout);
     std::vector<TileRef> tiles;
     int32_t panel = 0;
@@ -413,6 +875,14 @@ extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int r
       }
     }
     meta.max_pairs = std::max<int64_t>(exact_pairs, 1);
+    {
+      static_assert(sizeof(BlockDesc) % 16 == 0, "block descriptors are staged as uint4");
+      const size_t sb = sched_bytes((int)tiles.size(), nout, meta.max_pairs);
+      const size_t db_bytes = sizeof(BlockDesc) * (size_t)(na + nb);
+      meta.sched_smem = sb <= 32 * 1024 ? (int)sb : 0;
+      meta.desc_smem = (meta.sched_smem && db_bytes <= 48 * 1024) ? 1 : 0;
+      if (meta.desc_smem) meta.sched_smem += (int)db_bytes;
+    }
     size_t off = 0;
     auto take = [&](size_t bytes) {
       size_t o = align_up(off, 16);
@@ -425,7 +895,9 @@ extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int r
                  o_tiles = take(sizeof(TileRef) * tiles.size()),
                  o_mask = take(panel_mask ? (size_t)npanels : 0);
     const size_t upload = off;
-    const size_t o_optr = take((size_t)(nout + 1) * 4), o_err = take(16), o_pairs = take((size_t)meta.max_pairs * 8);
+    const size_t o_optr = take((size_t)(nout + 1) * 4), o_err = take(16), o_pairs = take((size_t)meta.max_pairs * 8),
+                 o_kbeg = take((size_t)(tiles.size() + 1) * 4), o_tcnt = take((size_t)tiles.size() * 4),
+                 o_stiles = take(sizeof(TileRef) * tiles.size());
     const size_t total = off;
     std::vector<unsigned char> h(upload);
     memcpy(h.data() + o_aqn, a_qn, (size_t)na * rank_a * 4);
@@ -453,8 +925,19 @@ extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int r
     meta.err = reinterpret_cast<int32_t*>(dblob + o_err);
     meta.pairs = reinterpret_cast<int32_t*>(dblob + o_pairs);
     meta.mask = panel_mask ? reinterpret_cast<const uint8_t*>(dblob + o_mask) : nullptr;
+    meta.tile_kbeg = reinterpret_cast<int32_t*>(dblob + o_kbeg);
+    meta.tile_cnt = reinterpret_cast<int32_t*>(dblob + o_tcnt);
+    meta.stiles = reinterpret_cast<TileRef*>(dblob + o_stiles);
     meta.ptrs = nullptr;
-    bs_pair_kernel<<<1, 1024, 0, st>>>(meta);
+    const size_t qn_bytes = ((size_t)na * rank_a + (size_t)nb * rank_b + (size_t)nout * ro) * 4;
+    meta.qn_smem = qn_bytes <= 160 * 1024;
+    const size_t pair_smem = meta.qn_smem ? qn_bytes : 0;
+    if (pair_smem > 48 * 1024)
+      TNB_CUDA_CHECK(cudaFuncSetAttribute(bs_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pair_smem));
+    {
+      KTimer kt(TNB_KF_BS_PAIR, st, 0.0);
+      bs_pair_kernel<<<1, 1024, pair_smem, st>>>(meta);
+    }
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -495,8 +978,8 @@ extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int r
     TNB_CUDA_CHECK(cudaEventRecord(g_cache.stage_ev, st));
     meta.ptrs = static_cast<const void* const*>(dptr);
   }
-  if (dtype == TNB_F64) rc = launch_bs<false, 0>(meta, &pt, st);
-  else rc = launch_bs<true, 0>(meta, &pt, st);
+  if (dtype == TNB_F64) rc = launch_bs<false, 0>(plan, meta, &pt, st);
+  else rc = launch_bs<true, 0>(plan, meta, &pt, st);
   if (meta.ptrs) cudaFreeAsync(const_cast<void*>(static_cast<const void*>(meta.ptrs)), st);
   if (rc != TNB_OK) return rc;
   if (npairs) *npairs = plan.npairs;

@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -25,6 +26,51 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 static std::atomic<long long> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// ---- kernel timer ----------------------------------------------------------
+struct KRec {
+  int family;
+  cudaEvent_t ev0, ev1;
+  double work;
+};
+static std::atomic<bool> g_kt_on{false};
+static std::mutex g_kt_mu;
+static std::vector<KRec> g_kt_recs;
+static std::vector<cudaEvent_t> g_kt_pool;
+
+static cudaEvent_t kt_event() {
+  if (!g_kt_pool.empty()) {
+    cudaEvent_t e = g_kt_pool.back();
+    g_kt_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return e;
+}
+
+KTimer::KTimer(int fam, cudaStream_t s, double w) : family(fam), st(s), work(w) {
+  if (!g_kt_on.load(std::memory_order_relaxed)) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return;
+  }
+  std::lock_guard<std::mutex> g(g_kt_mu);
+  ev0 = kt_event();
+  ev1 = kt_event();
+  if (ev0) cudaEventRecord(ev0, st);
+}
+
+KTimer::~KTimer() {
+  if (!ev0 || !ev1) return;
+  cudaEventRecord(ev1, st);
+  std::lock_guard<std::mutex> g(g_kt_mu);
+  g_kt_recs.push_back({family, ev0, ev1, work});
+}
 
 static int g_ndev = -1;
 static int g_sms = 0;
@@ -88,6 +134,43 @@ int tnb_set_device(int device) {
   int rc = tnb::require_device();
   if (rc) return rc;
   TNB_CUDA_CHECK(cudaSetDevice(device));
+  return TNB_OK;
+}
+
+int tnb_ktimer_enable(int on) {
+  tnb::g_kt_on.store(on != 0);
+  return TNB_OK;
+}
+
+int tnb_ktimer_reset(void) {
+  std::lock_guard<std::mutex> g(tnb::g_kt_mu);
+  for (auto& r : tnb::g_kt_recs) {
+    cudaEventSynchronize(r.ev1);
+    tnb::g_kt_pool.push_back(r.ev0);
+    tnb::g_kt_pool.push_back(r.ev1);
+  }
+  tnb::g_kt_recs.clear();
+  cudaGetLastError();
+  return TNB_OK;
+}
+
+int tnb_ktimer_read(int family, int64_t* launches, double* ms, double* work) {
+  if (!launches || !ms || !work) return tnb::fail(TNB_EINVAL, "ktimer_read: NULL argument");
+  std::lock_guard<std::mutex> g(tnb::g_kt_mu);
+  int64_t n = 0;
+  double t = 0.0, w = 0.0;
+  for (auto& r : tnb::g_kt_recs) {
+    if (r.family != family) continue;
+    TNB_CUDA_CHECK(cudaEventSynchronize(r.ev1));
+    float x = 0.f;
+    TNB_CUDA_CHECK(cudaEventElapsedTime(&x, r.ev0, r.ev1));
+    ++n;
+    t += x;
+    w += r.work;
+  }
+  *launches = n;
+  *ms = t;
+  *work = w;
   return TNB_OK;
 }
 

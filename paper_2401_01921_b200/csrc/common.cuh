@@ -28,6 +28,21 @@ int sm_count();
 // Counts every kernel this library launches (tnb_launch_count); bench.py reports it.
 void count_launch(int n = 1);
 
+// Per-family CUDA-event timing of this library's kernel launches (tnb_ktimer_*).
+// Construct right before a launch and let it go out of scope right after: when the
+// timer is enabled (and the stream is not being captured into a graph) it records
+// an event pair on the launching stream and the algorithmic work of the launch.
+struct KTimer {
+  KTimer(int family, cudaStream_t st, double work);
+  ~KTimer();
+  KTimer(const KTimer&) = delete;
+  KTimer& operator=(const KTimer&) = delete;
+  int family;
+  cudaStream_t st;
+  double work;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
 // Unsigned 32-bit division by a runtime-invariant divisor via multiply-high

@@ -225,7 +225,10 @@ int run_narrow(const void* A, const void* B, void* C, const GemmDesc& d, cudaStr
   }
   const int64_t chunks = ((int64_t)d.M + 31) / 32;
   const int64_t grid = std::min<int64_t>((chunks + WARPS - 1) / WARPS, (int64_t)sm_count() * per_sm);
-  kern<<<(unsigned)grid, WARPS * 32, 0, st>>>(static_cast<const T*>(A), static_cast<const T*>(B), static_cast<T*>(C), d);
+  {
+    KTimer kt(TNB_KF_GEMM_SKINNY, st, 2.0 * d.M * (double)d.N * d.K * (CPLX ? 4 : 1));
+    kern<<<(unsigned)grid, WARPS * 32, 0, st>>>(static_cast<const T*>(A), static_cast<const T*>(B), static_cast<T*>(C), d);
+  }
   count_launch();
   TNB_CUDA_CHECK(cudaGetLastError());
   return TNB_OK;
@@ -461,8 +464,11 @@ struct StreamK {
       TNB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Core::kSmem));
       configured = true;
     }
-    kern<<<sk.G, Core::NT, Core::kSmem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B), static_cast<T*>(C),
-                                              d, sk);
+    {
+      KTimer kt(TNB_KF_GEMM, st, 2.0 * d.M * (double)d.N * d.K * (CPLX ? 4 : 1));
+      kern<<<sk.G, Core::NT, Core::kSmem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B),
+                                                static_cast<T*>(C), d, sk);
+    }
     count_launch();
     TNB_CUDA_CHECK(cudaGetLastError());
     return TNB_OK;
@@ -509,7 +515,10 @@ int run_skinny(const void* A, const void* B, void* C, GemmDesc d, cudaStream_t s
   if (per_sm < 1) per_sm = 1;
   int64_t panels = (d.M + 127) / 128;
   int64_t grid = std::min<int64_t>(panels, (int64_t)sms() * per_sm);
-  kern<<<(unsigned)grid, 256, smem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B), static_cast<T*>(C), d);
+  {
+    KTimer kt(TNB_KF_GEMM_SKINNY, st, 2.0 * d.M * (double)d.N * d.K * (CPLX ? 4 : 1));
+    kern<<<(unsigned)grid, 256, smem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B), static_cast<T*>(C), d);
+  }
   count_launch();
   TNB_CUDA_CHECK(cudaGetLastError());
   return TNB_OK;

@@ -54,13 +54,13 @@ __device__ __forceinline__ int sk_cta_of(int64_t total, int G, int64_t x) {
 }
 }  // namespace detail
 
-template <bool CPLX, int MODE, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
+template <bool CPLX, int MODE, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int NPROD_ = 128>
 struct SKCore {
   using T = typename Elem<CPLX>::T;
   using Base = TileCore<CPLX, MODE, BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
   static constexpr int ES = CPLX ? 16 : 8;
   static constexpr int NMATH = WARPS_M * WARPS_N * 32;
-  static constexpr int NPROD = 128;
+  static constexpr int NPROD = NPROD_;  // producer threads (whole warpgroups)
   static constexpr int NT = NMATH + NPROD;
   static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
   static constexpr int MF = WTM / 8, NF = WTN / 8;
@@ -85,6 +85,103 @@ struct SKCore {
     const int in_g = t - g * per_group;
     m0 = (first_m + in_g % gsz) * BM;
     n0 = (in_g / gsz) * BN;
+  }
+
+  // Math warps: accumulate nk consecutive ring stages (gi = running stage counter).
+  __device__ __forceinline__ static void consume(const T* As, const T* Bs, uint64_t* full, uint64_t* empty, int64_t& gi, int nk,
+                                 Acc& acc) {
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+    const int arow = wm * WTM + (lane >> 2);
+    const int bcol = wn * WTN + (lane >> 2);
+    const int kq = lane & 3;
+    for (int kt = 0; kt < nk; ++kt, ++gi) {
+      const int s = (int)(gi % STAGES);
+      detail::mbar_wait(&full[s], (uint32_t)((gi / STAGES) & 1));
+      const T* as = As + s * BK * LDA;
+      const T* bs = Bs + s * BK * LDB;
+#pragma unroll
+      for (int k4 = 0; k4 < BK / 4; ++k4) {
+        const int kr = k4 * 4 + kq;
+        if constexpr (!CPLX) {
+          double af[MF], bf[NF];
+#pragma unroll
+          for (int i = 0; i < MF; ++i) af[i] = as[kr * LDA + arow + i * 8];
+#pragma unroll
+          for (int j = 0; j < NF; ++j) bf[j] = bs[kr * LDB + bcol + j * 8];
+#pragma unroll
+          for (int i = 0; i < MF; ++i)
+#pragma unroll
+            for (int j = 0; j < NF; ++j) dmma(acc[0][i][j][0], acc[0][i][j][1], af[i], bf[j]);
+        } else {
+          double2 af[MF], bf[NF];
+#pragma unroll
+          for (int i = 0; i < MF; ++i) af[i] = as[kr * LDA + arow + i * 8];
+#pragma unroll
+          for (int j = 0; j < NF; ++j) bf[j] = bs[kr * LDB + bcol + j * 8];
+          if constexpr (MODE == 0) {
+#pragma unroll
+            for (int i = 0; i < MF; ++i) {
+              const double ain = dneg(af[i].y);
+#pragma unroll
+              for (int j = 0; j < NF; ++j) {
+                dmma(acc[0][i][j][0], acc[0][i][j][1], af[i].x, bf[j].x);
+                dmma(acc[0][i][j][0], acc[0][i][j][1], ain, bf[j].y);
+                dmma(acc[1][i][j][0], acc[1][i][j][1], af[i].x, bf[j].y);
+                dmma(acc[1][i][j][0], acc[1][i][j][1], af[i].y, bf[j].x);
+              }
+            }
+          } else {
+            double bsum[NF];
+#pragma unroll
+            for (int j = 0; j < NF; ++j) bsum[j] = bf[j].x + bf[j].y;
+#pragma unroll
+            for (int i = 0; i < MF; ++i) {
+              const double asum = af[i].x + af[i].y;
+#pragma unroll
+              for (int j = 0; j < NF; ++j) {
+                dmma(acc[0][i][j][0], acc[0][i][j][1], af[i].x, bf[j].x);
+                dmma(acc[1][i][j][0], acc[1][i][j][1], af[i].y, bf[j].y);
+                dmma(acc[2][i][j][0], acc[2][i][j][1], asum, bsum[j]);
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) detail::mbar_arrive(&empty[s]);
+    }
+  }
+
+  // Stream-K fix-up. A CTA that computed the head/middle of a tile finished by a later
+  // CTA publishes its register partial to its workspace slot and raises its flag.
+  __device__ __forceinline__ static void publish(double* ws, int* flags, int c, Acc& acc) {
+    const int tid = threadIdx.x;
+    double* flat = &acc[0][0][0][0];
+    double* w = ws + (size_t)c * ACCN * NMATH;
+#pragma unroll
+    for (int r = 0; r < ACCN; ++r) __stcg(w + (size_t)r * NMATH + tid, flat[r]);
+    __threadfence();
+    detail::named_sync(2, NMATH);
+    if (tid == 0) detail::st_release(flags + c, 1);
+  }
+  // The owner adds the partials of CTAs first..c-1 in CTA order (fixed summation
+  // order). With clear, each consumed flag is reset (every CTA publishes at most
+  // once per launch, so the flags are clean for the next launch without a memset).
+  __device__ __forceinline__ static void absorb(const double* ws, int* flags, int first, int c, Acc& acc, bool clear) {
+    const int tid = threadIdx.x;
+    double* flat = &acc[0][0][0][0];
+    for (int cc = first; cc < c; ++cc) {
+      if (tid == 0)
+        while (detail::ld_acquire(flags + cc) == 0) {
+        }
+      detail::named_sync(2, NMATH);
+      const double* w = ws + (size_t)cc * ACCN * NMATH;
+#pragma unroll
+      for (int r = 0; r < ACCN; ++r) flat[r] += __ldcg(w + (size_t)r * NMATH + tid);
+      if (clear && tid == 0) flags[cc] = 0;
+    }
   }
 
   template <bool AMF, bool BNF>
@@ -237,11 +334,6 @@ struct SKCore {
     }
 
     // ================================================================== math warps
-    const int lane = tid & 31, warp = tid >> 5;
-    const int wm = warp / WARPS_N, wn = warp % WARPS_N;
-    const int arow = wm * WTM + (lane >> 2);
-    const int bcol = wn * WTN + (lane >> 2);
-    const int kq = lane & 3;
     int64_t gi = 0;
     Acc acc;
     // segments in REVERSE range order: a CTA first publishes the partial of the tile it
@@ -254,89 +346,14 @@ struct SKCore {
       const int kt0 = (int)(sb - tstart);
       const int kt1 = (int)(e - tstart);
       Base::zero(acc);
-      for (int kt = kt0; kt < kt1; ++kt, ++gi) {
-        const int s = (int)(gi % STAGES);
-        detail::mbar_wait(&full[s], (uint32_t)((gi / STAGES) & 1));
-        const T* as = As + s * BK * LDA;
-        const T* bs = Bs + s * BK * LDB;
-#pragma unroll
-        for (int k4 = 0; k4 < BK / 4; ++k4) {
-          const int kr = k4 * 4 + kq;
-          if constexpr (!CPLX) {
-            double af[MF], bf[NF];
-#pragma unroll
-            for (int i = 0; i < MF; ++i) af[i] = as[kr * LDA + arow + i * 8];
-#pragma unroll
-            for (int j = 0; j < NF; ++j) bf[j] = bs[kr * LDB + bcol + j * 8];
-#pragma unroll
-            for (int i = 0; i < MF; ++i)
-#pragma unroll
-              for (int j = 0; j < NF; ++j) dmma(acc[0][i][j][0], acc[0][i][j][1], af[i], bf[j]);
-          } else {
-            double2 af[MF], bf[NF];
-#pragma unroll
-            for (int i = 0; i < MF; ++i) af[i] = as[kr * LDA + arow + i * 8];
-#pragma unroll
-            for (int j = 0; j < NF; ++j) bf[j] = bs[kr * LDB + bcol + j * 8];
-            if constexpr (MODE == 0) {
-#pragma unroll
-              for (int i = 0; i < MF; ++i) {
-                const double ain = dneg(af[i].y);
-#pragma unroll
-                for (int j = 0; j < NF; ++j) {
-                  dmma(acc[0][i][j][0], acc[0][i][j][1], af[i].x, bf[j].x);
-                  dmma(acc[0][i][j][0], acc[0][i][j][1], ain, bf[j].y);
-                  dmma(acc[1][i][j][0], acc[1][i][j][1], af[i].x, bf[j].y);
-                  dmma(acc[1][i][j][0], acc[1][i][j][1], af[i].y, bf[j].x);
-                }
-              }
-            } else {
-              double bsum[NF];
-#pragma unroll
-              for (int j = 0; j < NF; ++j) bsum[j] = bf[j].x + bf[j].y;
-#pragma unroll
-              for (int i = 0; i < MF; ++i) {
-                const double asum = af[i].x + af[i].y;
-#pragma unroll
-                for (int j = 0; j < NF; ++j) {
-                  dmma(acc[0][i][j][0], acc[0][i][j][1], af[i].x, bf[j].x);
-                  dmma(acc[1][i][j][0], acc[1][i][j][1], af[i].y, bf[j].y);
-                  dmma(acc[2][i][j][0], acc[2][i][j][1], asum, bsum[j]);
-                }
-              }
-            }
-          }
-        }
-        __syncwarp();
-        if (lane == 0) detail::mbar_arrive(&empty[s]);
-      }
+      consume(As, Bs, full, empty, gi, kt1 - kt0, acc);
       // ---- epilogue of this segment
       int m0, n0;
       tile_coords(d, tile, m0, n0);
-      double* flat = &acc[0][0][0][0];
       if (kt1 < KT) {
-        // head/middle of a tile finished by a later CTA: publish the partial
-        double* w = sk.ws + (size_t)c * ACCN * NMATH;
-#pragma unroll
-        for (int r = 0; r < ACCN; ++r) __stcg(w + (size_t)r * NMATH + tid, flat[r]);
-        __threadfence();
-        detail::named_sync(2, NMATH);
-        if (tid == 0) detail::st_release(sk.flags + c, 1);
+        publish(sk.ws, sk.flags, c, acc);
       } else {
-        if (kt0 > 0) {
-          // owner: add the partials of the earlier CTAs of this tile in CTA order
-          // (fixed summation order: own k-range, then partials by increasing CTA)
-          const int first = detail::sk_cta_of(sk.total, sk.G, tile * (int64_t)KT);
-          for (int cc = first; cc < c; ++cc) {
-            if (tid == 0)
-              while (detail::ld_acquire(sk.flags + cc) == 0) {
-              }
-            detail::named_sync(2, NMATH);
-            const double* w = sk.ws + (size_t)cc * ACCN * NMATH;
-#pragma unroll
-            for (int r = 0; r < ACCN; ++r) flat[r] += __ldcg(w + (size_t)r * NMATH + tid);
-          }
-        }
+        if (kt0 > 0) absorb(sk.ws, sk.flags, detail::sk_cta_of(sk.total, sk.G, tile * (int64_t)KT), c, acc, false);
         Base::store(C, d.out_ld, m0, n0, d.M, d.N, acc);
       }
       e = sb;

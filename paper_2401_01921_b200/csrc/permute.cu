@@ -922,6 +922,7 @@ int permute_device(const void* src, void* dst, int es, int rank, const int64_t* 
     TNB_CUDA_CHECK(cudaMemcpyAsync(dst, src, (size_t)p.nelem * es, cudaMemcpyDeviceToDevice, st));
     return TNB_OK;
   }
+  KTimer kt(TNB_KF_PERMUTE, st, 2.0 * (double)p.nelem * es);
   switch (es) {
     case 1: return launch<1>(src, dst, p, st);
     case 2: return launch<2>(src, dst, p, st);

@@ -114,10 +114,12 @@ def test_blocks_without_pairs_are_zero(cuda):
         assert np.max(np.abs(out.get_block_(i).numpy() - want)) <= 1e-12
 
 
-def test_panel_masked_partition_reassembles_bitexact(cuda):
+def test_panel_masked_partition_reassembles(cuda):
     """Multi-GPU partition emulated on one GPU: each 'rank' computes only its LPT panels
     (panel mask through the C ABI); stitching the panels gives the unpartitioned result
-    bit for bit (the full K reduction of every panel is local)."""
+    (the full K reduction of every panel is local). The stream-K split of the k-iterations
+    depends on how much work a launch holds, so the summation order -- and the last bits --
+    can differ from the single-launch result: tolerance 1e-13 relative per panel."""
     import torch
     from paper_2401_01921_b200 import contraction as C
     from paper_2401_01921_b200 import parallel as P
@@ -144,4 +146,21 @@ def test_panel_masked_partition_reassembles_bitexact(cuda):
         ref = full._blocks[0]._slab
         spans = P.panel_spans(panels, [blk._off for blk in full._blocks])
         for s, n in spans:
-            assert torch.equal(stitched[s:s + n], ref[s:s + n])
+            err = torch.linalg.norm(stitched[s:s + n] - ref[s:s + n]).item()
+            assert err <= 1e-13 * max(torch.linalg.norm(ref[s:s + n]).item(), 1e-300), (s, n, err)
+
+
+def test_grouped_stream_k_is_deterministic(cuda):
+    """Same structure, same inputs -> bit-identical output on every call (fixed stream-K
+    split, partials added in CTA order, no data atomics), eager and graph-replayed."""
+    import torch
+    from paper_2401_01921_b200 import graphs
+    A, E, _ = _c4()
+    first = contract(A, E)._blocks[0]._slab.clone()
+    for _ in range(3):
+        assert torch.equal(contract(A, E)._blocks[0]._slab, first)
+    g = graphs.capture(lambda: contract(A, E))
+    for _ in range(3):
+        out = g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out._blocks[0]._slab, first)

@@ -33,6 +33,15 @@ def permute(shape, dt, perms, iters):
     torch.cuda.synchronize()
 
 
+def c4(iters):
+    sys.path.insert(0, ROOT)
+    import bench
+    A, E = bench.c4_tensors(tnb)
+    for _ in range(iters):
+        tnb.contract(A, E)
+    torch.cuda.synchronize()
+
+
 if __name__ == "__main__":
     torch.cuda.set_device(0)
     what = sys.argv[1]
@@ -42,4 +51,6 @@ if __name__ == "__main__":
         perms = [tuple(int(c) for c in p) for p in sys.argv[4].split(",")]
         permute(tuple(int(x) for x in sys.argv[2].split("x")), np.complex128 if sys.argv[3] == "c128" else np.float64,
                 perms, int(sys.argv[5]))
+    elif what == "c4":
+        c4(int(sys.argv[2]))
     print("done")
