@@ -235,9 +235,13 @@ def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, roof=True, s
         probe = net.launch().get_block_().contiguous().storage()
         out_host = torch.empty(probe.shape, dtype=probe.dtype, pin_memory=True)
 
+        # uploads in first-use order on the engine's copy stream: each contraction step
+        # waits only for its own operands, so R's copy runs under the A.L GEMM
+        first_use = tnb.tree_leaves(tnb.parse_order(order))
+
         def step():
-            for nm, p in pinned.items():
-                tensors[nm].get_block_().storage().copy_(p.reshape(-1), non_blocking=True)
+            for nm in first_use:
+                tensors[nm].get_block_().upload_(pinned[nm])
             out = net.launch()
             out_host.copy_(out.get_block_().contiguous().storage(), non_blocking=True)
         for _ in range(max(1, warmup)):

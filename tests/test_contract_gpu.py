@@ -121,3 +121,28 @@ def test_inputs_not_mutated_and_output_fresh(cuda):
     c = contract_pair(a, b)
     assert np.array_equal(a.numpy(), a0) and np.array_equal(b.numpy(), b0)
     assert not c.same_data(a) and not c.same_data(b)
+
+
+def test_async_upload_is_awaited_by_the_consumer(cuda):
+    """upload_ copies on the engine's copy stream; a contraction issued right after it
+    (on the compute stream) must see the NEW data, for dense and block-sparse operands,
+    and a pending upload must not be overtaken by a later upload into the same buffer."""
+    import torch
+    rng = np.random.default_rng(7)
+    a0, b0 = rng.standard_normal((300, 200)), rng.standard_normal((200, 100))
+    a1, b1 = rng.standard_normal((300, 200)), rng.standard_normal((200, 100))
+    A = UniTensor(storage.from_numpy(a0), labels=["i", "k"])
+    B = UniTensor(storage.from_numpy(b0), labels=["k", "j"])
+    contract(A, B)
+    for _ in range(3):
+        A.get_block_().upload_(torch.from_numpy(a1).pin_memory())
+        B.get_block_().upload_(b1)
+        got = contract(A, B).numpy()
+        assert rel_fro(got, a1 @ b1) <= 1e-13
+        A.get_block_().upload_(torch.from_numpy(a0).pin_memory())
+        A.get_block_().upload_(torch.from_numpy(a1).pin_memory())  # WAR/WAW on one buffer
+        assert rel_fro(contract(A, B).numpy(), a1 @ b1) <= 1e-13
+    with pytest.raises(ValueError):
+        A.get_block_().upload_(np.zeros(7))
+    with pytest.raises(TypeError):
+        A.get_block_().upload_(np.zeros((300, 200), dtype=np.complex128))
