@@ -559,7 +559,13 @@ def main():
                                                             for k, v in perm.items()}}}
         c4 = gpu_c4(tnb, max(10, args.steps), args.warmup, flush, dist)
         wl["blocksparse_c4"] = {"value": round(c4["gflops"], 2), "unit": "GFLOP/s (graph replay; eager in gflops_eager)",
-                                **c4}
+                                **c4,
+                                "roofline": {"bound": "tensor", "achieved": round(c4["bs_gemm_kernel_tflops"], 3),
+                                             "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                             "frac": round(c4["bs_gemm_kernel_tflops"] / FP64_PEAK_TFLOPS, 4),
+                                             "traffic": traffic_per_launch("bs_sk_kernel", np.float64),
+                                             "kernel": "bs_sk_kernel (grouped stream-K DMMA.8x8x4)",
+                                             "peak_source": PEAK_SOURCE}}
         bt = gpu_lawr_batch(tnb, 64, 512, np.complex128, max(2, args.steps // 4), 1, flush, dist)
         wl["lawr_batch64_c128_chi512"] = {"value": round(bt["gflops"], 2), "unit": "GFLOP/s (8 flop/complex MAC)",
                                           "scaling": "strong (64 instances sharded over ranks)", **bt}
