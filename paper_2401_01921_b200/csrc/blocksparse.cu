@@ -111,6 +111,12 @@ __device__ __forceinline__ bool b_matches(const BsMeta& m, const int32_t* aqn, c
   return true;
 }
 
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // In place: a[0..n) := inclusive prefix sums (one CTA, blockDim a multiple of 32).
 __device__ void cta_inclusive_scan(int32_t* a, int n) {
   __shared__ int32_t carry;
@@ -144,83 +150,133 @@ __device__ void cta_inclusive_scan(int32_t* a, int n) {
   }
 }
 
+// Shared-memory layout of the pairing kernel (qn tables, CSR, per-tile counts): every
+// table is re-read many times by dependent loops, so all of it lives on chip when it fits.
+__host__ __device__ inline size_t pair_smem_bytes(const BsMeta& m) {
+  return al16(((size_t)m.na * m.ra + (size_t)m.nb * m.rb + (size_t)m.nout * m.ro) * 4) +
+         al16((size_t)(m.nout + 1) * 4) + al16((size_t)m.na * 4) + al16((size_t)m.ntiles * 4) +
+         (size_t)m.ntiles * 8;
+}
+
 __global__ void __launch_bounds__(1024) bs_pair_kernel(const BsMeta m) {
-  extern __shared__ int32_t qsm[];
-  // the qn tables are re-read O(nout * (na + pairs * nb)) times: stage them on chip
+  extern __shared__ __align__(16) unsigned char psm[];
+  long long* stamp = reinterpret_cast<long long*>(m.err + 4);  // dev: phase timestamps
+  int nst = 0;
+#define TNB_STAMP() \
+  if (threadIdx.x == 0 && nst < 16) stamp[nst++] = gtimer();
+  TNB_STAMP()
   const int32_t* aqn = m.a_qn;
   const int32_t* bqn = m.b_qn;
   const int32_t* oqn = m.out_qn;
+  int32_t* optr = m.out_ptr;    // [nout+1]: counts, then the CSR row pointer
+  int32_t* tcnt = m.tile_cnt;   // [ntiles] k-iterations per tile (list order)
+  int32_t* kblk = nullptr;      // [na] K of each A block (smem only)
+  const int na_ = m.na * m.ra, nb_ = m.nb * m.rb, no_ = m.nout * m.ro;
   if (m.qn_smem) {
-    const int na_ = m.na * m.ra, nb_ = m.nb * m.rb, no_ = m.nout * m.ro;
-    for (int x = threadIdx.x; x < na_; x += blockDim.x) qsm[x] = m.a_qn[x];
-    for (int x = threadIdx.x; x < nb_; x += blockDim.x) qsm[na_ + x] = m.b_qn[x];
-    for (int x = threadIdx.x; x < no_; x += blockDim.x) qsm[na_ + nb_ + x] = m.out_qn[x];
-    aqn = qsm;
-    bqn = qsm + na_;
-    oqn = qsm + na_ + nb_;
+    int32_t* q = reinterpret_cast<int32_t*>(psm);
+    for (int x = threadIdx.x; x < na_; x += blockDim.x) q[x] = m.a_qn[x];
+    for (int x = threadIdx.x; x < nb_; x += blockDim.x) q[na_ + x] = m.b_qn[x];
+    for (int x = threadIdx.x; x < no_; x += blockDim.x) q[na_ + nb_ + x] = m.out_qn[x];
+    aqn = q;
+    bqn = q + na_;
+    oqn = q + na_ + nb_;
+    unsigned char* r = psm + al16((size_t)(na_ + nb_ + no_) * 4);
+    optr = reinterpret_cast<int32_t*>(r);
+    r += al16((size_t)(m.nout + 1) * 4);
+    kblk = reinterpret_cast<int32_t*>(r);
+    r += al16((size_t)m.na * 4);
+    tcnt = reinterpret_cast<int32_t*>(r);
+    for (int x = threadIdx.x; x < m.na; x += blockDim.x) kblk[x] = m.da[x].K;
     __syncthreads();
   }
-  int32_t* cnt = m.out_ptr + 1;  // counts first, then scanned in place
-  for (int o = threadIdx.x; o < m.nout; o += blockDim.x) {
+  TNB_STAMP()
+  // warp per output block: the A-block test is warp-uniform, lanes sweep the B blocks
+  // (a thread-per-block loop nest diverges and serialises across the warp)
+  const int lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  for (int o = threadIdx.x >> 5; o < m.nout; o += nwarp) {
     int c = 0;
     for (int i = 0; i < m.na; ++i) {
       if (!a_matches(m, aqn, oqn, i, o)) continue;
-      for (int j = 0; j < m.nb; ++j) c += b_matches(m, aqn, bqn, oqn, i, j, o) ? 1 : 0;
+      for (int j0 = 0; j0 < m.nb; j0 += 32) {
+        const bool hit = j0 + lane < m.nb && b_matches(m, aqn, bqn, oqn, i, j0 + lane, o);
+        c += __popc(__ballot_sync(0xffffffffu, hit));
+      }
     }
-    cnt[o] = c;
+    if (lane == 0) optr[o + 1] = c;
   }
-  if (threadIdx.x == 0) m.out_ptr[0] = 0;
+  if (threadIdx.x == 0) optr[0] = 0;
   __syncthreads();
-  cta_inclusive_scan(cnt, m.nout);
+  TNB_STAMP()
+  cta_inclusive_scan(optr + 1, m.nout);
+  TNB_STAMP()
   // write pairs of each output block in reference order (i asc, j asc)
-  if (m.out_ptr[m.nout] > m.max_pairs) {
+  if (optr[m.nout] > m.max_pairs) {
     if (threadIdx.x == 0) m.err[0] = 1;
     return;
   }
-  for (int o = threadIdx.x; o < m.nout; o += blockDim.x) {
-    int p = m.out_ptr[o];
+  for (int o = threadIdx.x >> 5; o < m.nout; o += nwarp) {
+    int p = optr[o];
+    int kt = 0;
     for (int i = 0; i < m.na; ++i) {
       if (!a_matches(m, aqn, oqn, i, o)) continue;
-      for (int j = 0; j < m.nb; ++j)
-        if (b_matches(m, aqn, bqn, oqn, i, j, o)) {
-          m.pairs[2 * p] = i;
-          m.pairs[2 * p + 1] = j;
-          ++p;
+      const int kti = ((kblk ? kblk[i] : m.da[i].K) + m.bk - 1) / m.bk;
+      for (int j0 = 0; j0 < m.nb; j0 += 32) {
+        const bool hit = j0 + lane < m.nb && b_matches(m, aqn, bqn, oqn, i, j0 + lane, o);
+        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const int q = p + __popc(bal & ((1u << lane) - 1u));  // j ascending within i
+          m.pairs[2 * q] = i;
+          m.pairs[2 * q + 1] = j0 + lane;
         }
+        p += __popc(bal);
+        kt += __popc(bal) * kti;
+      }
+    }
+    if (lane == 0) {
+      m.out_ptr[o + 1] = optr[o + 1];  // the CSR row pointer the GEMM reads
+      if (o == 0) m.out_ptr[0] = 0;
+      // every tile of block o has the same k-iterations; tile_kbeg (ntiles+1 >= nout
+      // entries) serves as scratch for them until the final prefix sums overwrite it
+      m.tile_kbeg[o] = kt;
     }
   }
   __syncthreads();
+  TNB_STAMP()
   // k-iterations per output tile (0 for tiles of other ranks' panels)
   for (int t = threadIdx.x; t < m.ntiles; t += blockDim.x) {
     const TileRef tr = m.tiles[t];
-    int c = 0;
-    if (!m.mask || m.mask[tr.panel])
-      for (int p = m.out_ptr[tr.o]; p < m.out_ptr[tr.o + 1]; ++p) c += (m.da[m.pairs[2 * p]].K + m.bk - 1) / m.bk;
-    m.tile_cnt[t] = c;
+    tcnt[t] = (!m.mask || m.mask[tr.panel]) ? m.tile_kbeg[tr.o] : 0;
   }
   __syncthreads();
   // schedule order: tiles ranked by k-iterations (descending, stable), laid out
   // big, small, big, small, ... so that every stream-K range holds at most a few
   // short segments (each segment / pair switch has a fixed gather set-up latency)
-  const bool reorder = m.ntiles <= 4096;
+  TNB_STAMP()
+  const bool reorder = m.qn_smem && m.ntiles <= 4096;
   for (int t = threadIdx.x; t < m.ntiles; t += blockDim.x) {
     int pos = t;
+    const int ct = tcnt[t];
     if (reorder) {
-      const int ct = m.tile_cnt[t];
       int r = 0;
       for (int u = 0; u < m.ntiles; ++u) {
-        const int cu = m.tile_cnt[u];
+        const int cu = tcnt[u];
         r += (cu > ct || (cu == ct && u < t)) ? 1 : 0;
       }
       const int half = (m.ntiles + 1) / 2;
       pos = r < half ? 2 * r : 2 * (m.ntiles - 1 - r) + 1;
     }
     m.stiles[pos] = m.tiles[t];
-    m.tile_kbeg[pos + 1] = m.tile_cnt[t];
+    m.tile_cnt[pos] = ct;  // (global copy, schedule order)
   }
-  if (threadIdx.x == 0) m.tile_kbeg[0] = 0;
   __syncthreads();
-  cta_inclusive_scan(m.tile_kbeg + 1, m.ntiles);
+  for (int t = threadIdx.x; t < m.ntiles; t += blockDim.x) tcnt[t] = m.tile_cnt[t];
+  __syncthreads();
+  TNB_STAMP()
+  cta_inclusive_scan(tcnt, m.ntiles);
+  TNB_STAMP()
+  for (int t = threadIdx.x; t <= m.ntiles; t += blockDim.x) m.tile_kbeg[t] = t ? tcnt[t - 1] : 0;
+  TNB_STAMP()
+#undef TNB_STAMP
 }
 
 // ---- grouped stream-K GEMM --------------------------------------------------
@@ -246,11 +302,7 @@ struct BsSK {
   long long* trace;
 };
 constexpr int kTraceW = 64;
-__device__ __forceinline__ long long gtimer() {
-  long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
+
 
 template <bool CPLX, int MODE, bool AMF, bool BNF>
 __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
@@ -895,7 +947,7 @@ extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int r
                  o_tiles = take(sizeof(TileRef) * tiles.size()),
                  o_mask = take(panel_mask ? (size_t)npanels : 0);
     const size_t upload = off;
-    const size_t o_optr = take((size_t)(nout + 1) * 4), o_err = take(16), o_pairs = take((size_t)meta.max_pairs * 8),
+    const size_t o_optr = take((size_t)(nout + 1) * 4), o_err = take(16 + 16 * 8), o_pairs = take((size_t)meta.max_pairs * 8),
                  o_kbeg = take((size_t)(tiles.size() + 1) * 4), o_tcnt = take((size_t)tiles.size() * 4),
                  o_stiles = take(sizeof(TileRef) * tiles.size());
     const size_t total = off;
@@ -912,7 +964,7 @@ extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int r
     TNB_CUDA_CHECK(cudaMalloc((void**)&plan.dblob, total));
     unsigned char* dblob = plan.dblob;
     TNB_CUDA_CHECK(cudaMemcpyAsync(dblob, h.data(), upload, cudaMemcpyHostToDevice, st));  // staged, then returns
-    TNB_CUDA_CHECK(cudaMemsetAsync(dblob + o_err, 0, 16, st));
+    TNB_CUDA_CHECK(cudaMemsetAsync(dblob + o_err, 0, 16 + 16 * 8, st));
     meta.a_qn = reinterpret_cast<const int32_t*>(dblob + o_aqn);
     meta.b_qn = reinterpret_cast<const int32_t*>(dblob + o_bqn);
     meta.out_qn = reinterpret_cast<const int32_t*>(dblob + o_oqn);
@@ -929,9 +981,12 @@ extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int r
     meta.tile_cnt = reinterpret_cast<int32_t*>(dblob + o_tcnt);
     meta.stiles = reinterpret_cast<TileRef*>(dblob + o_stiles);
     meta.ptrs = nullptr;
-    const size_t qn_bytes = ((size_t)na * rank_a + (size_t)nb * rank_b + (size_t)nout * ro) * 4;
-    meta.qn_smem = qn_bytes <= 160 * 1024;
-    const size_t pair_smem = meta.qn_smem ? qn_bytes : 0;
+    meta.qn_smem = 1;
+    size_t pair_smem = pair_smem_bytes(meta);
+    if (pair_smem > 200 * 1024) {  // very large structures: tables stay in global memory
+      meta.qn_smem = 0;
+      pair_smem = 0;
+    }
     if (pair_smem > 48 * 1024)
       TNB_CUDA_CHECK(cudaFuncSetAttribute(bs_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pair_smem));
     {
@@ -943,6 +998,14 @@ extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int r
     if (e != cudaSuccess) {
       cudaFree(dblob);
       return cuda_fail(e, "bs_contract: pairing kernel launch");
+    }
+    if (getenv("TNB_BS_TRACE")) {
+      long long st16[16];
+      TNB_CUDA_CHECK(cudaMemcpyAsync(st16, dblob + o_err + 16, sizeof(st16), cudaMemcpyDeviceToHost, st));
+      TNB_CUDA_CHECK(cudaStreamSynchronize(st));
+      fprintf(stderr, "[tnb pair phases us]");
+      for (int q = 1; q < 16 && st16[q] > 0; ++q) fprintf(stderr, " %.1f", (st16[q] - st16[0]) / 1e3);
+      fprintf(stderr, "\n");
     }
     plan.npairs = exact_pairs;
     plan.o_optr = o_optr;
