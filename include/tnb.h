@@ -128,12 +128,14 @@ int tnb_zero_flux_blocks(int nbonds, int nsyms, const int32_t* nsec,
                          int32_t* out_qn, int64_t* count);
 
 /* ---- a12: U(1)/Z_n block-sparse pairwise contraction (contract.py:137-167)
- * Block metadata is uploaded once per call in one device buffer; pairing is
- * computed ON DEVICE:
+ * Block metadata is uploaded once per block STRUCTURE (device-resident plan
+ * cache); pairing is computed ON DEVICE:
  *   for i in a-block order, for j ascending with key(b_j) == key(a_i):
  *       out[out_idx(i,j)] += A_i . B_j
- * and each output tile is owned by one CTA that accumulates its pairs in that
- * order (deterministic, no atomics).
+ * The k-iterations of all output tiles (each tile's pairs concatenated in that
+ * order) are split evenly over one persistent CTA per SM (grouped stream-K);
+ * a tile split across CTAs is finished by the CTA holding its last k-iteration,
+ * which adds the earlier partials in CTA order: deterministic, no atomics.
  *
  * Plan (host -> device):
  *   na, nb, nout      : block counts
@@ -178,6 +180,26 @@ int tnb_bs_contract_masked(int dtype, int na, int nb, int nout,
                            void* const* out_ptrs, int64_t npanels, const uint8_t* panel_mask,
                            int64_t max_pairs, int32_t* pairs_out, int64_t* npairs,
                            void* stream);
+
+/* Split form of the same operation for repeated calls on one block STRUCTURE
+ * (a Lanczos loop, a sweep over equal-structure sites): tnb_bs_plan builds --
+ * or finds in the device-resident plan cache -- the plan of a structure (same
+ * arguments as tnb_bs_contract_masked minus the data; panel_mask may be NULL)
+ * and returns an opaque id; tnb_bs_execute launches the grouped GEMM for one
+ * set of block pointers; tnb_bs_plan_pairs reads back the (i, j, out_idx)
+ * triples. Ids become stale (TNB_EINVAL) when the cache is flushed (>256
+ * structures or a device change): re-plan then. */
+int tnb_bs_plan(int dtype, int na, int nb, int nout, int rank_a, int rank_b,
+                const int32_t* a_qn, const int64_t* a_shape, const int32_t* a_perm,
+                const int32_t* b_qn, const int64_t* b_shape, const int32_t* b_perm,
+                int nc, const int32_t* a_axes, const int32_t* b_axes,
+                const int32_t* out_qn, const int64_t* out_shape,
+                int64_t npanels, const uint8_t* panel_mask,
+                int64_t* plan_id, int64_t* npairs, void* stream);
+int tnb_bs_execute(int64_t plan_id, const void* const* a_ptrs, const void* const* b_ptrs,
+                   void* const* out_ptrs, void* stream);
+int tnb_bs_plan_pairs(int64_t plan_id, int64_t max_pairs, int32_t* pairs_out, int64_t* npairs,
+                      void* stream);
 
 /* ---- a14: optimal contraction order DP (contract.py:271-343), host only ---
  * n tensors (n <= 16). Labels are interned to ints: nlab[t] labels for tensor

@@ -22,6 +22,7 @@ EXPORTS = (
     "tnb_synchronize", "tnb_permute", "tnb_contract_dense",
     "tnb_zero_flux_blocks", "tnb_bs_contract", "tnb_bs_contract_masked", "tnb_optimal_order",
     "tnb_ktimer_enable", "tnb_ktimer_reset", "tnb_ktimer_read",
+    "tnb_bs_plan", "tnb_bs_execute", "tnb_bs_plan_pairs",
 )
 
 # kernel families of the kernel timer (TNB_KF_* in include/tnb.h)
@@ -74,6 +75,11 @@ def _declare(lib):
                                     _pi32, _pi64, _pi32, _pi32, _pi64, _pi32,
                                     ctypes.c_int, _pi32, _pi32, _pi32, _pi64,
                                     _p, _p, _p, _i64, _p, _i64, _pi32, _pi64, _p], ctypes.c_int),
+        "tnb_bs_plan": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                         _pi32, _pi64, _pi32, _pi32, _pi64, _pi32,
+                         ctypes.c_int, _pi32, _pi32, _pi32, _pi64, _i64, _p, _pi64, _pi64, _p], ctypes.c_int),
+        "tnb_bs_execute": ([_i64, _p, _p, _p, _p], ctypes.c_int),
+        "tnb_bs_plan_pairs": ([_i64, _i64, _pi32, _pi64, _p], ctypes.c_int),
         "tnb_optimal_order": ([ctypes.c_int, ctypes.c_char_p, _pi32, _pi32, _pi64,
                                ctypes.c_char_p, _i64, ctypes.c_char_p], ctypes.c_int),
     }
@@ -238,6 +244,63 @@ def bs_contract(dtype, a_qn, a_shapes, a_perm, b_qn, b_shapes, b_perm, a_axes, b
     if want_pairs:
         return pairs[:npairs.value].copy()
     return None
+
+
+class BsPlan:
+    """Handle of a device-resident block-sparse plan (tnb_bs_plan): structure-only
+    metadata was uploaded and paired once; ``execute`` launches one grouped GEMM."""
+
+    __slots__ = ("id", "npairs", "na", "nb", "nout", "_aptr", "_bptr", "_optr")
+
+    def __init__(self, plan_id, npairs, na, nb, nout):
+        self.id, self.npairs, self.na, self.nb, self.nout = plan_id, npairs, na, nb, nout
+        self._aptr = (ctypes.c_void_p * max(na, 1))()
+        self._bptr = (ctypes.c_void_p * max(nb, 1))()
+        self._optr = (ctypes.c_void_p * max(nout, 1))()
+
+    def execute(self, a_ptrs, b_ptrs, out_ptrs, stream):
+        """Returns False if the plan went stale (cache flushed): the caller re-plans."""
+        self._aptr[:len(a_ptrs)] = a_ptrs
+        self._bptr[:len(b_ptrs)] = b_ptrs
+        self._optr[:len(out_ptrs)] = out_ptrs
+        rc = lib().tnb_bs_execute(self.id, self._aptr, self._bptr, self._optr, stream)
+        if rc == TNB_EINVAL and "stale" in last_error():
+            return False
+        check(rc, "bs_execute")
+        return True
+
+    def pairs(self, stream):
+        cap = max(self.npairs, 1)
+        out = np.zeros((cap, 3), dtype=np.int32)
+        n = ctypes.c_int64(0)
+        check(lib().tnb_bs_plan_pairs(self.id, cap, out.ctypes.data_as(_pi32), ctypes.byref(n), stream),
+              "bs_plan_pairs")
+        return out[:n.value].copy()
+
+
+def bs_plan(dtype, a_qn, a_shapes, a_perm, b_qn, b_shapes, b_perm, a_axes, b_axes, out_qn, out_shapes,
+            stream, panel_mask=None):
+    na, nb, nout = len(a_qn), len(b_qn), len(out_qn)
+    ra, rb = len(a_perm), len(b_perm)
+    aq, paq = _arr32(np.asarray(a_qn, dtype=np.int32).reshape(-1))
+    ash, pash = _arr64(np.asarray(a_shapes, dtype=np.int64).reshape(-1))
+    ap, pap = _arr32(a_perm)
+    bq, pbq = _arr32(np.asarray(b_qn, dtype=np.int32).reshape(-1))
+    bsh, pbsh = _arr64(np.asarray(b_shapes, dtype=np.int64).reshape(-1))
+    bp, pbp = _arr32(b_perm)
+    xa, pxa = _arr32(a_axes)
+    xb, pxb = _arr32(b_axes)
+    oq, poq = _arr32(np.asarray(out_qn, dtype=np.int32).reshape(-1))
+    osh, posh = _arr64(np.asarray(out_shapes, dtype=np.int64).reshape(-1))
+    mask = None
+    if panel_mask is not None:
+        mask = np.ascontiguousarray(np.asarray(panel_mask, dtype=np.uint8))
+    pid, npairs = ctypes.c_int64(0), ctypes.c_int64(0)
+    check(lib().tnb_bs_plan(dtype, na, nb, nout, ra, rb, paq, pash, pap, pbq, pbsh, pbp,
+                            len(a_axes), pxa, pxb, poq, posh,
+                            0 if mask is None else len(mask), None if mask is None else mask.ctypes.data_as(_p),
+                            ctypes.byref(pid), ctypes.byref(npairs), stream), "bs_plan")
+    return BsPlan(pid.value, npairs.value, na, nb, nout)
 
 
 def optimal_order(names, label_lists, dims):

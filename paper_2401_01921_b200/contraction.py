@@ -11,7 +11,8 @@ Public functions and their reference counterparts (pkg/src/tnkit/contract.py):
 Validation (labels, directions, sectors, duplicate free labels) happens here,
 before any device work, with the reference's exception types. The arithmetic
 is libtnb: ``tnb_contract_dense`` (DMMA GEMM reading lazily permuted operands in
-place) and ``tnb_bs_contract`` (device pairing + grouped GEMM). There is no CPU
+place) and ``tnb_bs_plan``/``tnb_bs_execute`` (device pairing once per block
+structure + grouped stream-K GEMM per call). There is no CPU
 fallback: int64/bool contractions raise TypeError.
 """
 import itertools
@@ -183,33 +184,55 @@ def _contract_blocks(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds, 
     qns = zero_flux_combos(out_bonds)
     if not qns:
         raise ValueError("no valid blocks: no combination of these bonds' sectors has zero flux")
-    shapes = [tuple(x.sectors[k][1] for x, k in zip(out_bonds, qn)) for qn in qns]
+    plan, shapes = _bs_plan(dt, a, ablk, aperm, b, bblk, bperm, a_pos, b_pos, out_bonds, qns, panel_mask)
     # every output block is fully written by the kernel (with a panel mask: the panels
     # of this rank; parallel.gather_panels fills the rest)
     oblk, _ = _slab_blocks(shapes, dt, zero=False)
-    _lib.bs_contract(dense.dtype_code(dt), a._qns, [x.storage_shape for x in ablk], aperm,
-                     b._qns, [x.storage_shape for x in bblk], bperm, a_pos, b_pos,
-                     qns, shapes, [x.data_ptr for x in ablk], [x.data_ptr for x in bblk],
-                     [x.data_ptr for x in oblk], dense.stream_handle(), panel_mask=panel_mask)
+    aptrs, bptrs, optrs = [x.data_ptr for x in ablk], [x.data_ptr for x in bblk], [x.data_ptr for x in oblk]
+    if not plan.execute(aptrs, bptrs, optrs, dense.stream_handle()):
+        _BS_PLANS.clear()  # the library flushed its plan cache: re-plan this structure
+        plan, _ = _bs_plan(dt, a, ablk, aperm, b, bblk, bperm, a_pos, b_pos, out_bonds, qns, panel_mask)
+        if not plan.execute(aptrs, bptrs, optrs, dense.stream_handle()):
+            raise _lib.EngineError("block-sparse plan went stale twice")
     return UniTensor._assemble(out_bonds, out_labels, len(a_free), "", oblk, qns)
+
+
+# Device-resident block-sparse plans (tnb_bs_plan), keyed by the block STRUCTURE of a
+# contraction: a repeated call (Lanczos matvec, equal-structure sites) only marshals the
+# block pointers and launches the grouped GEMM.
+_BS_PLANS = {}
+
+
+def _bs_plan(dt, a, ablk, aperm, b, bblk, bperm, a_pos, b_pos, out_bonds, qns, panel_mask=None):
+    a_sh = tuple(x.storage_shape for x in ablk)
+    b_sh = tuple(x.storage_shape for x in bblk)
+    key = (dt.char, tuple(a._qns), a_sh, tuple(aperm), tuple(b._qns), b_sh, tuple(bperm), tuple(a_pos),
+           tuple(b_pos), tuple(out_bonds), None if panel_mask is None else bytes(np.asarray(panel_mask, np.uint8)))
+    hit = _BS_PLANS.get(key)
+    if hit is not None:
+        return hit
+    shapes = [tuple(x.sectors[k][1] for x, k in zip(out_bonds, qn)) for qn in qns]
+    plan = _lib.bs_plan(dense.dtype_code(dt), a._qns, list(a_sh), aperm, b._qns, list(b_sh), bperm, a_pos, b_pos,
+                        qns, shapes, dense.stream_handle(), panel_mask=panel_mask)
+    if len(_BS_PLANS) >= 512:
+        _BS_PLANS.clear()
+    _BS_PLANS[key] = (plan, shapes)
+    return plan, shapes
 
 
 def block_pairs(a, b):
     """Device pairing table of a block-sparse contraction as (i, j, out_idx) rows in
-    reference accumulation order (contract.py:148-164); runs the contraction."""
+    reference accumulation order (contract.py:148-164): builds (or reuses) the
+    structure's device plan -- the pairing kernel -- and reads the table back."""
     a_pos, b_pos, a_free, b_free, out_labels, out_bonds = _pair_layout(a, b)
     dt = _result_dtype(a.dtype, b.dtype)
     ablk, aperm = _common_perm(a)
     bblk, bperm = _common_perm(b)
     ablk, bblk = _widen(ablk, dt), _widen(bblk, dt)
-    from .labeled import _slab_blocks, zero_flux_combos
+    from .labeled import zero_flux_combos
     qns = zero_flux_combos(out_bonds)
-    shapes = [tuple(x.sectors[k][1] for x, k in zip(out_bonds, qn)) for qn in qns]
-    oblk, _ = _slab_blocks(shapes, dt, zero=False)
-    return _lib.bs_contract(dense.dtype_code(dt), a._qns, [x.storage_shape for x in ablk], aperm,
-                            b._qns, [x.storage_shape for x in bblk], bperm, a_pos, b_pos,
-                            qns, shapes, [x.data_ptr for x in ablk], [x.data_ptr for x in bblk],
-                            [x.data_ptr for x in oblk], dense.stream_handle(), want_pairs=True)
+    plan, _ = _bs_plan(dt, a, ablk, aperm, b, bblk, bperm, a_pos, b_pos, out_bonds, qns)
+    return plan.pairs(dense.stream_handle())
 
 
 def _contract_blocks_scalar(a, b, ablk, bblk, a_pos, b_pos, dt):

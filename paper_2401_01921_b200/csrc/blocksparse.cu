@@ -658,7 +658,9 @@ struct Plan {
 
 struct PlanCache {
   std::mutex mu;
-  std::unordered_map<std::string, Plan> plans;
+  std::unordered_map<std::string, int64_t> index;  // structure key -> slot in plans
+  std::vector<Plan> plans;
+  uint32_t gen = 1;  // bumped when the cache is flushed: stale plan ids are rejected
   int device = -1;
   void* stage = nullptr;  // pinned staging for large pointer tables
   size_t stage_cap = 0;
@@ -760,18 +762,17 @@ void append(std::string& key, const X* p, size_t n) {
 }  // namespace
 }  // namespace tnb
 
-extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int rank_a, int rank_b,
-                                      const int32_t* a_qn, const int64_t* a_shape, const int32_t* a_perm,
-                                      const int32_t* b_qn, const int64_t* b_shape, const int32_t* b_perm, int nc,
-                                      const int32_t* a_axes, const int32_t* b_axes, const int32_t* out_qn,
-                                      const int64_t* out_shape, const void* const* a_ptrs,
-                                      const void* const* b_ptrs, void* const* out_ptrs, int64_t npanels,
-                                      const uint8_t* panel_mask, int64_t max_pairs, int32_t* pairs_out,
-                                      int64_t* npairs, void* stream) {
-  using namespace tnb;
+namespace tnb {
+namespace {
+
+// Caller holds g_cache.mu. Builds (pairing kernel on `st`) or finds the plan of a structure.
+int bs_plan_locked(int dtype, int na, int nb, int nout, int rank_a, int rank_b, const int32_t* a_qn,
+                   const int64_t* a_shape, const int32_t* a_perm, const int32_t* b_qn, const int64_t* b_shape,
+                   const int32_t* b_perm, int nc, const int32_t* a_axes, const int32_t* b_axes,
+                   const int32_t* out_qn, const int64_t* out_shape, int64_t npanels, const uint8_t* panel_mask,
+                   cudaStream_t st, int64_t* plan_id, int64_t* npairs) {
   int rc = require_device();
   if (rc) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
   if (dtype != TNB_F64 && dtype != TNB_C128)
     return fail(TNB_EUNSUP, "bs_contract: only float64 and complex128 are supported on the GPU path");
   if (na < 0 || nb < 0 || nout < 1 || rank_a < 1 || rank_b < 1 || rank_a > TNB_MAX_RANK || rank_b > TNB_MAX_RANK ||
@@ -799,19 +800,22 @@ extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int r
       append(key, panel_mask, (size_t)npanels);
     }
   }
-  std::lock_guard<std::mutex> lock(g_cache.mu);
   int dev = 0;
   TNB_CUDA_CHECK(cudaGetDevice(&dev));
   if (g_cache.device != dev) {
     g_cache.plans.clear();  // plans are per device (one process normally drives one GPU)
+    g_cache.index.clear();
+    ++g_cache.gen;
     g_cache.device = dev;
   }
-  auto hit = g_cache.plans.find(key);
-  if (hit == g_cache.plans.end()) {
+  auto hit = g_cache.index.find(key);
+  if (hit == g_cache.index.end()) {
     if (g_cache.plans.size() >= 256) {
-      TNB_CUDA_CHECK(cudaStreamSynchronize(st));
-      for (auto& kv : g_cache.plans) cudaFree(kv.second.dblob);
+      TNB_CUDA_CHECK(cudaDeviceSynchronize());
+      for (auto& pl : g_cache.plans) cudaFree(pl.dblob);
       g_cache.plans.clear();
+      g_cache.index.clear();
+      ++g_cache.gen;
     }
     Plan plan;
     plan.dtype = dtype;
@@ -1010,10 +1014,27 @@ extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int r
     plan.npairs = exact_pairs;
     plan.o_optr = o_optr;
     plan.o_pairs = o_pairs;
-    hit = g_cache.plans.emplace(key, plan).first;
+    g_cache.plans.push_back(plan);
+    hit = g_cache.index.emplace(key, (int64_t)g_cache.plans.size() - 1).first;
   }
-  Plan& plan = hit->second;
+  *plan_id = ((int64_t)g_cache.gen << 32) | hit->second;
+  if (npairs) *npairs = g_cache.plans[hit->second].npairs;
+  return TNB_OK;
+}
+
+Plan* plan_of(int64_t id) {
+  const uint32_t gen = (uint32_t)((uint64_t)id >> 32);
+  const int64_t slot = id & 0xffffffffll;
+  if (gen != g_cache.gen || slot < 0 || slot >= (int64_t)g_cache.plans.size()) return nullptr;
+  return &g_cache.plans[slot];
+}
+
+// Caller holds g_cache.mu. One grouped GEMM launch with this call's data pointers.
+int bs_execute_locked(Plan& plan, const void* const* a_ptrs, const void* const* b_ptrs, void* const* out_ptrs,
+                      cudaStream_t st) {
   BsMeta meta = plan.meta;
+  const int na = meta.na, nb = meta.nb, nout = meta.nout;
+  int rc = TNB_OK;
   // ---- per-call data pointers
   const int nptr = na + nb + nout;
   PtrTable pt;
@@ -1041,19 +1062,25 @@ extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int r
     TNB_CUDA_CHECK(cudaEventRecord(g_cache.stage_ev, st));
     meta.ptrs = static_cast<const void* const*>(dptr);
   }
-  if (dtype == TNB_F64) rc = launch_bs<false, 0>(plan, meta, &pt, st);
+  if (plan.dtype == TNB_F64) rc = launch_bs<false, 0>(plan, meta, &pt, st);
   else rc = launch_bs<true, 0>(plan, meta, &pt, st);
   if (meta.ptrs) cudaFreeAsync(const_cast<void*>(static_cast<const void*>(meta.ptrs)), st);
   if (rc != TNB_OK) return rc;
+  return TNB_OK;
+}
+
+// Caller holds g_cache.mu. (i, j, out_idx) triples in reference order (synchronises).
+int bs_pairs_locked(Plan& plan, int64_t max_pairs, int32_t* pairs_out, int64_t* npairs, cudaStream_t st) {
+  const int nout = plan.meta.nout;
   if (npairs) *npairs = plan.npairs;
-  if (pairs_out) {
+  {
     if (max_pairs < plan.npairs) return fail(TNB_EINVAL, "bs_contract: pairs_out too small");
     // bookkeeping readback: CSR grouped by output block -> reference order (i asc, j asc)
     std::vector<int32_t> optr(nout + 1);
     int32_t err = 0;
     TNB_CUDA_CHECK(cudaMemcpyAsync(optr.data(), plan.dblob + plan.o_optr, (size_t)(nout + 1) * 4,
                                    cudaMemcpyDeviceToHost, st));
-    TNB_CUDA_CHECK(cudaMemcpyAsync(&err, meta.err, 4, cudaMemcpyDeviceToHost, st));
+    TNB_CUDA_CHECK(cudaMemcpyAsync(&err, plan.meta.err, 4, cudaMemcpyDeviceToHost, st));
     TNB_CUDA_CHECK(cudaStreamSynchronize(st));
     if (err) return fail(TNB_EINVAL, "bs_contract: device pairing overflow");
     int64_t np = optr[nout];
@@ -1072,6 +1099,72 @@ extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int r
     if (npairs) *npairs = np;
   }
   return TNB_OK;
+}
+
+
+}  // namespace
+}  // namespace tnb
+
+extern "C" int tnb_bs_plan(int dtype, int na, int nb, int nout, int rank_a, int rank_b, const int32_t* a_qn,
+                           const int64_t* a_shape, const int32_t* a_perm, const int32_t* b_qn,
+                           const int64_t* b_shape, const int32_t* b_perm, int nc, const int32_t* a_axes,
+                           const int32_t* b_axes, const int32_t* out_qn, const int64_t* out_shape, int64_t npanels,
+                           const uint8_t* panel_mask, int64_t* plan_id, int64_t* npairs, void* stream) {
+  using namespace tnb;
+  int rc = require_device();
+  if (rc) return rc;
+  if (!plan_id) return fail(TNB_EINVAL, "bs_plan: plan_id is NULL");
+  std::lock_guard<std::mutex> lock(g_cache.mu);
+  return bs_plan_locked(dtype, na, nb, nout, rank_a, rank_b, a_qn, a_shape, a_perm, b_qn, b_shape, b_perm, nc, a_axes,
+                        b_axes, out_qn, out_shape, npanels, panel_mask, (cudaStream_t)stream, plan_id, npairs);
+}
+
+extern "C" int tnb_bs_execute(int64_t plan_id, const void* const* a_ptrs, const void* const* b_ptrs,
+                              void* const* out_ptrs, void* stream) {
+  using namespace tnb;
+  int rc = require_device();
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(g_cache.mu);
+  Plan* plan = plan_of(plan_id);
+  if (!plan) return fail(TNB_EINVAL, "bs_execute: stale or unknown plan id (plan cache was flushed)");
+  if ((plan->meta.na && !a_ptrs) || (plan->meta.nb && !b_ptrs) || !out_ptrs)
+    return fail(TNB_EINVAL, "bs_execute: NULL pointer table");
+  return bs_execute_locked(*plan, a_ptrs, b_ptrs, out_ptrs, (cudaStream_t)stream);
+}
+
+extern "C" int tnb_bs_plan_pairs(int64_t plan_id, int64_t max_pairs, int32_t* pairs_out, int64_t* npairs,
+                                 void* stream) {
+  using namespace tnb;
+  int rc = require_device();
+  if (rc) return rc;
+  if (!pairs_out) return fail(TNB_EINVAL, "bs_plan_pairs: pairs_out is NULL");
+  std::lock_guard<std::mutex> lock(g_cache.mu);
+  Plan* plan = plan_of(plan_id);
+  if (!plan) return fail(TNB_EINVAL, "bs_plan_pairs: stale or unknown plan id");
+  return bs_pairs_locked(*plan, max_pairs, pairs_out, npairs, (cudaStream_t)stream);
+}
+
+extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int rank_a, int rank_b,
+                                      const int32_t* a_qn, const int64_t* a_shape, const int32_t* a_perm,
+                                      const int32_t* b_qn, const int64_t* b_shape, const int32_t* b_perm, int nc,
+                                      const int32_t* a_axes, const int32_t* b_axes, const int32_t* out_qn,
+                                      const int64_t* out_shape, const void* const* a_ptrs,
+                                      const void* const* b_ptrs, void* const* out_ptrs, int64_t npanels,
+                                      const uint8_t* panel_mask, int64_t max_pairs, int32_t* pairs_out,
+                                      int64_t* npairs, void* stream) {
+  using namespace tnb;
+  int rc = require_device();
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> lock(g_cache.mu);
+  int64_t id = 0;
+  rc = bs_plan_locked(dtype, na, nb, nout, rank_a, rank_b, a_qn, a_shape, a_perm, b_qn, b_shape, b_perm, nc, a_axes,
+                      b_axes, out_qn, out_shape, npanels, panel_mask, st, &id, npairs);
+  if (rc) return rc;
+  Plan* plan = plan_of(id);
+  rc = bs_execute_locked(*plan, a_ptrs, b_ptrs, out_ptrs, st);
+  if (rc || !pairs_out) return rc;
+  return bs_pairs_locked(*plan, max_pairs, pairs_out, npairs, st);
 }
 
 extern "C" int tnb_bs_contract(int dtype, int na, int nb, int nout, int rank_a, int rank_b, const int32_t* a_qn,

@@ -164,3 +164,25 @@ def test_grouped_stream_k_is_deterministic(cuda):
         out = g.replay()
         torch.cuda.synchronize()
         assert torch.equal(out._blocks[0]._slab, first)
+
+
+def test_one_shot_abi_matches_plan_execute(cuda):
+    """tnb_bs_contract_masked (one call: plan + execute + pairs) and the split
+    tnb_bs_plan / tnb_bs_execute / tnb_bs_plan_pairs give identical bits and triples."""
+    import torch
+    from paper_2401_01921_b200 import _lib, dense
+    from paper_2401_01921_b200 import contraction as C
+    from paper_2401_01921_b200.labeled import _slab_blocks, zero_flux_combos
+    A, E, _ = _c4()
+    a_pos, b_pos, a_free, b_free, out_labels, out_bonds = C._pair_layout(A, E)
+    qns = zero_flux_combos(out_bonds)
+    shapes = [tuple(x.sectors[k][1] for x, k in zip(out_bonds, qn)) for qn in qns]
+    oblk, slab = _slab_blocks(shapes, np.dtype(np.float64), zero=False)
+    trip = _lib.bs_contract(_lib.TNB_F64, A._qns, [x.storage_shape for x in A._blocks], tuple(range(3)),
+                            E._qns, [x.storage_shape for x in E._blocks], tuple(range(3)), a_pos, b_pos,
+                            qns, shapes, [x.data_ptr for x in A._blocks], [x.data_ptr for x in E._blocks],
+                            [x.data_ptr for x in oblk], dense.stream_handle(), want_pairs=True)
+    ref = contract(A, E)
+    torch.cuda.synchronize()
+    assert torch.equal(slab[:ref._blocks[0]._slab.numel()], ref._blocks[0]._slab)
+    assert trip.tolist() == block_pairs(A, E).tolist()
