@@ -214,7 +214,7 @@ def lawr_macs(chi, d=2, D=5):
     return tnb.contraction_cost(tree, sets, dims), tnb.render_order(tree)
 
 
-def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, roof=True, seed=1234):
+def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, roof=True, seed=1234, graph=False):
     import torch
     inp = WL.lawr_inputs(chi, dtype=dtype, seed=seed + 17 * dist.rank)
     net, tensors = lawr_network(tnb, inp)
@@ -228,6 +228,14 @@ def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, roof=True, s
     assert net.get_order() == order
     res = {"ms_per_step": ms / steps, "flop_per_step": flop, "order": order, "launches_per_step": launches}
     res["gflops"] = dist.sum(flop) / (ms / steps) / 1e6  # all ranks' work / max time
+    if graph:
+        # the same launch replayed from Network.compile() (CUDA graph: no host work per step)
+        cn = net.compile()
+        for _ in range(warmup):
+            cn.launch()
+        gms = time_steps(cn.launch, steps, flush, dist) / steps
+        res["graph_ms_per_step"] = gms
+        res["gflops_graph"] = dist.sum(flop) / gms / 1e6
     if e2e:
         # end to end through the public API: pinned host inputs -> HBM, launch, result -> host
         pinned = {nm: torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for nm, a in inp.items()}
@@ -355,7 +363,17 @@ def gpu_c4(tnb, steps, warmup, flush, dist):
     n_k, ms_k, _ = tnb._lib.ktimer_read(tnb._lib.KF_BS_GEMM)
     tnb._lib.ktimer_reset()
     kms = ms_k / max(n_k, 1)
-    return {"ms_per_call_eager": ms, "host_wall_ms_per_call": wall, "ms_per_call_graph": gms,
+    extra = {}
+    if dist.world > 1:
+        # one C4 contraction partitioned over the ranks (LPT output panels, local K
+        # reduction, NCCL all-gather of the slab): strong scaling of a single call
+        from paper_2401_01921_b200 import parallel
+        for _ in range(warmup):
+            parallel.contract_sharded(A, E)
+        sms = time_steps(lambda: parallel.contract_sharded(A, E), steps, flush, dist) / steps
+        extra = {"sharded_ms_per_call": sms, "sharded_gflops": 2 * C4_MACS / sms / 1e6,
+                 "sharded_scaling": "strong (one contraction partitioned over ranks + NCCL all-gather)"}
+    return {**extra, "ms_per_call_eager": ms, "host_wall_ms_per_call": wall, "ms_per_call_graph": gms,
             "bs_gemm_kernel_ms": kms, "bs_gemm_kernel_tflops": 2 * C4_MACS / kms / 1e9,
             "gflops_eager": dist.sum(2 * C4_MACS) / ms / 1e6, "gflops": dist.sum(2 * C4_MACS) / gms / 1e6}
 
@@ -547,9 +565,11 @@ def main():
         wl["lawr_c128_chi1024"] = {"value": round(c3["gflops"], 2), "unit": "GFLOP/s (8 flop/complex MAC)",
                                    "ms_per_step": c3["ms_per_step"], "roofline": c3["roofline"],
                                    "complex_mode": tnb.get_complex_mode()}
-        c1 = gpu_lawr(tnb, 128, np.float64, max(10, args.steps), args.warmup, flush, dist, e2e=False, roof=False)
-        wl["lawr_f64_chi128"] = {"value": round(c1["gflops"], 2), "unit": "GFLOP/s",
-                                 "ms_per_step": c1["ms_per_step"]}
+        c1 = gpu_lawr(tnb, 128, np.float64, max(10, args.steps), args.warmup, flush, dist, e2e=False, roof=False,
+                      graph=True)
+        wl["lawr_f64_chi128"] = {"value": round(c1["gflops"], 2), "unit": "GFLOP/s (eager Network.launch)",
+                                 "ms_per_step": c1["ms_per_step"], "graph_ms_per_step": c1["graph_ms_per_step"],
+                                 "gflops_graph": round(c1["gflops_graph"], 2)}
         perm = gpu_permute(tnb, max(4, args.steps), args.warmup, flush, dist)
         best = max(v["median_gbs"] for v in perm.values())
         wl["permute_sweep"] = {"unit": "GB/s (2 x bytes / time, median over perms)", "cases": perm,
