@@ -113,6 +113,18 @@ int tnb_contract_dense(const void* a, int dtype_a, int rank_a,
                        int nc, const int32_t* a_axes, const int32_t* b_axes,
                        void* out, int cplx_mode, void* stream);
 
+/* ---- batched strided copies (block slab <-> packed payload / sector matrix)
+ * For every segment: rows x row_bytes bytes from src + src_off (row pitch
+ * src_pitch) to dst + dst_off (row pitch dst_pitch). Offsets and pitches are in
+ * bytes relative to the two base pointers; segments must not overlap in dst.
+ * One launch; vector width chosen per row from the alignment. Used by the
+ * .utn container I/O (io.py:56-107 payload = blocks' C-order bytes in block
+ * order) and the block-sparse matricisation (linalg.py:70-142). */
+typedef struct {
+  int64_t src_off, dst_off, rows, row_bytes, src_pitch, dst_pitch;
+} TnbCopy2D;
+int tnb_copy2d_batched(const void* src, void* dst, int64_t nseg, const TnbCopy2D* segs, void* stream);
+
 /* ---- a3: zero-flux block enumeration (unitensor.py:31-45), host only ------
  * Bonds are given as flattened charge tables:
  *   nbonds, nsyms; nsec[b]; btype[b] (+1 IN, -1 OUT);

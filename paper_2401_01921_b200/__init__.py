@@ -11,7 +11,7 @@ Tensors live in HBM; the Python layer keeps the reference's labels / bonds /
 qnums / Network semantics and calls libtnb.so through a C ABI (include/tnb.h).
 There is no CPU fallback.
 """
-from . import eig, graphs, parallel, random, workloads
+from . import eig, graphs, linalg, parallel, random, workloads
 from . import dense as storage
 from ._lib import EngineError, EngineUnavailable
 from .blueprint import Network
@@ -22,6 +22,7 @@ from .contraction import (block_pairs, brute_force_order, contract, contract_pai
 from .dense import (Bool, Complex128, DenseTensor, Float64, Int64, arange, eye, from_numpy, kron, normal, ones,
                     uniform, zeros)
 from .labeled import ElementProxy, UniTensor
+from .io import load_unitensor, save_unitensor
 
 # Cytnx-style aliases (PAPER.md listings)
 Contract = contract
@@ -29,6 +30,7 @@ Contract = contract
 __version__ = "0.1.0"
 
 __all__ = [
+    "load_unitensor", "save_unitensor",
     "Bond", "BondType", "IN", "OUT", "REGULAR", "Bool", "Complex128", "DenseTensor", "ElementProxy", "Float64",
     "Int64", "Network", "Symmetry", "UniTensor", "EngineError", "EngineUnavailable", "arange", "block_pairs",
     "brute_force_order", "contract", "Contract", "contract_pair", "contraction_cost", "execute_tree", "eye",

@@ -22,7 +22,7 @@ EXPORTS = (
     "tnb_synchronize", "tnb_permute", "tnb_contract_dense",
     "tnb_zero_flux_blocks", "tnb_bs_contract", "tnb_bs_contract_masked", "tnb_optimal_order",
     "tnb_ktimer_enable", "tnb_ktimer_reset", "tnb_ktimer_read",
-    "tnb_bs_plan", "tnb_bs_execute", "tnb_bs_plan_pairs",
+    "tnb_bs_plan", "tnb_bs_execute", "tnb_bs_plan_pairs", "tnb_copy2d_batched",
 )
 
 # kernel families of the kernel timer (TNB_KF_* in include/tnb.h)
@@ -80,6 +80,7 @@ def _declare(lib):
                          ctypes.c_int, _pi32, _pi32, _pi32, _pi64, _i64, _p, _pi64, _pi64, _p], ctypes.c_int),
         "tnb_bs_execute": ([_i64, _p, _p, _p, _p], ctypes.c_int),
         "tnb_bs_plan_pairs": ([_i64, _i64, _pi32, _pi64, _p], ctypes.c_int),
+        "tnb_copy2d_batched": ([_p, _p, _i64, _p, _p], ctypes.c_int),
         "tnb_optimal_order": ([ctypes.c_int, ctypes.c_char_p, _pi32, _pi32, _pi64,
                                ctypes.c_char_p, _i64, ctypes.c_char_p], ctypes.c_int),
     }
@@ -301,6 +302,17 @@ def bs_plan(dtype, a_qn, a_shapes, a_perm, b_qn, b_shapes, b_perm, a_axes, b_axe
                             0 if mask is None else len(mask), None if mask is None else mask.ctypes.data_as(_p),
                             ctypes.byref(pid), ctypes.byref(npairs), stream), "bs_plan")
     return BsPlan(pid.value, npairs.value, na, nb, nout)
+
+
+COPY2D_DTYPE = np.dtype([("src_off", "<i8"), ("dst_off", "<i8"), ("rows", "<i8"), ("row_bytes", "<i8"),
+                         ("src_pitch", "<i8"), ("dst_pitch", "<i8")])  # TnbCopy2D
+
+
+def copy2d_batched(src_ptr, dst_ptr, segs, stream):
+    """One launch of tnb_copy2d_batched; `segs` is a COPY2D_DTYPE structured array."""
+    segs = np.ascontiguousarray(segs, dtype=COPY2D_DTYPE)
+    check(lib().tnb_copy2d_batched(src_ptr, dst_ptr, len(segs), segs.ctypes.data_as(_p) if len(segs) else None,
+                                   stream), "copy2d_batched")
 
 
 def optimal_order(names, label_lists, dims):

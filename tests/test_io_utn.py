@@ -1,0 +1,94 @@
+"""(f)4: the .utn container (pkg/src/tnkit/io.py) read into / written from HBM.
+
+Fixtures in tests/golden/utn were written by the REFERENCE's save_unitensor
+(oracle/make_golden_utn.py); loads must reproduce the blocks bit for bit and saves
+must reproduce the reference's files byte for byte."""
+import json
+import os
+import struct
+
+import numpy as np
+import pytest
+
+from paper_2401_01921_b200 import io as tio
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "utn")
+CASES = ["dense", "complex_directed", "u1", "u1xz2", "int64", "u1_odd_sectors", "u1_c128"]
+
+
+def _header(path):
+    raw = open(path, "rb").read()
+    assert raw[:5] == tio.MAGIC
+    (ver,) = struct.unpack("<I", raw[5:9])
+    (hlen,) = struct.unpack("<I", raw[9:13])
+    return ver, raw[13:13 + hlen], raw[13 + hlen:]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_bond_json_round_trip_matches_reference_header(case):
+    """CPU: bonds parsed from the reference's header serialise back to the same JSON."""
+    ver, hraw, _ = _header(os.path.join(GOLD, case + ".utn"))
+    assert ver == tio.VERSION
+    h = json.loads(hraw)
+    again = [tio._bond_to_json(tio._bond_from_json(d)) for d in h["bonds"]]
+    assert json.dumps(again) == json.dumps(h["bonds"])
+
+
+def test_bad_magic_and_version_rejected(tmp_path):
+    """CPU: same checks and messages as io.py:85-90, raised before any device work."""
+    bad = tmp_path / "bad.utn"
+    bad.write_bytes(b"NOPE\x00" + b"\x00" * 16)
+    with pytest.raises(ValueError, match="magic"):
+        tio.load_unitensor(bad)
+    raw = bytearray(open(os.path.join(GOLD, "dense.utn"), "rb").read())
+    raw[5] = 99
+    v = tmp_path / "v.utn"
+    v.write_bytes(bytes(raw))
+    with pytest.raises(ValueError, match="version"):
+        tio.load_unitensor(v)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES)
+def test_load_reference_file_bitexact(cuda, case):
+    z = np.load(os.path.join(GOLD, "blocks.npz"))
+    meta = json.loads(str(z["meta"]))[case]
+    t = tio.load_unitensor(os.path.join(GOLD, case + ".utn"))
+    assert t.name == meta["name"] and t.labels == meta["labels"] and t.rowrank == meta["rowrank"]
+    assert str(t.dtype) == meta["dtype"] and t.nblocks == meta["nblocks"]
+    if meta["qns"] is not None:
+        assert [list(q) for q in t._qns] == meta["qns"]
+    for i in range(t.nblocks):
+        want = z[f"{case}_b{i}"]
+        got = t.get_block_(i).numpy() if t.is_sym else t.get_block_().numpy()
+        assert got.dtype == want.dtype and np.array_equal(got, want), (case, i)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES)
+def test_save_reproduces_reference_bytes(cuda, tmp_path, case):
+    src = os.path.join(GOLD, case + ".utn")
+    t = tio.load_unitensor(src)
+    out = tmp_path / "out.utn"
+    tio.save_unitensor(t, out)
+    assert open(out, "rb").read() == open(src, "rb").read()
+
+
+@pytest.mark.gpu
+def test_lazily_permuted_blocks_are_materialised_on_save(cuda, tmp_path):
+    from paper_2401_01921_b200 import UniTensor
+    t = tio.load_unitensor(os.path.join(GOLD, "dense.utn"))
+    p = t.permute(["c", "a", "b"])  # lazy: save must run tnb_permute and write logical order
+    f = tmp_path / "p.utn"
+    p.save(f)
+    q = UniTensor.load(f)
+    assert q.labels == ["c", "a", "b"] and q.shape == p.shape
+    assert np.array_equal(q.get_block_().numpy(), p.get_block_().contiguous().numpy())
+    # block-sparse: a permuted tensor keeps its block LIST order (unitensor.py:312), so its
+    # file lists qn tuples out of enumeration order and the reference's loader rejects it
+    # (io.py:100-104); the engine mirrors that check and message
+    s = tio.load_unitensor(os.path.join(GOLD, "u1_odd_sectors.utn")).permute(["vr", "vl", "p"])
+    g = tmp_path / "s.utn"
+    s.save(g)
+    with pytest.raises(ValueError, match="Qn indices"):
+        UniTensor.load(g)
