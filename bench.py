@@ -428,6 +428,48 @@ def gpu_peps(tnb, n_sites, chi, D, d, steps, warmup, flush, dist):
             "flop_per_site": flop, "gflops": flop * n_sites / ms / 1e6}
 
 
+def c4_two_site(tnb, seed=5):
+    """(f)3 workload: a two-site U(1) wavefunction on the C4 bonds, psi[vl, p1, p2, vr],
+    rowrank 2 -> 23 charge sectors up to 516 x 516 (1.5M stored elements)."""
+    u1 = tnb.Symmetry.u1()
+    V = tnb.Bond(btype=tnb.IN, sectors=WL.c4_sectors(), syms=[u1])
+    P = tnb.Bond(btype=tnb.IN, sectors=[(1, 1), (-1, 1)], syms=[u1])
+    psi = tnb.UniTensor([V, P, P, V.redirect()], labels=["vl", "p1", "p2", "vr"], name="psi", rowrank=2)
+    tnb.random.normal_(psi, seed=seed)
+    return psi
+
+
+def gpu_svd(tnb, steps, warmup, flush, dist):
+    import torch
+    psi = c4_two_site(tnb)
+    fn = lambda: tnb.linalg.svd_truncate(psi, keepdim=1024)  # noqa: E731
+    for _ in range(max(1, warmup)):
+        fn()
+    ms = time_steps(fn, steps, flush, dist) / steps
+    return {"ms_per_call": ms, "keepdim": 1024, "sectors": 23,
+            "note": "per-sector factorisation = batched cuSOLVER (torch.linalg.svd); matricise/scatter = tnb_copy2d_batched"}
+
+
+def gpu_utn(tnb, steps, warmup, dist):
+    """(f)4 workload: .utn load of the C4 MPS tensor A (6.1 MB payload) from the page cache
+    into HBM (host wall: read + one H2D + one scatter launch, synchronised)."""
+    import tempfile
+    import torch
+    A, _ = c4_tensors(tnb)
+    path = os.path.join(tempfile.gettempdir(), f"tnb_c4_A_{dist.rank}.utn")
+    tnb.save_unitensor(A, path)
+    nbytes = sum(b.size * b.itemsize for b in A.get_blocks_())
+    for _ in range(max(1, warmup)):
+        tnb.load_unitensor(path)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        tnb.load_unitensor(path)
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) / steps * 1e3
+    return {"ms_per_load": ms, "payload_bytes": nbytes, "gbs": nbytes / ms / 1e6, "path": path}
+
+
 # ----------------------------------------------------------------------------- CPU side
 def cpu_threads():
     try:
@@ -471,6 +513,37 @@ def cpu_permute(budget_s=6.0):
         rates.append(2 * src.nbytes / (time.perf_counter() - t0) / 1e9)
     return {"value": float(np.median(rates)), "unit": "GB/s", "cores": 1, "kind": "port",
             "sample": f"{len(rates)} of the 23 rank-4 [64]^4 f64 permutes (np.ascontiguousarray, single-threaded)"}
+
+
+def cpu_svd(budget_s=3.0):
+    """Oracle port of svd_truncate (np.linalg.svd per sector, same ranking) on the C4
+    two-site sector matrices; matricisation excluded (it is host bookkeeping there)."""
+    import torch
+    import paper_2401_01921_b200 as tnb
+    psi = c4_two_site(tnb)
+    mz = tnb.linalg._Matricized(psi)
+    mats = [v[k].cpu().numpy() for m, n, mem, off, v in mz.groups for k in range(len(mem))]
+    ts = []
+    t_start = time.perf_counter()
+    while time.perf_counter() - t_start < budget_s and len(ts) < 10:
+        t0 = time.perf_counter()
+        ORACLE.svd_truncate_values(mats, 1024)
+        ts.append(time.perf_counter() - t0)
+    return {"value": min(ts) * 1e3, "unit": "ms per svd_truncate", "cores": cpu_threads(), "kind": "port",
+            "sample": f"{len(ts)} x 23-sector svd_truncate (np.linalg.svd, OpenBLAS), best-of"}
+
+
+def cpu_utn(path, nbytes, budget_s=2.0):
+    ts = []
+    t_start = time.perf_counter()
+    while time.perf_counter() - t_start < budget_s and len(ts) < 50:
+        t0 = time.perf_counter()
+        ORACLE.load_utn(path)
+        ts.append(time.perf_counter() - t0)
+    best = min(ts)
+    return {"value": nbytes / best / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": f"{len(ts)} loads of the C4 A tensor into numpy (io.py:83-107 restated), best-of",
+            "ms_per_load": best * 1e3}
 
 
 def cpu_c4(budget_s=3.0):
@@ -592,6 +665,11 @@ def main():
         pe = gpu_peps(tnb, 32, 256, 8, 2, 1, 1, flush, dist)
         wl["peps_chi256_D8"] = {"value": round(pe["gflops"], 2), "unit": "GFLOP/s",
                                 "scaling": "strong (32 sites sharded over ranks)", **pe}
+        sv = gpu_svd(tnb, 3, 1, flush, dist)
+        wl["svd_truncate_two_site_c4"] = {"value": round(sv["ms_per_call"], 3), "unit": "ms per call",
+                                          "higher_is_better": False, **sv}
+        ut = gpu_utn(tnb, 10, 2, dist)
+        wl["utn_load_c4"] = {"value": round(ut["gbs"], 3), "unit": "GB/s (payload / host wall)", **ut}
         line["workloads"] = wl
     if dist.rank == 0 and not args.no_cpu:
         cb = cpu_lawr(1024, np.float64)
@@ -600,6 +678,9 @@ def main():
             line["workloads"]["lawr_f64_chi128"]["cpu_baseline"] = cpu_lawr(128, np.float64, budget_s=2, max_iter=50)
             line["workloads"]["permute_sweep"]["cpu_baseline"] = cpu_permute()
             line["workloads"]["blocksparse_c4"]["cpu_baseline"] = cpu_c4()
+            line["workloads"]["svd_truncate_two_site_c4"]["cpu_baseline"] = cpu_svd()
+            u = line["workloads"]["utn_load_c4"]
+            line["workloads"]["utn_load_c4"]["cpu_baseline"] = cpu_utn(u["path"], u["payload_bytes"])
     if dist.rank == 0:
         print(json.dumps(line))
     return 0

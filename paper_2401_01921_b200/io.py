@@ -5,8 +5,9 @@ uint32 header length, a UTF-8 JSON header (``name``, ``labels``, ``rowrank``, ``
 ``bonds``, ``blocks``), then every block's C-order little-endian element bytes,
 concatenated in block-enumeration order.
 
-B200 path: the payload is read with ONE ``readinto`` into a pinned host
-buffer and crosses PCIe in ONE copy; a single ``tnb_copy2d_batched`` launch scatters the
+B200 path: the payload is read in 4 MB chunks into two pinned host
+buffers while the previous chunk crosses PCIe (file read and transfer overlap); a single
+``tnb_copy2d_batched`` launch scatters the
 packed blocks to their 64-byte-aligned places in the tensor's HBM slab. Saving runs the
 same in reverse: lazily
 permuted blocks are materialised by ``tnb_permute``, one gather launch packs the blocks,
@@ -118,16 +119,44 @@ def load_unitensor(path):
             if tuple(info["shape"]) != b.shape:
                 raise ValueError(f"{path}: block {i} has shape {tuple(info['shape'])}, expected {b.shape}")
         segs, base, nbytes = _segments(blocks, dt.itemsize, packed_to_slab=True)
-        host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
-        got = f.readinto(memoryview(host.numpy())) if nbytes else 0
-        if got != nbytes:
-            raise ValueError(f"{path}: truncated payload ({got} of {nbytes} bytes)")
-    if nbytes:
-        # one PCIe copy of the packed payload (pinned source: torch's host allocator keeps
-        # it alive until the copy has run), then one scatter launch into the block slab
-        staging = host.to(dense.device(), non_blocking=True)
-        _lib.copy2d_batched(staging.data_ptr(), base, segs, dense.stream_handle())
+        if nbytes:
+            staging = torch.empty(nbytes, dtype=torch.uint8, device=dense.device())
+            _read_to_device(f, staging, nbytes, path)
+            # one scatter launch: packed payload -> 64-byte-aligned blocks of the slab
+            _lib.copy2d_batched(staging.data_ptr(), base, segs, dense.stream_handle())
     return ut
+
+
+_CHUNK = 4 << 20
+_PINNED = []
+
+
+def _read_to_device(f, staging, nbytes, path):
+    """Pipelined file -> HBM: the file is read into two pinned chunk buffers in turn while
+    the previous chunk's host->device copy runs (read and PCIe transfer overlap)."""
+    if not _PINNED:
+        _PINNED.extend([torch.empty(_CHUNK, dtype=torch.uint8, pin_memory=True) for _ in range(2)])
+        _PINNED.extend([torch.cuda.Event(), torch.cuda.Event()])
+    bufs, evs = _PINNED[:2], _PINNED[2:]
+    stream = torch.cuda.current_stream()
+    pending = [False, False]
+    off, k = 0, 0
+    while off < nbytes:
+        n = min(_CHUNK, nbytes - off)
+        b = k & 1
+        if pending[b]:
+            evs[b].synchronize()  # the copy out of this buffer has finished
+        got = f.readinto(memoryview(bufs[b].numpy())[:n])
+        if got != n:
+            raise ValueError(f"{path}: truncated payload ({off + (got or 0)} of {nbytes} bytes)")
+        staging[off:off + n].copy_(bufs[b][:n], non_blocking=True)
+        evs[b].record(stream)
+        pending[b] = True
+        off += n
+        k += 1
+    for b in range(2):
+        if pending[b]:
+            evs[b].synchronize()  # buffers are reused by the next load
 
 
 def _save_method(self, path):

@@ -133,3 +133,58 @@ def test_c4_structure_golden():
     assert [list(t) for t in trip] == meta["triples"]
     norms = [np.linalg.norm(r) for r in res]
     assert np.allclose(norms, z["norms"], rtol=1e-12, atol=0)
+
+
+def test_oracle_utn_loader_matches_reference_files():
+    """The oracle's .utn reader reproduces the reference-written fixtures' blocks."""
+    import json
+    import os
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "utn")
+    z = np.load(os.path.join(gold, "blocks.npz"))
+    meta = json.loads(str(z["meta"]))
+    for case, m in meta.items():
+        header, blocks = oracle.load_utn(os.path.join(gold, case + ".utn"))
+        assert header["name"] == m["name"] and header["labels"] == m["labels"] and len(blocks) == m["nblocks"]
+        for i, b in enumerate(blocks):
+            assert np.array_equal(b, z[f"{case}_b{i}"])
+
+
+def test_oracle_svd_truncate_matches_reference_goldens():
+    """Sector matricisation + truncation ranking of the oracle vs the reference's outputs."""
+    import json
+    import os
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "svd.npz"))
+    meta = json.loads(str(z["meta"]))
+    for name, m in meta.items():
+        st = m["input"]
+        if st["qns"] is None:
+            mats = [z[f"{name}_in0"].reshape(int(np.prod(z[f"{name}_in0"].shape[:st["rowrank"]])), -1)]
+        else:
+            bonds = st["bonds"]
+            r = st["rowrank"]
+            nsym = len(bonds[0]["syms"])
+            mods = [0 if s == "U1" else int(s[1:]) for s in bonds[0]["syms"]]
+
+            def charge(rq):
+                c = [0] * nsym
+                for b, k in zip(bonds[:r], rq):
+                    q = bonds and b["sectors"][k][0]
+                    sgn = -1 if b["btype"] == "OUT" else 1
+                    c = [(x + sgn * y) % n if n else x + sgn * y for x, y, n in zip(c, q, mods)]
+                return tuple(c)
+            blocks = [z[f"{name}_in{i}"] for i in range(len(st["qns"]))]
+            mats = [mm for _, mm in oracle.sector_matrices(
+                blocks, [tuple(q) for q in st["qns"]],
+                lambda rq: int(np.prod([bonds[a]["sectors"][k][1] for a, k in enumerate(rq)])),
+                lambda cq: int(np.prod([bonds[r + a]["sectors"][k][1] for a, k in enumerate(cq)])),
+                charge, r)]
+        smax = max(float(np.max(np.linalg.svd(mm, compute_uv=False))) for mm in mats)
+        keeps, ss, _, _, _ = oracle.svd_truncate_values(mats, 10 ** 9)
+        for i, s in enumerate(ss):
+            assert np.max(np.abs(s - z[f"{name}_s{i}"])) <= 1e-12 * smax
+        for k, tr in enumerate(m["trunc"]):
+            keeps, ss, _, _, disc = oracle.svd_truncate_values(mats, tr["keepdim"], tr["err"], tr["min_blockdim"])
+            assert [x for x in keeps if x > 0] == [shp[0] for shp in tr["S"]["shapes"]]
+            want = z[f"{name}_t{k}_err"]
+            got = np.array(disc) if disc else np.zeros(1)
+            assert np.allclose(got, want, rtol=0, atol=1e-12 * max(1.0, smax))
