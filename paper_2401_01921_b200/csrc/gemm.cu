@@ -137,6 +137,77 @@ __global__ void splitk_reduce_kernel(const typename Elem<CPLX>::T* __restrict__ 
   }
 }
 
+// ------------------------------------------------------------------ dot kernel
+// C[M, N] with M * N <= 16 and any K (a (nearly) fully contracted step, e.g. the closing
+// a* contraction of a PEPS site: M = N = 1, K = 8192): memory-bound, no tensor-core tile
+// to fill. CTA c sums its contiguous K chunk for every output (thread-strided k, fixed
+// shuffle tree, warps summed in order) and writes one partial per output;
+// splitk_reduce_kernel then adds the CTA partials in CTA order -- deterministic.
+template <bool CPLX>
+__global__ void __launch_bounds__(256) dot_kernel(const typename Elem<CPLX>::T* __restrict__ A,
+                                                  const typename Elem<CPLX>::T* __restrict__ B,
+                                                  typename Elem<CPLX>::T* __restrict__ ws,
+                                                  const __grid_constant__ GemmDesc d, int64_t kchunk) {
+  using T = typename Elem<CPLX>::T;
+  constexpr int MAXMN = 16;
+  __shared__ int64_t rowOff[MAXMN], colOff[MAXMN];
+  __shared__ T red[8][MAXMN];
+  const int M = d.M, N = d.N, MN = M * N;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < M) rowOff[tid] = group_offset(d.rowA, tid);
+  if (tid >= 32 && tid - 32 < N) colOff[tid - 32] = group_offset(d.colB, tid - 32);
+  __syncthreads();
+  const int64_t kb = (int64_t)blockIdx.x * kchunk;
+  const int64_t ke = min64((int64_t)d.K, kb + kchunk);
+  double re[MAXMN], im[MAXMN];
+#pragma unroll
+  for (int j = 0; j < MAXMN; ++j) re[j] = im[j] = 0.0;
+  for (int64_t k = kb + tid; k < ke; k += blockDim.x) {
+    const int64_t oa = group_offset(d.kA, (uint32_t)k), ob = group_offset(d.kB, (uint32_t)k);
+#pragma unroll
+    for (int m = 0; m < MAXMN; ++m) {
+      if (m >= M) break;
+      const T a = __ldcs(A + rowOff[m] + oa);
+#pragma unroll
+      for (int n = 0; n < MAXMN; ++n) {
+        if (n >= N || m * N + n >= MAXMN) break;
+        const T b = __ldg(B + colOff[n] + ob);
+        const int j = m * N + n;
+        if constexpr (!CPLX) {
+          re[j] = fma(a, b, re[j]);
+        } else {
+          re[j] = fma(a.x, b.x, re[j]);
+          re[j] = fma(-a.y, b.y, re[j]);
+          im[j] = fma(a.x, b.y, im[j]);
+          im[j] = fma(a.y, b.x, im[j]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < MAXMN; ++j) {
+    if (j >= MN) break;
+    double x = re[j], y = im[j];
+    for (int o = 16; o > 0; o >>= 1) {
+      x += __shfl_xor_sync(0xffffffffu, x, o);
+      if constexpr (CPLX) y += __shfl_xor_sync(0xffffffffu, y, o);
+    }
+    if (lane == 0) {
+      if constexpr (!CPLX) red[warp][j] = x;
+      else red[warp][j] = make_double2(x, y);
+    }
+  }
+  __syncthreads();
+  if (tid < MN) {
+    T s = red[0][tid];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      if constexpr (!CPLX) s += red[w][tid];
+      else s = make_double2(s.x + red[w][tid].x, s.y + red[w][tid].y);
+    }
+    ws[(int64_t)blockIdx.x * MN + tid] = s;
+  }
+}
+
 // ------------------------------------------------------------------ narrow kernel
 // C[M, N] for N <= 16, K <= 32 (the T1.W step of L.A.W.R: N = K = 10): HBM-bound.
 // One warp owns 32 consecutive rows (one per lane): a lane issues all K gathered
@@ -530,14 +601,49 @@ size_t skinny_smem(const GemmDesc& d) {
   return (size_t)ES * (d.K * d.N + 128 * (d.K + 1) + 128 * d.N) + 8 * (d.K + 128);
 }
 
+template <bool CPLX>
+int run_dot(const void* A, const void* B, void* C, const GemmDesc& d, cudaStream_t st) {
+  using T = typename Elem<CPLX>::T;
+  constexpr int ES = CPLX ? 16 : 8;
+  const int64_t K = d.K, MN = (int64_t)d.M * d.N;
+  const int64_t G = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms() * 4, (K + 2047) / 2048));
+  const int64_t kchunk = (K + G - 1) / G;
+  void* ws = nullptr;
+  TNB_CUDA_CHECK(cudaMallocAsync(&ws, (size_t)(G * MN) * ES, st));
+  {
+    KTimer kt(TNB_KF_GEMM_SKINNY, st, 2.0 * d.M * (double)d.N * d.K * (CPLX ? 4 : 1));
+    dot_kernel<CPLX><<<(unsigned)G, 256, 0, st>>>(static_cast<const T*>(A), static_cast<const T*>(B),
+                                                  static_cast<T*>(ws), d, kchunk);
+  }
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    splitk_reduce_kernel<CPLX><<<1, 32, 0, st>>>(static_cast<const T*>(ws), static_cast<T*>(C), MN, (int)G);
+    count_launch();
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(ws, st);
+  if (e != cudaSuccess) return cuda_fail(e, "contract: dot kernel launch");
+  return TNB_OK;
+}
+
 template <bool CPLX, int MODE>
 int dispatch(const void* A, const void* B, void* C, GemmDesc& d, cudaStream_t st) {
+  if ((int64_t)d.M * d.N <= 16) return run_dot<CPLX>(A, B, C, d, st);
   if (d.N <= 16 && d.K <= 16 && d.M >= 4096) return run_narrow<CPLX, 16, 16>(A, B, C, d, st);
   if constexpr (!CPLX)
     if (d.N <= 16 && d.K <= 32 && d.M >= 4096) return run_narrow<CPLX, 16, 32>(A, B, C, d, st);
   if (d.N <= 64 && d.K <= 64 && d.M >= 4096 && skinny_smem<CPLX>(d) <= 160 * 1024)
     return run_skinny<CPLX>(A, B, C, d, st);
-  if constexpr (!CPLX) return StreamK<false, 0, 128, 128, 16, 4, 4, 4>::run(A, B, C, d, st);
+  if constexpr (!CPLX) {
+    // tile shape with the least padding (N = 64 or M = 64 rows waste half a 128 x 128 tile)
+    auto pad = [](int64_t x, int64_t t) { return (x + t - 1) / t * t; };
+    const int64_t a128 = pad(d.M, 128) * pad(d.N, 128), aN64 = pad(d.M, 128) * pad(d.N, 64),
+                  aM64 = pad(d.M, 64) * pad(d.N, 128);
+    if (aN64 < a128 && aN64 <= aM64) return StreamK<false, 0, 128, 64, 16, 4, 4, 4>::run(A, B, C, d, st);
+    if (aM64 < a128) return StreamK<false, 0, 64, 128, 16, 4, 4, 4>::run(A, B, C, d, st);
+    return StreamK<false, 0, 128, 128, 16, 4, 4, 4>::run(A, B, C, d, st);
+  }
   else if constexpr (MODE == 0) return StreamK<true, 0, 64, 128, 8, 4, 4, 4>::run(A, B, C, d, st);
   else return StreamK<true, 1, 64, 64, 8, 4, 4, 4>::run(A, B, C, d, st);
 }
@@ -590,12 +696,35 @@ int contract_dense_device(const void* a, int dta, int ra, const int64_t* sa, con
     if (!acon[k]) rowA.push_back({A.ldim[k], A.lstride[k]});
   for (int k = 0; k < rb; ++k)
     if (!bcon[k]) colB.push_back({B.ldim[k], B.lstride[k]});
+  rowA = merge_digits(rowA);
+  colB = merge_digits(colB);
   // contracted digits: merge only when both operands allow it
   std::vector<Digit> ka_raw, kb_raw;
   for (int i = 0; i < nc; ++i) {
     if (A.ldim[aax[i]] == 1) continue;
     ka_raw.push_back({A.ldim[aax[i]], A.lstride[aax[i]]});
     kb_raw.push_back({B.ldim[bax[i]], B.lstride[bax[i]]});
+  }
+  // An operand whose free rows (cols) are not unit-stride is gathered along K, so its
+  // loads coalesce only if consecutive k are adjacent in ITS memory: when exactly one
+  // operand is like that, walk K in that operand's memory order (strides descending).
+  // (Summation order over K is free; e.g. the PEPS a* step reads B with a 128 KB
+  // stride per k in shared-label order -- 8.7x DRAM over-fetch -- and at stride 1 here.)
+  const bool a_kfast = !(!rowA.empty() && rowA.back().stride == 1 && rowA.back().dim >= 4);
+  const bool b_kfast = !(!colB.empty() && colB.back().stride == 1 && colB.back().dim >= 4);
+  const bool k_memorder = a_kfast != b_kfast && ka_raw.size() > 1;
+  if (k_memorder) {
+    std::vector<size_t> idx(ka_raw.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+    const std::vector<Digit>& key = a_kfast ? ka_raw : kb_raw;
+    std::stable_sort(idx.begin(), idx.end(), [&](size_t x, size_t y) { return key[x].stride > key[y].stride; });
+    std::vector<Digit> ka2, kb2;
+    for (size_t i : idx) {
+      ka2.push_back(ka_raw[i]);
+      kb2.push_back(kb_raw[i]);
+    }
+    ka_raw.swap(ka2);
+    kb_raw.swap(kb2);
   }
   for (size_t i = 0; i < ka_raw.size(); ++i) {
     if (!kA.empty() && kA.back().stride == ka_raw[i].dim * ka_raw[i].stride &&
@@ -609,12 +738,14 @@ int contract_dense_device(const void* a, int dta, int ra, const int64_t* sa, con
       kB.push_back(kb_raw[i]);
     }
   }
-  rowA = merge_digits(rowA);
-  colB = merge_digits(colB);
   // Contraction order over K is free (only the summation order changes): put the
   // digit that makes every 16-wide k-tile affine innermost, preferring a digit
-  // that is contiguous in one of the operands.
-  if (kA.size() > 1) {
+  // that is contiguous in one of the operands -- unless K follows the memory order of
+  // the one k-gathered operand (its smallest-stride digit innermost: coalescing beats
+  // the cheaper affine address path; e.g. the PEPS a* step, innermost dn at stride 2
+  // interleaved with the free s axis of the same rows).
+  const bool keep_order = k_memorder;
+  if (kA.size() > 1 && !keep_order) {
     int best = -1;
     int64_t best_score = -1;
     for (size_t i = 0; i < kA.size(); ++i) {

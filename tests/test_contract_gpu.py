@@ -146,3 +146,30 @@ def test_async_upload_is_awaited_by_the_consumer(cuda):
         A.get_block_().upload_(np.zeros(7))
     with pytest.raises(TypeError):
         A.get_block_().upload_(np.zeros((300, 200), dtype=np.complex128))
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.complex128])
+def test_dispatch_paths_dot_and_half_tiles(cuda, dt, cplx_mode):
+    """Every GEMM dispatch path against numpy: M*N <= 16 (dot kernel + ordered CTA reduce),
+    N = 64 / M = 64 / N = 192 (128x64 and 64x128 stream-K tiles), permuted operands."""
+    rng = np.random.default_rng(31)
+
+    def arr(shape):
+        x = rng.standard_normal(shape)
+        if dt == np.complex128:
+            x = x + 1j * rng.standard_normal(shape)
+        return x.astype(dt)
+
+    cases = [((1, 10007), (10007, 1)), ((3, 777), (777, 5)), ((16, 4096), (4096, 1)),
+             ((300, 500), (500, 64)), ((64, 500), (500, 300)), ((257, 129), (129, 192))]
+    for (m, k), (k2, n) in cases:
+        a, b = arr((k, m)), arr((n, k2))  # stored transposed: the contraction reads permuted views
+        A = UniTensor(storage.from_numpy(a), labels=["k", "m"]).permute(["m", "k"])
+        B = UniTensor(storage.from_numpy(b), labels=["n", "k"]).permute(["k", "n"])
+        got = contract(A, B).numpy()
+        want = a.T @ b.T
+        assert rel_fro(got, want) <= 1e-13, ((m, k, n), rel_fro(got, want))
+    # deterministic: a second call is bit-identical
+    A = UniTensor(storage.from_numpy(arr((2, 50000))), labels=["m", "k"])
+    B = UniTensor(storage.from_numpy(arr((50000, 3))), labels=["k", "n"])
+    assert np.array_equal(contract(A, B).numpy(), contract(A, B).numpy())

@@ -42,6 +42,17 @@ def c4(iters):
     torch.cuda.synchronize()
 
 
+def peps_step(iters):
+    """The C5 a* step: A(256,8,256,8,8,8,2) x B(8,8,256,256,8,8) -> (8,8,2,8,8) (M=128, N=64)."""
+    a = storage.normal([256, 8, 256, 8, 8, 8, 2], seed=1)
+    b = storage.normal([8, 8, 256, 256, 8, 8], seed=2)
+    A = UniTensor(a, labels=["c1", "l", "c2", "dn", "u", "r", "s"])
+    B = UniTensor(b, labels=["u2", "r2", "c1", "c2", "l", "dn"])
+    for _ in range(iters):
+        tnb.contract(A, B)
+    torch.cuda.synchronize()
+
+
 if __name__ == "__main__":
     torch.cuda.set_device(0)
     what = sys.argv[1]
@@ -51,6 +62,8 @@ if __name__ == "__main__":
         perms = [tuple(int(c) for c in p) for p in sys.argv[4].split(",")]
         permute(tuple(int(x) for x in sys.argv[2].split("x")), np.complex128 if sys.argv[3] == "c128" else np.float64,
                 perms, int(sys.argv[5]))
+    elif what == "peps_step":
+        peps_step(int(sys.argv[2]))
     elif what == "c4":
         c4(int(sys.argv[2]))
     print("done")
