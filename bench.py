@@ -378,6 +378,22 @@ def gpu_c4(tnb, steps, warmup, flush, dist):
             "gflops_eager": dist.sum(2 * C4_MACS) / ms / 1e6, "gflops": dist.sum(2 * C4_MACS) / gms / 1e6}
 
 
+def gpu_c4_batch(tnb, n_total, steps, warmup, flush, dist):
+    """A batch of independent C4 block-sparse contractions (e.g. the sites of a sweep),
+    sharded by unit across ranks (no data-path collective): strong scaling of the batch."""
+    mine = [i for i in range(n_total) if i % dist.world == dist.rank]
+    pairs = [c4_tensors(tnb, seed=777 + 2 * i) for i in mine]
+
+    def step():
+        for A, E in pairs:
+            tnb.contract(A, E)
+    for _ in range(warmup):
+        step()
+    ms = time_steps(step, steps, flush, dist) / steps
+    return {"ms_per_step": ms, "instances": n_total, "per_rank": len(mine),
+            "gflops": 2 * C4_MACS * n_total / ms / 1e6}
+
+
 def gpu_lawr_batch(tnb, n_total, chi, dtype, steps, warmup, flush, dist):
     """C3b: a batch of independent L.A.W.R matvecs, sharded by instance across ranks."""
     mine = [i for i in range(n_total) if i % dist.world == dist.rank]
@@ -659,6 +675,9 @@ def main():
                                              "traffic": traffic_per_launch("bs_sk_kernel", np.float64),
                                              "kernel": "bs_sk_kernel (grouped stream-K DMMA.8x8x4)",
                                              "peak_source": PEAK_SOURCE}}
+        cb = gpu_c4_batch(tnb, 64, max(3, args.steps // 2), args.warmup, flush, dist)
+        wl["blocksparse_c4_batch64"] = {"value": round(cb["gflops"], 2), "unit": "GFLOP/s",
+                                        "scaling": "strong (64 contractions sharded over ranks)", **cb}
         bt = gpu_lawr_batch(tnb, 64, 512, np.complex128, max(2, args.steps // 4), 1, flush, dist)
         wl["lawr_batch64_c128_chi512"] = {"value": round(bt["gflops"], 2), "unit": "GFLOP/s (8 flop/complex MAC)",
                                           "scaling": "strong (64 instances sharded over ranks)", **bt}

@@ -640,6 +640,10 @@ int dispatch(const void* A, const void* B, void* C, GemmDesc& d, cudaStream_t st
     auto pad = [](int64_t x, int64_t t) { return (x + t - 1) / t * t; };
     const int64_t a128 = pad(d.M, 128) * pad(d.N, 128), aN64 = pad(d.M, 128) * pad(d.N, 64),
                   aM64 = pad(d.M, 64) * pad(d.N, 128);
+    // small problems (fewer than ~8 k-iterations of 128 x 128 tiles per SM, e.g. L.A.W.R at
+    // chi = 128): 64 x 64 tiles give 4x more stream-K work units, so more SMs take part
+    const int64_t it128 = (pad(d.M, 128) / 128) * (pad(d.N, 128) / 128) * ((d.K + 15) / 16);
+    if (it128 < (int64_t)sms() * 8) return StreamK<false, 0, 64, 64, 16, 4, 4, 4>::run(A, B, C, d, st);
     if (aN64 < a128 && aN64 <= aM64) return StreamK<false, 0, 128, 64, 16, 4, 4, 4>::run(A, B, C, d, st);
     if (aM64 < a128) return StreamK<false, 0, 64, 128, 16, 4, 4, 4>::run(A, B, C, d, st);
     return StreamK<false, 0, 128, 128, 16, 4, 4, 4>::run(A, B, C, d, st);

@@ -173,3 +173,13 @@ def test_dispatch_paths_dot_and_half_tiles(cuda, dt, cplx_mode):
     A = UniTensor(storage.from_numpy(arr((2, 50000))), labels=["m", "k"])
     B = UniTensor(storage.from_numpy(arr((50000, 3))), labels=["k", "n"])
     assert np.array_equal(contract(A, B).numpy(), contract(A, B).numpy())
+
+
+def test_small_problem_tiles(cuda):
+    """chi = 128 L.A.W.R-sized steps take the 64 x 64 stream-K tiles: parity vs numpy."""
+    rng = np.random.default_rng(5)
+    for (m, k, n) in [(256, 128, 640), (200, 640, 100), (65, 33, 70)]:
+        a, b = rng.standard_normal((m, k)), rng.standard_normal((k, n))
+        A = UniTensor(storage.from_numpy(a), labels=["m", "k"])
+        B = UniTensor(storage.from_numpy(b), labels=["k", "n"])
+        assert rel_fro(contract(A, B).numpy(), a @ b) <= 1e-13
