@@ -463,7 +463,8 @@ def gpu_svd(tnb, steps, warmup, flush, dist):
         fn()
     ms = time_steps(fn, steps, flush, dist) / steps
     return {"ms_per_call": ms, "keepdim": 1024, "sectors": 23,
-            "note": "per-sector factorisation = batched cuSOLVER (torch.linalg.svd); matricise/scatter = tnb_copy2d_batched"}
+            "note": "float64 sectors: one launch of the batched one-sided Jacobi kernel (tnb_svd_jacobi_batched, "
+                    "a 16-CTA cluster per sector); matricise/scatter = tnb_copy2d_batched"}
 
 
 def gpu_utn(tnb, steps, warmup, dist):

@@ -125,6 +125,23 @@ typedef struct {
 } TnbCopy2D;
 int tnb_copy2d_batched(const void* src, void* dst, int64_t nseg, const TnbCopy2D* segs, void* stream);
 
+/* ---- batched one-sided Jacobi SVD of sector matrices (linalg.py:246-341) ---
+ * Each sector: A (m x n, 1 <= m <= n, row-major float64) in `a` (read only),
+ * workspaces b (m x n) and q (m x m); outputs the thin factors in torch/LAPACK layout
+ * u (m x m row-major), s (m, descending), vh (m x n row-major) and *status:
+ * sweeps used (> 0), -1 not converged within max_sweeps, -2 rank deficient
+ * (a singular value <= rank_tol * max: its v row cannot be normalised; the
+ * caller recomputes that sector). A row pair is rotated while
+ * |b_p.b_q| > tol * sqrt(n) * eps * |b_p||b_q| (eps = 2^-52).
+ * One thread-block cluster per sector, all sectors in one launch. */
+typedef struct {
+  void *a, *b, *q, *u, *s, *vh;
+  int32_t* status;
+  int64_t m, n;
+} TnbSvdSector;
+int tnb_svd_jacobi_batched(int nsec, const TnbSvdSector* secs, int max_sweeps, double tol,
+                           double rank_tol, void* stream);
+
 /* ---- a3: zero-flux block enumeration (unitensor.py:31-45), host only ------
  * Bonds are given as flattened charge tables:
  *   nbonds, nsyms; nsec[b]; btype[b] (+1 IN, -1 OUT);

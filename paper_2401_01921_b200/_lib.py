@@ -22,7 +22,7 @@ EXPORTS = (
     "tnb_synchronize", "tnb_permute", "tnb_contract_dense",
     "tnb_zero_flux_blocks", "tnb_bs_contract", "tnb_bs_contract_masked", "tnb_optimal_order",
     "tnb_ktimer_enable", "tnb_ktimer_reset", "tnb_ktimer_read",
-    "tnb_bs_plan", "tnb_bs_execute", "tnb_bs_plan_pairs", "tnb_copy2d_batched",
+    "tnb_bs_plan", "tnb_bs_execute", "tnb_bs_plan_pairs", "tnb_copy2d_batched", "tnb_svd_jacobi_batched",
 )
 
 # kernel families of the kernel timer (TNB_KF_* in include/tnb.h)
@@ -81,6 +81,8 @@ def _declare(lib):
         "tnb_bs_execute": ([_i64, _p, _p, _p, _p], ctypes.c_int),
         "tnb_bs_plan_pairs": ([_i64, _i64, _pi32, _pi64, _p], ctypes.c_int),
         "tnb_copy2d_batched": ([_p, _p, _i64, _p, _p], ctypes.c_int),
+        "tnb_svd_jacobi_batched": ([ctypes.c_int, _p, ctypes.c_int, ctypes.c_double, ctypes.c_double, _p],
+                                   ctypes.c_int),
         "tnb_optimal_order": ([ctypes.c_int, ctypes.c_char_p, _pi32, _pi32, _pi64,
                                ctypes.c_char_p, _i64, ctypes.c_char_p], ctypes.c_int),
     }
@@ -313,6 +315,18 @@ def copy2d_batched(src_ptr, dst_ptr, segs, stream):
     segs = np.ascontiguousarray(segs, dtype=COPY2D_DTYPE)
     check(lib().tnb_copy2d_batched(src_ptr, dst_ptr, len(segs), segs.ctypes.data_as(_p) if len(segs) else None,
                                    stream), "copy2d_batched")
+
+
+SVD_SECTOR_DTYPE = np.dtype([("a", "<u8"), ("b", "<u8"), ("q", "<u8"), ("u", "<u8"), ("s", "<u8"), ("vh", "<u8"),
+                             ("status", "<u8"), ("m", "<i8"), ("n", "<i8")])  # TnbSvdSector
+
+
+def svd_jacobi_batched(sectors, stream, max_sweeps=30, tol=2.0, rank_tol=1e-13):
+    """One launch of tnb_svd_jacobi_batched over a SVD_SECTOR_DTYPE structured array."""
+    secs = np.ascontiguousarray(sectors, dtype=SVD_SECTOR_DTYPE)
+    check(lib().tnb_svd_jacobi_batched(len(secs), secs.ctypes.data_as(_p) if len(secs) else None,
+                                       int(max_sweeps), float(tol), float(rank_tol), stream),
+          "svd_jacobi_batched")
 
 
 def optimal_order(names, label_lists, dims):

@@ -16,10 +16,13 @@ Same contract as the reference (pkg/src/tnkit/linalg.py):
 
 B200 path: blocks -> sector matrices is ONE ``tnb_copy2d_batched`` launch into a
 sector slab laid out by matrix shape, so every group of equal-shape sectors is already a
-``[batch, m, n]`` array; each shape group is factorised by one batched cuSOLVER call
-(``torch.linalg.svd`` -- a library factorisation, like cuBLAS for a plain GEMM); the
-factors U / S / Vdag are scattered into their block slabs by one ``tnb_copy2d_batched``
-launch each. Only the singular values (for the truncation ranking) cross to the host.
+``[batch, m, n]`` array; all float64 sectors are factorised by ONE launch of the
+engine's batched one-sided Jacobi kernel (``tnb_svd_jacobi_batched``, csrc/svd.cu: a
+thread-block cluster per sector, all sectors concurrently); complex128 sectors and any
+sector the kernel flags (not converged / rank deficient) use the library factorisation
+(``torch.linalg.svd``, cuSOLVER). The factors U / S / Vdag are scattered into their block
+slabs by one ``tnb_copy2d_batched`` launch each. Only the singular values (for the
+truncation ranking) and the per-group status words cross to the host.
 """
 import numpy as np
 import torch
@@ -149,14 +152,61 @@ def _row_charge(row_bonds, row_qn, syms):
     return charge
 
 
+# float64 sector matrices go through the engine's batched Jacobi kernel
+# (tnb_svd_jacobi_batched: one thread-block cluster per sector, all sectors in one launch);
+# complex128, and any sector the kernel flags (not converged / rank deficient), through the
+# library factorisation. "library" forces the latter for everything.
+SVD_BACKEND = "jacobi"
+
+
+def _library_svd(view):
+    u, s, vh = torch.linalg.svd(view, full_matrices=False)
+    # cuSOLVER hands back column-major factors as strided (and, for complex Vh, lazily
+    # conjugated) views; the scatters read plain row-major memory
+    return u.resolve_conj().contiguous(), s.contiguous(), vh.resolve_conj().contiguous()
+
+
+def _transpose(batch):
+    """[b, r, c] -> [b, c, r] through tnb_permute (contiguous device tensors)."""
+    b, r, c = batch.shape
+    out = torch.empty((b, c, r), dtype=batch.dtype, device=batch.device)
+    if batch.numel():
+        _lib.permute(batch.data_ptr(), out.data_ptr(), batch.element_size(), [b, r, c], [0, 2, 1],
+                     dense.stream_handle())
+    return out
+
+
 def _factorise(mz):
-    """Batched thin SVD of every shape group: (U, S, Vh) device tensors per group."""
+    """Thin SVD of every shape group: (U [b,m,k], S [b,k], Vh [b,k,n]) device tensors."""
+    if mz.dt != dense.Float64 or SVD_BACKEND != "jacobi":
+        return [_library_svd(g[4]) for g in mz.groups]
+    jobs, recs = [], []
+    for gi, (m, n, members, off, view) in enumerate(mz.groups):
+        tall = m > n
+        a = _transpose(view) if tall else view  # rows to orthogonalise: the shorter side
+        b, r, c = a.shape
+        dev = a.device
+        u = torch.empty((b, r, r), dtype=torch.float64, device=dev)
+        sv = torch.empty((b, r), dtype=torch.float64, device=dev)
+        vh = torch.empty((b, r, c), dtype=torch.float64, device=dev)
+        q = torch.empty((b, r, r), dtype=torch.float64, device=dev)
+        w = torch.empty((b, r, c), dtype=torch.float64, device=dev)  # rotated rows (a stays intact)
+        st = torch.zeros(b, dtype=torch.int32, device=dev)
+        es = 8
+        for k in range(b):
+            jobs.append((a.data_ptr() + k * r * c * es, w.data_ptr() + k * r * c * es, q.data_ptr() + k * r * r * es,
+                         u.data_ptr() + k * r * r * es, sv.data_ptr() + k * r * es, vh.data_ptr() + k * r * c * es,
+                         st.data_ptr() + 4 * k, r, c))
+        recs.append((tall, u, sv, vh, q, st, (a, w)))
+    _lib.svd_jacobi_batched(np.array(jobs, dtype=_lib.SVD_SECTOR_DTYPE), dense.stream_handle())
     out = []
-    for m, n, members, off, view in mz.groups:
-        u, s, vh = torch.linalg.svd(view, full_matrices=False)
-        # cuSOLVER hands back column-major factors as strided (and, for complex Vh, lazily
-        # conjugated) views; the scatters read plain row-major memory
-        out.append((u.resolve_conj().contiguous(), s.contiguous(), vh.resolve_conj().contiguous()))
+    for (m, n, members, off, view), (tall, u, sv, vh, q, st, a) in zip(mz.groups, recs):
+        if bool((st <= 0).any()):  # (one small device->host read per group)
+            out.append(_library_svd(view))
+            continue
+        if tall:  # A^T = U' S V'^T  ->  A = V' S U'^T
+            u, vh = _transpose(vh), _transpose(u)
+        out.append((u, sv, vh))
     return out
 
 
