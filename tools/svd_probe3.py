@@ -34,9 +34,9 @@ for tol in (2.0, 8.0, 32.0):
     for sweeps in (30,):
         jobs = []
         a = torch.randn(516, 516, dtype=torch.float64, device="cuda")
-        q = torch.empty_like(a); u = torch.empty_like(a); vh = torch.empty_like(a)
+        q = torch.empty_like(a); u = torch.empty_like(a); vh = torch.empty_like(a); w = torch.empty_like(a)
         s = torch.empty(516, dtype=torch.float64, device="cuda"); st = torch.zeros(1, dtype=torch.int32, device="cuda")
-        jobs.append((a.data_ptr(), q.data_ptr(), u.data_ptr(), s.data_ptr(), vh.data_ptr(), st.data_ptr(), 516, 516))
+        jobs.append((a.data_ptr(), w.data_ptr(), q.data_ptr(), u.data_ptr(), s.data_ptr(), vh.data_ptr(), st.data_ptr(), 516, 516))
         ref = torch.linalg.svdvals(a.clone())
         torch.cuda.synchronize()
         t0 = time.perf_counter()
