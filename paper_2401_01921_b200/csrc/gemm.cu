@@ -21,6 +21,7 @@
 // no atomics). Very skinny problems (N, K <= 64: e.g. the MPO step of
 // L.A.W.R) go to a separate memory-bound kernel.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -646,6 +647,7 @@ int dispatch(const void* A, const void* B, void* C, GemmDesc& d, cudaStream_t st
     if (it128 < (int64_t)sms() * 8) return StreamK<false, 0, 64, 64, 16, 4, 4, 4>::run(A, B, C, d, st);
     if (aN64 < a128 && aN64 <= aM64) return StreamK<false, 0, 128, 64, 16, 4, 4, 4>::run(A, B, C, d, st);
     if (aM64 < a128) return StreamK<false, 0, 64, 128, 16, 4, 4, 4>::run(A, B, C, d, st);
+    // (BK = 32 with 3 stages measured 15% slower than BK = 16 with 4 stages)
     return StreamK<false, 0, 128, 128, 16, 4, 4, 4>::run(A, B, C, d, st);
   }
   else if constexpr (MODE == 0) return StreamK<true, 0, 64, 128, 8, 4, 4, 4>::run(A, B, C, d, st);
@@ -787,7 +789,7 @@ int contract_dense_device(const void* a, int dta, int ra, const int64_t* sa, con
   if (d.kA.n == 0) {
     d.kaff.ok = 0;  // K == 1: the single (partial) k-tile takes the table path
   } else if (d.kA.dim[d.kA.n - 1] % 16 == 0) {
-    d.kaff.ok = 1;
+    d.kaff.ok = (d.kA.dim[d.kA.n - 1] % 32 == 0) ? 2 : 1;  // k-tiles of 16 (or 32) stay affine
     d.kaff.ksA = d.kA.stride[d.kA.n - 1];
     d.kaff.ksB = d.kB.stride[d.kB.n - 1];
   }

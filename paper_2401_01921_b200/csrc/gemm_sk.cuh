@@ -255,7 +255,7 @@ struct SKCore {
         for (int kt = kt0; kt < kt1; ++kt, ++gi) {
           const int s = (int)(gi % STAGES);
           const int k0 = kt * BK;
-          if (d.kaff.ok && k0 + BK <= d.K) {
+          if (d.kaff.ok >= (BK + 15) / 16 && k0 + BK <= d.K) {
             const T* pa = A + group_offset(d.kA, k0);
             const T* pb = B + group_offset(d.kB, k0);
             if (gi >= STAGES) detail::mbar_wait(&empty[s], (uint32_t)(((gi / STAGES) & 1) ^ 1));
