@@ -651,56 +651,82 @@ def main():
             "clocks": clocks, "steps_ms": head["steps_ms"]}
     if not args.no_secondary:
         wl = {}
-        c3 = gpu_lawr(tnb, 1024, np.complex128, max(3, args.steps // 2), args.warmup, flush, dist, e2e=False)
-        wl["lawr_c128_chi1024"] = {"value": round(c3["gflops"], 2), "unit": "GFLOP/s (8 flop/complex MAC)",
-                                   "ms_per_step": c3["ms_per_step"], "roofline": c3["roofline"],
-                                   "complex_mode": tnb.get_complex_mode()}
-        c1 = gpu_lawr(tnb, 128, np.float64, max(10, args.steps), args.warmup, flush, dist, e2e=False, roof=False,
-                      graph=True)
-        wl["lawr_f64_chi128"] = {"value": round(c1["gflops"], 2), "unit": "GFLOP/s (eager Network.launch)",
-                                 "ms_per_step": c1["ms_per_step"], "graph_ms_per_step": c1["graph_ms_per_step"],
-                                 "gflops_graph": round(c1["gflops_graph"], 2)}
-        perm = gpu_permute(tnb, max(4, args.steps), args.warmup, flush, dist)
-        best = max(v["median_gbs"] for v in perm.values())
-        wl["permute_sweep"] = {"unit": "GB/s (2 x bytes / time, median over perms)", "cases": perm,
-                               "roofline": {"bound": "hbm", "peak": hbm_peak, "unit": "GB/s",
-                                            "peak_source": hbm_src,
-                                            "frac_median": {k: round(v["median_gbs"] / hbm_peak, 4)
-                                                            for k, v in perm.items()}}}
-        c4 = gpu_c4(tnb, max(10, args.steps), args.warmup, flush, dist)
-        wl["blocksparse_c4"] = {"value": round(c4["gflops"], 2), "unit": "GFLOP/s (graph replay; eager in gflops_eager)",
-                                **c4,
-                                "roofline": {"bound": "tensor", "achieved": round(c4["bs_gemm_kernel_tflops"], 3),
-                                             "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                                             "frac": round(c4["bs_gemm_kernel_tflops"] / FP64_PEAK_TFLOPS, 4),
-                                             "traffic": traffic_per_launch("bs_sk_kernel", np.float64),
-                                             "kernel": "bs_sk_kernel (grouped stream-K DMMA.8x8x4)",
-                                             "peak_source": PEAK_SOURCE}}
-        cb = gpu_c4_batch(tnb, 64, max(3, args.steps // 2), args.warmup, flush, dist)
-        wl["blocksparse_c4_batch64"] = {"value": round(cb["gflops"], 2), "unit": "GFLOP/s",
-                                        "scaling": "strong (64 contractions sharded over ranks)", **cb}
-        bt = gpu_lawr_batch(tnb, 64, 512, np.complex128, max(2, args.steps // 4), 1, flush, dist)
-        wl["lawr_batch64_c128_chi512"] = {"value": round(bt["gflops"], 2), "unit": "GFLOP/s (8 flop/complex MAC)",
-                                          "scaling": "strong (64 instances sharded over ranks)", **bt}
-        pe = gpu_peps(tnb, 32, 256, 8, 2, 1, 1, flush, dist)
-        wl["peps_chi256_D8"] = {"value": round(pe["gflops"], 2), "unit": "GFLOP/s",
-                                "scaling": "strong (32 sites sharded over ranks)", **pe}
-        sv = gpu_svd(tnb, 3, 1, flush, dist)
-        wl["svd_truncate_two_site_c4"] = {"value": round(sv["ms_per_call"], 3), "unit": "ms per call",
-                                          "higher_is_better": False, **sv}
-        ut = gpu_utn(tnb, 10, 2, dist)
-        wl["utn_load_c4"] = {"value": round(ut["gbs"], 3), "unit": "GB/s (payload / host wall)", **ut}
+
+        def w_c3():
+            c3 = gpu_lawr(tnb, 1024, np.complex128, max(3, args.steps // 2), args.warmup, flush, dist, e2e=False)
+            return {"value": round(c3["gflops"], 2), "unit": "GFLOP/s (8 flop/complex MAC)",
+                    "ms_per_step": c3["ms_per_step"], "roofline": c3["roofline"], "complex_mode": tnb.get_complex_mode()}
+
+        def w_c1():
+            c1 = gpu_lawr(tnb, 128, np.float64, max(10, args.steps), args.warmup, flush, dist, e2e=False, roof=False,
+                          graph=True)
+            return {"value": round(c1["gflops"], 2), "unit": "GFLOP/s (eager Network.launch)",
+                    "ms_per_step": c1["ms_per_step"], "graph_ms_per_step": c1["graph_ms_per_step"],
+                    "gflops_graph": round(c1["gflops_graph"], 2)}
+
+        def w_perm():
+            perm = gpu_permute(tnb, max(4, args.steps), args.warmup, flush, dist)
+            return {"unit": "GB/s (2 x bytes / time, median over perms)", "cases": perm,
+                    "roofline": {"bound": "hbm", "peak": hbm_peak, "unit": "GB/s", "peak_source": hbm_src,
+                                 "frac_median": {k: round(v["median_gbs"] / hbm_peak, 4) for k, v in perm.items()}}}
+
+        def w_c4():
+            c4 = gpu_c4(tnb, max(10, args.steps), args.warmup, flush, dist)
+            return {"value": round(c4["gflops"], 2), "unit": "GFLOP/s (graph replay; eager in gflops_eager)", **c4,
+                    "roofline": {"bound": "tensor", "achieved": round(c4["bs_gemm_kernel_tflops"], 3),
+                                 "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                 "frac": round(c4["bs_gemm_kernel_tflops"] / FP64_PEAK_TFLOPS, 4),
+                                 "traffic": traffic_per_launch("bs_sk_kernel", np.float64),
+                                 "kernel": "bs_sk_kernel (grouped stream-K DMMA.8x8x4)", "peak_source": PEAK_SOURCE}}
+
+        def w_c4b():
+            cb = gpu_c4_batch(tnb, 64, max(3, args.steps // 2), args.warmup, flush, dist)
+            return {"value": round(cb["gflops"], 2), "unit": "GFLOP/s",
+                    "scaling": "strong (64 contractions sharded over ranks)", **cb}
+
+        def w_c3b():
+            bt = gpu_lawr_batch(tnb, 64, 512, np.complex128, max(2, args.steps // 4), 1, flush, dist)
+            return {"value": round(bt["gflops"], 2), "unit": "GFLOP/s (8 flop/complex MAC)",
+                    "scaling": "strong (64 instances sharded over ranks)", **bt}
+
+        def w_peps():
+            pe = gpu_peps(tnb, 32, 256, 8, 2, 1, 1, flush, dist)
+            return {"value": round(pe["gflops"], 2), "unit": "GFLOP/s", "scaling": "strong (32 sites sharded over ranks)",
+                    **pe}
+
+        def w_svd():
+            sv = gpu_svd(tnb, 3, 1, flush, dist)
+            return {"value": round(sv["ms_per_call"], 3), "unit": "ms per call", "higher_is_better": False, **sv}
+
+        def w_utn():
+            ut = gpu_utn(tnb, 10, 2, dist)
+            return {"value": round(ut["gbs"], 3), "unit": "GB/s (payload / host wall)", **ut}
+
+        # each secondary workload is isolated: a failure is recorded, the headline line still prints
+        for name, fn in [("lawr_c128_chi1024", w_c3), ("lawr_f64_chi128", w_c1), ("permute_sweep", w_perm),
+                         ("blocksparse_c4", w_c4), ("blocksparse_c4_batch64", w_c4b),
+                         ("lawr_batch64_c128_chi512", w_c3b), ("peps_chi256_D8", w_peps),
+                         ("svd_truncate_two_site_c4", w_svd), ("utn_load_c4", w_utn)]:
+            try:
+                wl[name] = fn()
+            except Exception as e:  # noqa: BLE001
+                wl[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
         line["workloads"] = wl
     if dist.rank == 0 and not args.no_cpu:
         cb = cpu_lawr(1024, np.float64)
         line["cpu_baseline"] = cb
         if not args.no_secondary:
-            line["workloads"]["lawr_f64_chi128"]["cpu_baseline"] = cpu_lawr(128, np.float64, budget_s=2, max_iter=50)
-            line["workloads"]["permute_sweep"]["cpu_baseline"] = cpu_permute()
-            line["workloads"]["blocksparse_c4"]["cpu_baseline"] = cpu_c4()
-            line["workloads"]["svd_truncate_two_site_c4"]["cpu_baseline"] = cpu_svd()
-            u = line["workloads"]["utn_load_c4"]
-            line["workloads"]["utn_load_c4"]["cpu_baseline"] = cpu_utn(u["path"], u["payload_bytes"])
+            wl = line["workloads"]
+            cpu_legs = [("lawr_f64_chi128", lambda: cpu_lawr(128, np.float64, budget_s=2, max_iter=50)),
+                        ("permute_sweep", cpu_permute), ("blocksparse_c4", cpu_c4),
+                        ("svd_truncate_two_site_c4", cpu_svd),
+                        ("utn_load_c4", lambda: cpu_utn(wl["utn_load_c4"]["path"], wl["utn_load_c4"]["payload_bytes"]))]
+            for name, fn in cpu_legs:
+                if name in wl and "error" not in wl[name]:
+                    try:
+                        wl[name]["cpu_baseline"] = fn()
+                    except Exception as e:  # noqa: BLE001
+                        wl[name]["cpu_baseline"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if dist.rank == 0:
         print(json.dumps(line))
     return 0
