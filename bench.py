@@ -467,6 +467,36 @@ def gpu_svd(tnb, steps, warmup, flush, dist):
                     "a 16-CTA cluster per sector); matricise/scatter = tnb_copy2d_batched"}
 
 
+LANCZOS_ITERS = 30
+
+
+def gpu_lanczos(tnb, chi, dist):
+    """(f)1+(f)2 workload: Lanczos iterations on the Hermitian L.A.W.R effective Hamiltonian
+    at chi (ORACLE.hermitian_lawr_inputs), matvec = the compiled Network replayed as a CUDA
+    graph, Krylov basis + full reorthogonalisation in HBM. Fixed iteration count
+    (max_iter) so GPU and CPU time the same work: ms per Lanczos iteration."""
+    import torch
+    from paper_2401_01921_b200 import eig
+    inp = ORACLE.hermitian_lawr_inputs(chi, seed=7)
+    net, _ = lawr_network(tnb, inp)
+    op = eig.NetworkMatvec(net.compile(), "A")
+
+    def run():
+        try:
+            eig.lanczos(op, k=1, tol=1e-14, max_iter=LANCZOS_ITERS, seed=3)
+        except eig.ConvergenceError:
+            pass
+    run()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    run()
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3
+    return {"ms_per_iteration": ms / LANCZOS_ITERS, "iterations": LANCZOS_ITERS, "chi": chi,
+            "matvec": "Network.compile() graph replay (L.A.W.R, f64)"}
+
+
 def gpu_utn(tnb, steps, warmup, dist):
     """(f)4 workload: .utn load of the C4 MPS tensor A (6.1 MB payload) from the page cache
     into HBM (host wall: read + one H2D + one scatter launch, synchronised)."""
@@ -561,6 +591,27 @@ def cpu_utn(path, nbytes, budget_s=2.0):
     return {"value": nbytes / best / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
             "sample": f"{len(ts)} loads of the C4 A tensor into numpy (io.py:83-107 restated), best-of",
             "ms_per_load": best * 1e3}
+
+
+def cpu_lanczos(chi, iters=4):
+    """Oracle port of linalg.lanczos with the oracle's L.A.W.R launch as matvec (the
+    reference's DMRG inner loop on numpy/OpenBLAS), `iters` iterations."""
+    inp = ORACLE.hermitian_lawr_inputs(chi, seed=7)
+    shape = inp["A"].shape
+
+    def mv(v):
+        arrs = dict(inp)
+        arrs["A"] = v.reshape(shape)
+        out, _ = ORACLE.launch(ORACLE.lawr_slots(), "b, q, b2", arrs)
+        return np.ascontiguousarray(out).reshape(-1)
+    t0 = time.perf_counter()
+    try:
+        ORACLE.lanczos(mv, int(np.prod(shape)), k=1, tol=1e-14, max_iter=iters, seed=3)
+    except RuntimeError:
+        pass
+    dt = time.perf_counter() - t0
+    return {"value": dt / iters * 1e3, "unit": "ms per Lanczos iteration", "cores": cpu_threads(), "kind": "port",
+            "sample": f"{iters} iterations of the oracle's Lanczos (numpy L.A.W.R matvec, chi={chi})"}
 
 
 def cpu_c4(budget_s=3.0):
@@ -698,6 +749,11 @@ def main():
             sv = gpu_svd(tnb, 3, 1, flush, dist)
             return {"value": round(sv["ms_per_call"], 3), "unit": "ms per call", "higher_is_better": False, **sv}
 
+        def w_lanczos():
+            lz = gpu_lanczos(tnb, 1024, dist)
+            return {"value": round(lz["ms_per_iteration"], 4), "unit": "ms per Lanczos iteration",
+                    "higher_is_better": False, **lz}
+
         def w_utn():
             ut = gpu_utn(tnb, 10, 2, dist)
             return {"value": round(ut["gbs"], 3), "unit": "GB/s (payload / host wall)", **ut}
@@ -706,7 +762,8 @@ def main():
         for name, fn in [("lawr_c128_chi1024", w_c3), ("lawr_f64_chi128", w_c1), ("permute_sweep", w_perm),
                          ("blocksparse_c4", w_c4), ("blocksparse_c4_batch64", w_c4b),
                          ("lawr_batch64_c128_chi512", w_c3b), ("peps_chi256_D8", w_peps),
-                         ("svd_truncate_two_site_c4", w_svd), ("utn_load_c4", w_utn)]:
+                         ("svd_truncate_two_site_c4", w_svd), ("lanczos_lawr_chi1024", w_lanczos),
+                         ("utn_load_c4", w_utn)]:
             try:
                 wl[name] = fn()
             except Exception as e:  # noqa: BLE001
@@ -719,7 +776,7 @@ def main():
             wl = line["workloads"]
             cpu_legs = [("lawr_f64_chi128", lambda: cpu_lawr(128, np.float64, budget_s=2, max_iter=50)),
                         ("permute_sweep", cpu_permute), ("blocksparse_c4", cpu_c4),
-                        ("svd_truncate_two_site_c4", cpu_svd),
+                        ("svd_truncate_two_site_c4", cpu_svd), ("lanczos_lawr_chi1024", lambda: cpu_lanczos(1024)),
                         ("utn_load_c4", lambda: cpu_utn(wl["utn_load_c4"]["path"], wl["utn_load_c4"]["payload_bytes"]))]
             for name, fn in cpu_legs:
                 if name in wl and "error" not in wl[name]:

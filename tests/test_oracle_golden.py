@@ -188,3 +188,21 @@ def test_oracle_svd_truncate_matches_reference_goldens():
             want = z[f"{name}_t{k}_err"]
             got = np.array(disc) if disc else np.zeros(1)
             assert np.allclose(got, want, rtol=0, atol=1e-12 * max(1.0, smax))
+
+
+def test_oracle_lanczos_matches_reference():
+    """The oracle's Lanczos restatement reproduces the reference's Ritz values on the
+    Hermitian L.A.W.R operator (tests/golden/lanczos.npz, oracle/make_golden_lanczos.py)."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "lanczos.npz"))
+    inp = {k[3:]: z[k] for k in z.files if k.startswith("in_")}
+    shape = inp["A"].shape
+
+    def mv(v):
+        arrs = dict(inp)
+        arrs["A"] = v.reshape(shape)
+        out, _ = oracle.launch(oracle.lawr_slots(), "b, q, b2", arrs)
+        return np.ascontiguousarray(out).reshape(-1)
+    for seed in (3, 11):
+        theta, _, _ = oracle.lanczos(mv, int(np.prod(shape)), k=2, tol=1e-12, seed=seed)
+        assert np.allclose(theta, z[f"theta_seed{seed}"], rtol=0, atol=1e-12)
