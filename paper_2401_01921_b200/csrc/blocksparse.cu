@@ -283,7 +283,8 @@ __global__ void __launch_bounds__(1024) bs_pair_kernel(const BsMeta m) {
 template <bool CPLX, int MODE>
 struct BsCfg {
   // 64x64 tiles suit the sector sizes; at this tile size the gather rate, not the DMMA
-  // rate, is the limit, so two producer warpgroups feed the 16 math warps
+  // rate, is the limit, so two producer warpgroups feed the 16 math warps (measured: 4 math
+  // warps of 32x32 tiles, 1 or 2 CTAs per SM, were 15% slower)
   static constexpr int BM = 64, BN = 64, BK = CPLX ? 8 : 16, WM = 4, WN = 4, STAGES = 8, NPROD = 256;
   using Core = SKCore<CPLX, MODE, BM, BN, BK, WM, WN, STAGES, NPROD>;
 };
@@ -674,33 +675,29 @@ struct PlanCache {
 };
 PlanCache g_cache;
 
+constexpr int kMaxBsCtas = 2048;  // flags region: one int per persistent CTA
+constexpr size_t kBsPartialOff = 16384;
+
 template <bool CPLX, int MODE, bool AMF, bool BNF>
-int launch_bs_one(const BsMeta& meta, const PtrTable* pt, const BsSK& sk, int G, cudaStream_t st) {
+int launch_bs_one(const BsMeta& meta, const PtrTable* pt, BsSK sk, bool capturing, cudaStream_t st) {
   using Core = typename BsCfg<CPLX, MODE>::Core;
   auto kern = bs_sk_kernel<CPLX, MODE, AMF, BNF>;
   const size_t smem = al16(Core::kSmem) + (size_t)meta.sched_smem;
   static size_t configured = 0;
+  static size_t occ_smem = 0;
+  static int occ = 0;
   if (configured < smem) {
     TNB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = smem;
   }
-  {
-    KTimer kt(TNB_KF_BS_GEMM, st, 0.0);
-    kern<<<G, Core::NT, smem, st>>>(meta, *pt, sk);
+  if (occ_smem != smem) {  // persistent grid = every CTA slot: all co-resident (stream-K hand-offs)
+    TNB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Core::NT, smem));
+    occ_smem = smem;
   }
-  count_launch();
-  TNB_CUDA_CHECK(cudaGetLastError());
-  return TNB_OK;
-}
-
-// Caller holds g_cache.mu.
-template <bool CPLX, int MODE>
-int launch_bs(const Plan& plan, const BsMeta& meta, const PtrTable* pt, cudaStream_t st) {
-  using Core = typename BsCfg<CPLX, MODE>::Core;
-  if (meta.ntiles == 0) return TNB_OK;
-  const int G = sm_count();  // one persistent CTA per SM (all co-resident: stream-K hand-offs)
-  const size_t ws_need = (size_t)G * Core::ACCN * Core::NMATH * 8;
-  const size_t need = ws_need + (size_t)G * 4 + 64;
+  if (occ < 1) return fail(TNB_ECUDA, "bs_contract: grouped GEMM kernel does not fit on an SM");
+  const int G = std::min(sm_count() * occ, kMaxBsCtas);
+  // workspace: flags (self-resetting) at offset 0, register partials after kBsPartialOff
+  const size_t need = kBsPartialOff + (size_t)G * Core::ACCN * Core::NMATH * 8;
   if (g_cache.ws_bytes < need) {
     if (g_cache.ws) {
       TNB_CUDA_CHECK(cudaDeviceSynchronize());
@@ -708,34 +705,24 @@ int launch_bs(const Plan& plan, const BsMeta& meta, const PtrTable* pt, cudaStre
       g_cache.ws = nullptr;
       g_cache.ws_bytes = 0;
     }
-    // sized for the larger (complex) accumulator set so both dtypes share it
-    using CCore = typename BsCfg<true, 0>::Core;
-    const size_t want = std::max(need, (size_t)G * CCore::ACCN * CCore::NMATH * 8 + (size_t)G * 4 + 64);
-    TNB_CUDA_CHECK(cudaMalloc(&g_cache.ws, want));
-    TNB_CUDA_CHECK(cudaMemset(g_cache.ws, 0, want));
-    g_cache.ws_bytes = want;
+    TNB_CUDA_CHECK(cudaMalloc(&g_cache.ws, need));
+    TNB_CUDA_CHECK(cudaMemset(g_cache.ws, 0, need));
+    g_cache.ws_bytes = need;
   }
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  TNB_CUDA_CHECK(cudaStreamIsCapturing(st, &cs));
-  const bool capturing = cs != cudaStreamCaptureStatusNone;
-  if (!capturing && g_cache.ws_ev && g_cache.ws_stream != st) TNB_CUDA_CHECK(cudaStreamWaitEvent(st, g_cache.ws_ev, 0));
-  BsSK sk;
-  sk.ws = static_cast<double*>(g_cache.ws);
-  // flags live after the largest partial area (fixed offset for both dtypes)
-  using CCore = typename BsCfg<true, 0>::Core;
-  sk.flags = reinterpret_cast<int*>(static_cast<char*>(g_cache.ws) + (size_t)G * CCore::ACCN * CCore::NMATH * 8);
+  sk.flags = static_cast<int*>(g_cache.ws);
+  sk.ws = reinterpret_cast<double*>(static_cast<char*>(g_cache.ws) + kBsPartialOff);
   sk.trace = nullptr;
   static const char* trace_path = getenv("TNB_BS_TRACE");
   if (trace_path && !capturing) {
     TNB_CUDA_CHECK(cudaMallocAsync((void**)&sk.trace, (size_t)G * kTraceW * 8, st));
     TNB_CUDA_CHECK(cudaMemsetAsync(sk.trace, 0, (size_t)G * kTraceW * 8, st));
   }
-  int rc;
-  if (plan.amf && plan.bnf) rc = launch_bs_one<CPLX, MODE, true, true>(meta, pt, sk, G, st);
-  else if (plan.amf) rc = launch_bs_one<CPLX, MODE, true, false>(meta, pt, sk, G, st);
-  else if (plan.bnf) rc = launch_bs_one<CPLX, MODE, false, true>(meta, pt, sk, G, st);
-  else rc = launch_bs_one<CPLX, MODE, false, false>(meta, pt, sk, G, st);
-  if (rc) return rc;
+  {
+    KTimer kt(TNB_KF_BS_GEMM, st, 0.0);
+    kern<<<G, Core::NT, smem, st>>>(meta, *pt, sk);
+  }
+  count_launch();
+  TNB_CUDA_CHECK(cudaGetLastError());
   if (sk.trace) {
     std::vector<long long> h((size_t)G * kTraceW);
     TNB_CUDA_CHECK(cudaMemcpyAsync(h.data(), sk.trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
@@ -746,6 +733,24 @@ int launch_bs(const Plan& plan, const BsMeta& meta, const PtrTable* pt, cudaStre
       fclose(f);
     }
   }
+  return TNB_OK;
+}
+
+// Caller holds g_cache.mu.
+template <bool CPLX, int MODE>
+int launch_bs(const Plan& plan, const BsMeta& meta, const PtrTable* pt, cudaStream_t st) {
+  if (meta.ntiles == 0) return TNB_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  TNB_CUDA_CHECK(cudaStreamIsCapturing(st, &cs));
+  const bool capturing = cs != cudaStreamCaptureStatusNone;
+  if (!capturing && g_cache.ws_ev && g_cache.ws_stream != st) TNB_CUDA_CHECK(cudaStreamWaitEvent(st, g_cache.ws_ev, 0));
+  BsSK sk;
+  int rc;
+  if (plan.amf && plan.bnf) rc = launch_bs_one<CPLX, MODE, true, true>(meta, pt, sk, capturing, st);
+  else if (plan.amf) rc = launch_bs_one<CPLX, MODE, true, false>(meta, pt, sk, capturing, st);
+  else if (plan.bnf) rc = launch_bs_one<CPLX, MODE, false, true>(meta, pt, sk, capturing, st);
+  else rc = launch_bs_one<CPLX, MODE, false, false>(meta, pt, sk, capturing, st);
+  if (rc) return rc;
   if (!capturing) {
     if (!g_cache.ws_ev) TNB_CUDA_CHECK(cudaEventCreateWithFlags(&g_cache.ws_ev, cudaEventDisableTiming));
     TNB_CUDA_CHECK(cudaEventRecord(g_cache.ws_ev, st));
