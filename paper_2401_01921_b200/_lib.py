@@ -174,14 +174,22 @@ def permute(src_ptr, dst_ptr, elem_size, shape, perm, stream):
     check(lib().tnb_permute(src_ptr, dst_ptr, elem_size, len(shape), sp, pp, stream), "permute")
 
 
+_DENSE_ARGS = {}
+
+
 def contract_dense(a_ptr, a_dt, a_shape, a_perm, b_ptr, b_dt, b_shape, b_perm,
                    a_axes, b_axes, out_ptr, cplx_mode, stream):
-    sa, psa = _arr64(a_shape)
-    pa, ppa = _arr32(a_perm)
-    sb, psb = _arr64(b_shape)
-    pb, ppb = _arr32(b_perm)
-    xa, pxa = _arr32(a_axes)
-    xb, pxb = _arr32(b_axes)
+    # the integer descriptor arrays of a contraction shape are marshalled once and reused
+    # (a Network relaunched on same-shape operands re-marshals nothing)
+    key = (tuple(a_shape), tuple(a_perm), tuple(b_shape), tuple(b_perm), tuple(a_axes), tuple(b_axes))
+    args = _DENSE_ARGS.get(key)
+    if args is None:
+        arrs = [_arr64(a_shape), _arr32(a_perm), _arr64(b_shape), _arr32(b_perm), _arr32(a_axes), _arr32(b_axes)]
+        args = (arrs, [p for _, p in arrs])
+        if len(_DENSE_ARGS) >= 4096:
+            _DENSE_ARGS.clear()
+        _DENSE_ARGS[key] = args
+    psa, ppa, psb, ppb, pxa, pxb = args[1]
     check(lib().tnb_contract_dense(a_ptr, a_dt, len(a_shape), psa, ppa,
                                    b_ptr, b_dt, len(b_shape), psb, ppb,
                                    len(a_axes), pxa, pxb, out_ptr, cplx_mode, stream),
