@@ -126,7 +126,8 @@ typedef struct {
 int tnb_copy2d_batched(const void* src, void* dst, int64_t nseg, const TnbCopy2D* segs, void* stream);
 
 /* ---- batched one-sided Jacobi SVD of sector matrices (linalg.py:246-341) ---
- * Each sector: A (m x n, 1 <= m <= n, row-major float64) in `a` (read only),
+ * Each sector: A (m x n, 1 <= m <= n, row-major, dtype TNB_F64 or TNB_C128; s is
+ * float64 either way) in `a` (read only),
  * workspaces b (m x n) and q (m x m); outputs the thin factors in torch/LAPACK layout
  * u (m x m row-major), s (m, descending), vh (m x n row-major) and *status:
  * sweeps used (> 0), -1 not converged within max_sweeps, -2 rank deficient
@@ -139,7 +140,7 @@ typedef struct {
   int32_t* status;
   int64_t m, n;
 } TnbSvdSector;
-int tnb_svd_jacobi_batched(int nsec, const TnbSvdSector* secs, int max_sweeps, double tol,
+int tnb_svd_jacobi_batched(int dtype, int nsec, const TnbSvdSector* secs, int max_sweeps, double tol,
                            double rank_tol, void* stream);
 
 /* ---- a3: zero-flux block enumeration (unitensor.py:31-45), host only ------

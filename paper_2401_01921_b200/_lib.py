@@ -81,8 +81,8 @@ def _declare(lib):
         "tnb_bs_execute": ([_i64, _p, _p, _p, _p], ctypes.c_int),
         "tnb_bs_plan_pairs": ([_i64, _i64, _pi32, _pi64, _p], ctypes.c_int),
         "tnb_copy2d_batched": ([_p, _p, _i64, _p, _p], ctypes.c_int),
-        "tnb_svd_jacobi_batched": ([ctypes.c_int, _p, ctypes.c_int, ctypes.c_double, ctypes.c_double, _p],
-                                   ctypes.c_int),
+        "tnb_svd_jacobi_batched": ([ctypes.c_int, ctypes.c_int, _p, ctypes.c_int, ctypes.c_double,
+                                    ctypes.c_double, _p], ctypes.c_int),
         "tnb_optimal_order": ([ctypes.c_int, ctypes.c_char_p, _pi32, _pi32, _pi64,
                                ctypes.c_char_p, _i64, ctypes.c_char_p], ctypes.c_int),
     }
@@ -329,10 +329,10 @@ SVD_SECTOR_DTYPE = np.dtype([("a", "<u8"), ("b", "<u8"), ("q", "<u8"), ("u", "<u
                              ("status", "<u8"), ("m", "<i8"), ("n", "<i8")])  # TnbSvdSector
 
 
-def svd_jacobi_batched(sectors, stream, max_sweeps=30, tol=2.0, rank_tol=1e-13):
+def svd_jacobi_batched(sectors, stream, max_sweeps=30, tol=2.0, rank_tol=1e-13, dtype=TNB_F64):
     """One launch of tnb_svd_jacobi_batched over a SVD_SECTOR_DTYPE structured array."""
     secs = np.ascontiguousarray(sectors, dtype=SVD_SECTOR_DTYPE)
-    check(lib().tnb_svd_jacobi_batched(len(secs), secs.ctypes.data_as(_p) if len(secs) else None,
+    check(lib().tnb_svd_jacobi_batched(int(dtype), len(secs), secs.ctypes.data_as(_p) if len(secs) else None,
                                        int(max_sweeps), float(tol), float(rank_tol), stream),
           "svd_jacobi_batched")
 

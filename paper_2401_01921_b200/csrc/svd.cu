@@ -2,10 +2,12 @@
 // (the factorisation step of linalg.svd / svd_truncate, pkg/src/tnkit/linalg.py:246-341,
 // where the reference calls LAPACK gesdd sector by sector).
 //
-// Every sector matrix A (m x n, m <= n, row-major, float64) is factorised by
+// Every sector matrix A (m x n, m <= n, row-major, float64 or complex128) is factorised by
 // Hestenes' one-sided Jacobi on its ROWS -- rows are contiguous, so every access is a
 // coalesced row sweep:  B = Q A with Q orthogonal (product of plane rotations) and the
-// rows of B mutually orthogonal; then sigma_i = |b_i|, v_i = b_i / sigma_i, U = Q^T.
+// rows of B mutually orthogonal; then sigma_i = |b_i|, v_i = b_i / sigma_i, U = Q^H
+// (complex pairs: the phase of <b_p, b_q> is rotated out of b_q first, then the real
+// rotation applies).
 // Rows are paired by a round-robin tournament (m/2 disjoint pairs per round, m-1
 // rounds per sweep) and sweeps repeat until a whole sweep performs no rotation
 // (|b_p . b_q| <= tol |b_p| |b_q| for every pair) or max_sweeps is hit.
@@ -29,15 +31,14 @@ namespace {
 
 constexpr int kCluster = 16;  // non-portable cluster size (B200 allows 16)
 constexpr int kWarps = 16;
-constexpr int kRegPL = 20;    // rows up to 640 long are held in registers (20 per lane)
 
 struct SvdTask {
-  const double* a; // [m][n] in (read only)
-  double* b;       // [m][n] workspace: the rotated rows
-  double* q;       // [m][m] workspace: accumulated rotations (rows)
-  double* u;       // [m][m] out
-  double* s;       // [m] out
-  double* vh;      // [m][n] out
+  const void* a;   // [m][n] in (read only)
+  void* b;         // [m][n] workspace: the rotated rows
+  void* q;         // [m][m] workspace: accumulated rotations (rows)
+  void* u;         // [m][m] out
+  double* s;       // [m] out (real)
+  void* vh;        // [m][n] out
   int* status;     // [1] out: sweeps used (>0), -1 not converged, -2 rank deficient
   int* counter;    // [2] rotation counters (zero on entry)
   double* norm;    // [m] scratch: |b_i|
@@ -71,20 +72,92 @@ __device__ __forceinline__ void rr_pair(int P, int r, int i, int& a, int& b) {
   }
 }
 
+// ---- scalar helpers: real (double) and complex (double2) rows -----------------------
+template <bool CPLX>
+struct Sc;
+template <>
+struct Sc<false> {
+  using T = double;
+  static constexpr int kRegPL = 20;  // rows up to 640 long live in registers (20 per lane)
+  __device__ static T zero() { return 0.0; }
+  __device__ static T one() { return 1.0; }
+  __device__ static double abs2(T x) { return x * x; }
+  __device__ static void acc2(double& acc, T x) { acc = fma(x, x, acc); }
+  // acc += conj(x) * y  (split into re / im accumulators)
+  __device__ static void dot(double& re, double& im, T x, T y) { re = fma(x, y, re); }
+  __device__ static T conj(T x) { return x; }
+  __device__ static T scale(double c, T x) { return c * x; }
+  // phase p (unit; +-1 for real rows) times y
+  __device__ static T mulph(double pr, double pi, T y) { return pr * y; }
+  __device__ static T lin(double c, T x, double s, T y) { return c * x + s * y; }  // c x + s y
+};
+template <>
+struct Sc<true> {
+  using T = double2;
+  static constexpr int kRegPL = 10;
+  __device__ static T zero() { return make_double2(0.0, 0.0); }
+  __device__ static T one() { return make_double2(1.0, 0.0); }
+  __device__ static double abs2(T x) { return fma(x.x, x.x, x.y * x.y); }
+  __device__ static void acc2(double& acc, T x) { acc = fma(x.x, x.x, fma(x.y, x.y, acc)); }
+  __device__ static void dot(double& re, double& im, T x, T y) {
+    re = fma(x.x, y.x, fma(x.y, y.y, re));
+    im = fma(x.x, y.y, fma(-x.y, y.x, im));
+  }
+  __device__ static T conj(T x) { return make_double2(x.x, -x.y); }
+  __device__ static T scale(double c, T x) { return make_double2(c * x.x, c * x.y); }
+  __device__ static T mulph(double pr, double pi, T y) {
+    return make_double2(fma(pr, y.x, -pi * y.y), fma(pr, y.y, pi * y.x));
+  }
+  __device__ static T lin(double c, T x, double s, T y) {
+    return make_double2(fma(c, x.x, s * y.x), fma(c, x.y, s * y.y));
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ T ldcg(const T* p) {
+  return __ldcg(p);
+}
+template <typename T>
+__device__ __forceinline__ void stcg(T* p, T v) {
+  __stcg(p, v);
+}
+
+// One plane rotation of rows (a, b) of B and Q, given al = |b_a|^2, be = |b_b|^2 and
+// g = <b_a, b_b> = |g| e^{i phi}: with b' = e^{-i phi} b_b the real Hestenes rotation on
+// (b_a, b') makes them orthogonal; Q rows take the same unitary 2 x 2 map.
+// Returns false if the pair is already orthogonal to the threshold.
+__device__ __forceinline__ bool rotation(double al, double be, double gre, double gim, double thresh, double& c,
+                                         double& s, double& pr, double& pi) {
+  const double ga = sqrt(gre * gre + gim * gim);
+  if (!(ga > thresh * sqrt(al * be)) || al == 0.0 || be == 0.0) return false;
+  pr = gre / ga;  // e^{-i phi} = conj(g) / |g|
+  pi = -gim / ga;
+  const double zeta = (be - al) / (2.0 * ga);
+  const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+  c = 1.0 / sqrt(1.0 + tt * tt);
+  s = c * tt;
+  return true;
+}
+
+template <bool CPLX>
 __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32)
     jacobi_rows_kernel(const SvdTask* __restrict__ tasks, int max_sweeps, double tol, double rank_tol) {
+  using S = Sc<CPLX>;
+  using T = typename S::T;
+  constexpr int RPL = S::kRegPL;
   const SvdTask t = tasks[blockIdx.x / kCluster];
   const int crank = (int)cluster_rank();
   const int lane = threadIdx.x & 31;
   const int gw = crank * kWarps + (threadIdx.x >> 5);  // warp index within the cluster
   constexpr int NW = kCluster * kWarps;
   const int m = t.m, n = t.n;
-  double* __restrict__ B = t.b;
-  double* __restrict__ Q = t.q;
+  T* __restrict__ B = static_cast<T*>(t.b);
+  T* __restrict__ Q = static_cast<T*>(t.q);
+  const T* __restrict__ Ain = static_cast<const T*>(t.a);
   // Q = I, B = A
   for (int64_t x = (int64_t)gw * 32 + lane; x < (int64_t)m * m; x += (int64_t)NW * 32)
-    __stcg(Q + x, (x / m == x % m) ? 1.0 : 0.0);
-  for (int64_t x = (int64_t)gw * 32 + lane; x < (int64_t)m * n; x += (int64_t)NW * 32) __stcg(B + x, t.a[x]);
+    stcg(Q + x, (x / m == x % m) ? S::one() : S::zero());
+  for (int64_t x = (int64_t)gw * 32 + lane; x < (int64_t)m * n; x += (int64_t)NW * 32) stcg(B + x, Ain[x]);
   cluster_sync_all();
   const int P = m + (m & 1);  // an odd row count gets a virtual zero row (its pairs are skipped)
   // rotation threshold on |cos(b_p, b_q)|: tol x the rounding level of a length-n dot product
@@ -104,79 +177,78 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32)
             a = b;
             b = x;
           }
-          double* ra = B + (int64_t)a * n;
-          double* rb = B + (int64_t)b * n;
-          double* qa = Q + (int64_t)a * m;
-          double* qb = Q + (int64_t)b * m;
-          if (n <= 32 * kRegPL) {
+          T* ra = B + (int64_t)a * n;
+          T* rb = B + (int64_t)b * n;
+          T* qa = Q + (int64_t)a * m;
+          T* qb = Q + (int64_t)b * m;
+          double c, s, pr, pi;
+          if (n <= 32 * RPL && m <= 32 * RPL) {
             // rows held in registers: one L2 round trip for B's rows, one for Q's
-            double x[kRegPL], y[kRegPL];
-            double al = 0.0, be = 0.0, ga = 0.0;
+            T x[RPL], y[RPL];
+            double al = 0.0, be = 0.0, gre = 0.0, gim = 0.0;
 #pragma unroll
-            for (int u = 0; u < kRegPL; ++u) {
+            for (int u = 0; u < RPL; ++u) {
               const int j = lane + 32 * u;
-              x[u] = j < n ? __ldcg(ra + j) : 0.0;
-              y[u] = j < n ? __ldcg(rb + j) : 0.0;
+              x[u] = j < n ? ldcg(ra + j) : S::zero();
+              y[u] = j < n ? ldcg(rb + j) : S::zero();
             }
 #pragma unroll
-            for (int u = 0; u < kRegPL; ++u) {
-              al = fma(x[u], x[u], al);
-              be = fma(y[u], y[u], be);
-              ga = fma(x[u], y[u], ga);
+            for (int u = 0; u < RPL; ++u) {
+              S::acc2(al, x[u]);
+              S::acc2(be, y[u]);
+              S::dot(gre, gim, x[u], y[u]);
             }
             al = warp_sum(al);
             be = warp_sum(be);
-            ga = warp_sum(ga);
-            if (!(fabs(ga) > thresh * sqrt(al * be)) || al == 0.0 || be == 0.0) continue;
-            const double zeta = (be - al) / (2.0 * ga);
-            const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
+            gre = warp_sum(gre);
+            if constexpr (CPLX) gim = warp_sum(gim);
+            if (!rotation(al, be, gre, gim, thresh, c, s, pr, pi)) continue;
 #pragma unroll
-            for (int u = 0; u < kRegPL; ++u) {
+            for (int u = 0; u < RPL; ++u) {
               const int j = lane + 32 * u;
               if (j < n) {
-                __stcg(ra + j, c * x[u] - s * y[u]);
-                __stcg(rb + j, s * x[u] + c * y[u]);
+                const T yp = S::mulph(pr, pi, y[u]);
+                stcg(ra + j, S::lin(c, x[u], -s, yp));
+                stcg(rb + j, S::lin(s, x[u], c, yp));
               }
             }
 #pragma unroll
-            for (int u = 0; u < kRegPL; ++u) {
+            for (int u = 0; u < RPL; ++u) {
               const int j = lane + 32 * u;
-              x[u] = j < m ? __ldcg(qa + j) : 0.0;
-              y[u] = j < m ? __ldcg(qb + j) : 0.0;
+              x[u] = j < m ? ldcg(qa + j) : S::zero();
+              y[u] = j < m ? ldcg(qb + j) : S::zero();
             }
 #pragma unroll
-            for (int u = 0; u < kRegPL; ++u) {
+            for (int u = 0; u < RPL; ++u) {
               const int j = lane + 32 * u;
               if (j < m) {
-                __stcg(qa + j, c * x[u] - s * y[u]);
-                __stcg(qb + j, s * x[u] + c * y[u]);
+                const T yp = S::mulph(pr, pi, y[u]);
+                stcg(qa + j, S::lin(c, x[u], -s, yp));
+                stcg(qb + j, S::lin(s, x[u], c, yp));
               }
             }
           } else {
-            double al = 0.0, be = 0.0, ga = 0.0;
+            double al = 0.0, be = 0.0, gre = 0.0, gim = 0.0;
             for (int j = lane; j < n; j += 32) {
-              const double x = __ldcg(ra + j), y = __ldcg(rb + j);
-              al = fma(x, x, al);
-              be = fma(y, y, be);
-              ga = fma(x, y, ga);
+              const T x = ldcg(ra + j), y = ldcg(rb + j);
+              S::acc2(al, x);
+              S::acc2(be, y);
+              S::dot(gre, gim, x, y);
             }
             al = warp_sum(al);
             be = warp_sum(be);
-            ga = warp_sum(ga);
-            if (!(fabs(ga) > thresh * sqrt(al * be)) || al == 0.0 || be == 0.0) continue;
-            const double zeta = (be - al) / (2.0 * ga);
-            const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
+            gre = warp_sum(gre);
+            if constexpr (CPLX) gim = warp_sum(gim);
+            if (!rotation(al, be, gre, gim, thresh, c, s, pr, pi)) continue;
             for (int j = lane; j < n; j += 32) {
-              const double x = __ldcg(ra + j), y = __ldcg(rb + j);
-              __stcg(ra + j, c * x - s * y);
-              __stcg(rb + j, s * x + c * y);
+              const T x = ldcg(ra + j), yp = S::mulph(pr, pi, ldcg(rb + j));
+              stcg(ra + j, S::lin(c, x, -s, yp));
+              stcg(rb + j, S::lin(s, x, c, yp));
             }
             for (int j = lane; j < m; j += 32) {
-              const double x = __ldcg(qa + j), y = __ldcg(qb + j);
-              __stcg(qa + j, c * x - s * y);
-              __stcg(qb + j, s * x + c * y);
+              const T x = ldcg(qa + j), yp = S::mulph(pr, pi, ldcg(qb + j));
+              stcg(qa + j, S::lin(c, x, -s, yp));
+              stcg(qb + j, S::lin(s, x, c, yp));
             }
           }
           ++nrot;  // (warp-uniform)
@@ -199,13 +271,12 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32)
     status = 1;
   }
   cluster_sync_all();
-  // ---- finalize: sigma_i = |b_i| -> rank (descending, ties by row) -> U, S, Vh
+  // ---- finalize: sigma_i = |b_i| -> rank (descending, ties by row) -> U = Q^H, S, Vh = B / S
+  T* __restrict__ U = static_cast<T*>(t.u);
+  T* __restrict__ VH = static_cast<T*>(t.vh);
   for (int i = gw; i < m; i += NW) {
     double x2 = 0.0;
-    for (int j = lane; j < n; j += 32) {
-      const double x = __ldcg(B + (int64_t)i * n + j);
-      x2 = fma(x, x, x2);
-    }
+    for (int j = lane; j < n; j += 32) x2 += S::abs2(ldcg(B + (int64_t)i * n + j));
     x2 = warp_sum(x2);
     if (lane == 0) __stcg(t.norm + i, sqrt(x2));
   }
@@ -227,8 +298,8 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32)
     if (si <= rank_tol * smax) deficient = true;
     if (lane == 0) t.s[rank] = si;
     const double inv = si > 0.0 ? 1.0 / si : 0.0;
-    for (int j = lane; j < n; j += 32) t.vh[(int64_t)rank * n + j] = __ldcg(B + (int64_t)i * n + j) * inv;
-    for (int j = lane; j < m; j += 32) t.u[(int64_t)j * m + rank] = __ldcg(Q + (int64_t)i * m + j);
+    for (int j = lane; j < n; j += 32) VH[(int64_t)rank * n + j] = S::scale(inv, ldcg(B + (int64_t)i * n + j));
+    for (int j = lane; j < m; j += 32) U[(int64_t)j * m + rank] = S::conj(ldcg(Q + (int64_t)i * m + j));
   }
   if (deficient && lane == 0) atomicExch(t.status, -2);
   cluster_sync_all();
@@ -237,30 +308,48 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32)
   }
 }
 
+template <bool CPLX>
+int launch_jacobi(const void* tasks, int nsec, int max_sweeps, double tol, double rank_tol, double work,
+                  cudaStream_t st) {
+  auto kern = jacobi_rows_kernel<CPLX>;
+  static bool configured = false;
+  if (!configured) {
+    TNB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured = true;
+  }
+  {
+    KTimer kt(TNB_KF_OTHER, st, work);
+    kern<<<nsec * kCluster, kWarps * 32, 0, st>>>(static_cast<const SvdTask*>(tasks), max_sweeps, tol, rank_tol);
+  }
+  count_launch();
+  TNB_CUDA_CHECK(cudaGetLastError());
+  return TNB_OK;
+}
+
 }  // namespace
 }  // namespace tnb
 
-extern "C" int tnb_svd_jacobi_batched(int nsec, const TnbSvdSector* secs, int max_sweeps, double tol,
+extern "C" int tnb_svd_jacobi_batched(int dtype, int nsec, const TnbSvdSector* secs, int max_sweeps, double tol,
                                       double rank_tol, void* stream) {
   using namespace tnb;
   int rc = require_device();
   if (rc) return rc;
+  if (dtype != TNB_F64 && dtype != TNB_C128) return fail(TNB_EUNSUP, "svd_jacobi: float64 / complex128 only");
   if (nsec < 0 || (nsec > 0 && !secs) || max_sweeps < 1) return fail(TNB_EINVAL, "svd_jacobi: bad arguments");
   if (nsec == 0) return TNB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   std::vector<SvdTask> h(nsec);
+  int64_t msum = 0;
+  double work = 0.0;
   for (int i = 0; i < nsec; ++i) {
     const TnbSvdSector& x = secs[i];
     if (x.m < 1 || x.n < x.m || !x.a || !x.b || !x.q || !x.u || !x.s || !x.vh || !x.status)
       return fail(TNB_EINVAL, "svd_jacobi: sector needs 1 <= m <= n and all buffers");
-    h[i] = {static_cast<const double*>(x.a), static_cast<double*>(x.b), static_cast<double*>(x.q),
-            static_cast<double*>(x.u),
-            static_cast<double*>(x.s), static_cast<double*>(x.vh), x.status, nullptr, nullptr,
-            (int)x.m, (int)x.n};
+    h[i] = {x.a, x.b, x.q, x.u, static_cast<double*>(x.s), x.vh, x.status, nullptr, nullptr, (int)x.m, (int)x.n};
+    msum += x.m;
+    work += 2.0 * x.m * (double)x.m * x.n;
   }
-  // device task table + rotation counters + norm / rank scratch in one allocation
-  int64_t msum = 0;
-  for (int i = 0; i < nsec; ++i) msum += secs[i].m;
+  // device task table + rotation counters + norm scratch in one allocation
   const size_t tb = sizeof(SvdTask) * (size_t)nsec, cb = sizeof(int) * 2 * (size_t)nsec;
   const size_t nb = sizeof(double) * (size_t)msum;
   void* mem = nullptr;
@@ -274,23 +363,12 @@ extern "C" int tnb_svd_jacobi_batched(int nsec, const TnbSvdSector* secs, int ma
   cudaError_t e = cudaMemcpyAsync(mem, h.data(), tb, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(counters, 0, cb, st);
   for (int i = 0; e == cudaSuccess && i < nsec; ++i) e = cudaMemsetAsync(secs[i].status, 0, sizeof(int), st);
-  if (e == cudaSuccess) {
-    double work = 0.0;
-    for (int i = 0; i < nsec; ++i) work += 2.0 * secs[i].m * (double)secs[i].m * secs[i].n;
-    static bool configured = false;
-    if (!configured) {
-      e = cudaFuncSetAttribute(jacobi_rows_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      configured = e == cudaSuccess;
-    }
-    if (e == cudaSuccess) {
-      KTimer kt(TNB_KF_OTHER, st, work);
-      jacobi_rows_kernel<<<nsec * kCluster, kWarps * 32, 0, st>>>(static_cast<const SvdTask*>(mem), max_sweeps,
-                                                                    tol, rank_tol);
-      e = cudaGetLastError();
-    }
+  if (e != cudaSuccess) {
+    cudaFreeAsync(mem, st);
+    return cuda_fail(e, "svd_jacobi: task upload");
   }
-  count_launch();
+  rc = dtype == TNB_F64 ? launch_jacobi<false>(mem, nsec, max_sweeps, tol, rank_tol, work, st)
+                        : launch_jacobi<true>(mem, nsec, max_sweeps, tol, rank_tol, work, st);
   cudaFreeAsync(mem, st);
-  if (e != cudaSuccess) return cuda_fail(e, "svd_jacobi: launch");
-  return TNB_OK;
+  return rc;
 }

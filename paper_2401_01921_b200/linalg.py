@@ -16,11 +16,11 @@ Same contract as the reference (pkg/src/tnkit/linalg.py):
 
 B200 path: blocks -> sector matrices is ONE ``tnb_copy2d_batched`` launch into a
 sector slab laid out by matrix shape, so every group of equal-shape sectors is already a
-``[batch, m, n]`` array; all float64 sectors are factorised by ONE launch of the
-engine's batched one-sided Jacobi kernel (``tnb_svd_jacobi_batched``, csrc/svd.cu: a
-thread-block cluster per sector, all sectors concurrently); complex128 sectors and any
-sector the kernel flags (not converged / rank deficient) use the library factorisation
-(``torch.linalg.svd``, cuSOLVER). The factors U / S / Vdag are scattered into their block
+``[batch, m, n]`` array; all sectors (float64 or complex128) are factorised by ONE launch of
+the engine's batched one-sided Jacobi kernel (``tnb_svd_jacobi_batched``, csrc/svd.cu: a
+thread-block cluster per sector, all sectors concurrently); any sector the kernel flags
+(not converged / rank deficient) is refactorised by the library (``torch.linalg.svd``,
+cuSOLVER). The factors U / S / Vdag are scattered into their block
 slabs by one ``tnb_copy2d_batched`` launch each. Only the singular values (for the
 truncation ranking) and the per-group status words cross to the host.
 """
@@ -152,10 +152,10 @@ def _row_charge(row_bonds, row_qn, syms):
     return charge
 
 
-# float64 sector matrices go through the engine's batched Jacobi kernel
-# (tnb_svd_jacobi_batched: one thread-block cluster per sector, all sectors in one launch);
-# complex128, and any sector the kernel flags (not converged / rank deficient), through the
-# library factorisation. "library" forces the latter for everything.
+# sector matrices go through the engine's batched Jacobi kernel (tnb_svd_jacobi_batched: one
+# thread-block cluster per sector, all sectors in one launch); any sector the kernel flags
+# (not converged / rank deficient) through the library factorisation. "library" forces the
+# latter for everything.
 SVD_BACKEND = "jacobi"
 
 
@@ -178,34 +178,38 @@ def _transpose(batch):
 
 def _factorise(mz):
     """Thin SVD of every shape group: (U [b,m,k], S [b,k], Vh [b,k,n]) device tensors."""
-    if mz.dt != dense.Float64 or SVD_BACKEND != "jacobi":
+    if SVD_BACKEND != "jacobi":
         return [_library_svd(g[4]) for g in mz.groups]
+    tdt = dense._TORCH[mz.dt]
+    es = mz.dt.itemsize
     jobs, recs = [], []
     for gi, (m, n, members, off, view) in enumerate(mz.groups):
         tall = m > n
         a = _transpose(view) if tall else view  # rows to orthogonalise: the shorter side
         b, r, c = a.shape
         dev = a.device
-        u = torch.empty((b, r, r), dtype=torch.float64, device=dev)
+        u = torch.empty((b, r, r), dtype=tdt, device=dev)
         sv = torch.empty((b, r), dtype=torch.float64, device=dev)
-        vh = torch.empty((b, r, c), dtype=torch.float64, device=dev)
-        q = torch.empty((b, r, r), dtype=torch.float64, device=dev)
-        w = torch.empty((b, r, c), dtype=torch.float64, device=dev)  # rotated rows (a stays intact)
+        vh = torch.empty((b, r, c), dtype=tdt, device=dev)
+        q = torch.empty((b, r, r), dtype=tdt, device=dev)
+        w = torch.empty((b, r, c), dtype=tdt, device=dev)  # rotated rows (a stays intact)
         st = torch.zeros(b, dtype=torch.int32, device=dev)
-        es = 8
         for k in range(b):
             jobs.append((a.data_ptr() + k * r * c * es, w.data_ptr() + k * r * c * es, q.data_ptr() + k * r * r * es,
-                         u.data_ptr() + k * r * r * es, sv.data_ptr() + k * r * es, vh.data_ptr() + k * r * c * es,
+                         u.data_ptr() + k * r * r * es, sv.data_ptr() + k * r * 8, vh.data_ptr() + k * r * c * es,
                          st.data_ptr() + 4 * k, r, c))
         recs.append((tall, u, sv, vh, q, st, (a, w)))
-    _lib.svd_jacobi_batched(np.array(jobs, dtype=_lib.SVD_SECTOR_DTYPE), dense.stream_handle())
+    _lib.svd_jacobi_batched(np.array(jobs, dtype=_lib.SVD_SECTOR_DTYPE), dense.stream_handle(),
+                            dtype=dense.dtype_code(mz.dt))
     out = []
     for (m, n, members, off, view), (tall, u, sv, vh, q, st, a) in zip(mz.groups, recs):
         if bool((st <= 0).any()):  # (one small device->host read per group)
             out.append(_library_svd(view))
             continue
-        if tall:  # A^T = U' S V'^T  ->  A = V' S U'^T
+        if tall:  # A^T = U' S V'^H  ->  A = conj(V') S U'^T: U = conj(Vh')^T, Vh = conj(U')^T
             u, vh = _transpose(vh), _transpose(u)
+            if mz.dt == dense.Complex128:
+                u, vh = u.conj_physical_(), vh.conj_physical_()
         out.append((u, sv, vh))
     return out
 
