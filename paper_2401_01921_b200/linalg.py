@@ -199,6 +199,9 @@ def _factorise(mz):
                          u.data_ptr() + k * r * r * es, sv.data_ptr() + k * r * 8, vh.data_ptr() + k * r * c * es,
                          st.data_ptr() + 4 * k, r, c))
         recs.append((tall, u, sv, vh, q, st, (a, w)))
+    # largest sectors first: clusters are scheduled in task order and only ~9 16-CTA clusters
+    # are resident at once, so the critical (largest) sector must not wait behind small ones
+    jobs.sort(key=lambda j: -(j[7] * j[7] * j[8]))
     _lib.svd_jacobi_batched(np.array(jobs, dtype=_lib.SVD_SECTOR_DTYPE), dense.stream_handle(),
                             dtype=dense.dtype_code(mz.dt))
     out = []
