@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
     constexpr int RA = AMF ? 1 : 4, RB = BNF ? 1 : 4;
     const uint32_t sAbase = smem_u32(As), sBbase = smem_u32(Bs);
     constexpr uint32_t stA = BK * LDA * ES, stB = BK * LDB * ES;
-    int64_t gi = 0;
+    uint32_t gi = 0;  // stage counter (per CTA < 2^32)
     for (int64_t e = it1; e > it0;) {
       const int t = tile_of(e - 1);
       const int64_t tstart = kbeg[t];
@@ -464,58 +464,79 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
           mapB(jj, nn, kk);
           rB[jj] = colOffB[nn];
         }
-        // this thread's gather sources for the whole pair (nullptr = padding row/col);
-        // per k-tile only the k offset moves
-        const T* pA[EA];
-        const T* pB[EB];
+        // this thread's gathers for the whole pair: 32-bit element offsets from the block base
+        // (-1 = padding row/col) and shared-memory byte offsets within a stage; per k-tile only
+        // the k offset moves
+        int32_t oA[EA], oB[EB];
+        uint32_t dA[EA], dB[EB];
 #pragma unroll
         for (int x = 0; x < EA; ++x) {
           int mm, kk;
           mapA(x, mm, kk);
           const int64_t ro = rA[x % RA];
-          pA[x] = ro >= 0 ? A + (ro + (int64_t)kk * ksA) : nullptr;
+          oA[x] = ro >= 0 ? (int32_t)(ro + (int64_t)kk * ksA) : -1;
+          dA[x] = (uint32_t)(kk * LDA + mm) * ES;
         }
 #pragma unroll
         for (int x = 0; x < EB; ++x) {
           int nn, kk;
           mapB(x, nn, kk);
           const int64_t co = rB[x % RB];
-          pB[x] = co >= 0 ? B + (co + (int64_t)kk * ksB) : nullptr;
+          oB[x] = co >= 0 ? (int32_t)(co + (int64_t)kk * ksB) : -1;
+          dB[x] = (uint32_t)(kk * LDB + nn) * ES;
         }
         const int64_t lend = (kend - pbase) < nkt ? (kend - pbase) : nkt;
         for (int64_t lk = kt - pbase; lk < lend; ++lk, ++gi) {
           const int s = (int)(gi % STAGES);
           const int k0 = (int)lk * BK;
           if (aff) {
-            // per-element base addresses are fixed for the whole pair; only the k offset moves
-            const int64_t koA = nA == 0 ? 0 : (nA == 1 ? (int64_t)k0 * ksA : group_offset(da.k_g, k0));
-            const int64_t koB = nB == 0 ? 0 : (nB == 1 ? (int64_t)k0 * ksB : group_offset(db.k_g, k0));
-            const int krem = Kp - k0;  // >= BK: whole k-tile
-            if (gi >= STAGES) detail::mbar_wait(&empty[s], (uint32_t)(((gi / STAGES) & 1) ^ 1));
+            const int32_t koA = nA == 0 ? 0 : (nA == 1 ? k0 * (int32_t)ksA : (int32_t)group_offset(da.k_g, k0));
+            const int32_t koB = nB == 0 ? 0 : (nB == 1 ? k0 * (int32_t)ksB : (int32_t)group_offset(db.k_g, k0));
+            const int krem = Kp - k0;
+            if (gi >= STAGES) detail::mbar_wait(&empty[s], ((gi / STAGES) & 1) ^ 1);
             const uint32_t sa = sAbase + s * stA, sbb = sBbase + s * stB;
+            if (krem >= BK) {  // whole k-tile: validity = padding row/col only
 #pragma unroll
-            for (int x = 0; x < EA; ++x) {
-              int mm, kk;
-              mapA(x, mm, kk);
-              const bool v = pA[x] != nullptr && kk < krem;
-              const T* src = v ? pA[x] + koA : A;
-              const uint32_t dst = sa + (uint32_t)(kk * LDA + mm) * ES;
-              if constexpr (CPLX)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
-              else
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0));
-            }
+              for (int x = 0; x < EA; ++x) {
+                const bool v = oA[x] >= 0;
+                const T* src = A + (v ? oA[x] + koA : 0);
+                if constexpr (CPLX)
+                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa + dA[x]), "l"(src), "r"(v ? 16 : 0));
+                else
+                  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa + dA[x]), "l"(src), "r"(v ? 8 : 0));
+              }
 #pragma unroll
-            for (int x = 0; x < EB; ++x) {
-              int nn, kk;
-              mapB(x, nn, kk);
-              const bool v = pB[x] != nullptr && kk < krem;
-              const T* src = v ? pB[x] + koB : B;
-              const uint32_t dst = sbb + (uint32_t)(kk * LDB + nn) * ES;
-              if constexpr (CPLX)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
-              else
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0));
+              for (int x = 0; x < EB; ++x) {
+                const bool v = oB[x] >= 0;
+                const T* src = B + (v ? oB[x] + koB : 0);
+                if constexpr (CPLX)
+                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sbb + dB[x]), "l"(src), "r"(v ? 16 : 0));
+                else
+                  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sbb + dB[x]), "l"(src), "r"(v ? 8 : 0));
+              }
+            } else {  // ragged last k-tile of the pair
+#pragma unroll
+              for (int x = 0; x < EA; ++x) {
+                int mm, kk;
+                mapA(x, mm, kk);
+                const bool v = oA[x] >= 0 && kk < krem;
+                const T* src = A + (v ? oA[x] + koA : 0);
+                if constexpr (CPLX)
+                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa + dA[x]), "l"(src), "r"(v ? 16 : 0));
+                else
+                  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa + dA[x]), "l"(src), "r"(v ? 8 : 0));
+              }
+#pragma unroll
+              for (int x = 0; x < EB; ++x) {
+                int nn, kk;
+                mapB(x, nn, kk);
+                const bool v = oB[x] >= 0 && kk < krem;
+                const T* src = B + (v ? oB[x] + koB : 0);
+                if constexpr (CPLX)
+                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sbb + dB[x]), "l"(src), "r"(v ? 16 : 0));
+                else
+                  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sbb + dB[x]), "l"(src), "r"(v ? 8 : 0));
+              }
             }
             detail::cp_async_mbar_arrive_noinc(&full[s]);
             continue;
@@ -579,7 +600,7 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
     const int M = oM[tr.o], N = oN[tr.o];
     Base::store(static_cast<T*>(const_cast<void*>(ptrs[m.na + m.nb + tr.o])), N, tr.m0, tr.n0, M, N, acc);
   }
-  int64_t gi = 0;
+  uint32_t gi = 0;
   long long* tr_ = (sk.trace && tid == 0) ? sk.trace + (size_t)c * kTraceW : nullptr;
   int nseg = 0;
   if (tr_) tr_[0] = gtimer();
@@ -865,7 +886,7 @@ int bs_plan_locked(int dtype, int na, int nb, int nout, int rank_a, int rank_b, 
         kk.push_back({shp[p], ss[p]});
         K *= shp[p];
       }
-      if (F >= (1ll << 31) || K >= (1ll << 31)) return false;
+      if (F * K >= (1ll << 31)) return false;  // 32-bit element offsets inside a block
       bd.F = (int32_t)F;
       bd.K = (int32_t)K;
       return fill_group(fr, true, bd.free_g) && fill_group(kk, false, bd.k_g);

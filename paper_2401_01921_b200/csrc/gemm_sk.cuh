@@ -88,7 +88,7 @@ struct SKCore {
   }
 
   // Math warps: accumulate nk consecutive ring stages (gi = running stage counter).
-  __device__ __forceinline__ static void consume(const T* As, const T* Bs, uint64_t* full, uint64_t* empty, int64_t& gi, int nk,
+  __device__ __forceinline__ static void consume(const T* As, const T* Bs, uint64_t* full, uint64_t* empty, uint32_t& gi, int nk,
                                  Acc& acc) {
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
@@ -223,7 +223,7 @@ struct SKCore {
       constexpr int RA = AMF ? 1 : 4, RB = BNF ? 1 : 4;
       const uint32_t sAbase = smem_u32(As), sBbase = smem_u32(Bs);
       constexpr uint32_t stA = BK * LDA * ES, stB = BK * LDB * ES;
-      int64_t gi = 0;
+      uint32_t gi = 0;  // stage counter (per CTA < 2^32)
       // segments in REVERSE range order: a CTA first publishes the partial of the tile it
       // shares with its successor and finishes (as owner) the tile it shares with its
       // predecessor last, so no CTA waits on one that is still early in its range
@@ -334,7 +334,7 @@ struct SKCore {
     }
 
     // ================================================================== math warps
-    int64_t gi = 0;
+    uint32_t gi = 0;
     Acc acc;
     // segments in REVERSE range order: a CTA first publishes the partial of the tile it
     // shares with its successor and finishes (as owner) the tile it shares with its
