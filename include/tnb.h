@@ -127,8 +127,9 @@ int tnb_copy2d_batched(const void* src, void* dst, int64_t nseg, const TnbCopy2D
 
 /* ---- batched one-sided Jacobi SVD of sector matrices (linalg.py:246-341) ---
  * Each sector: A (m x n, 1 <= m <= n, row-major, dtype TNB_F64 or TNB_C128; s is
- * float64 either way) in `a` (read only),
- * workspaces b (m x n) and q (m x m); outputs the thin factors in torch/LAPACK layout
+ * float64 either way) in `a` (read only), workspaces b (m x ldb) and q (m x ldq)
+ * with ldb = n, ldq = m for complex128 and both rounded up to even for float64
+ * (16-byte rows); outputs the thin factors in torch/LAPACK layout
  * u (m x m row-major), s (m, descending), vh (m x n row-major) and *status:
  * sweeps used (> 0), -1 not converged within max_sweeps, -2 rank deficient
  * (a singular value <= rank_tol * max: its v row cannot be normalised; the

@@ -31,6 +31,7 @@ namespace {
 
 constexpr int kCluster = 16;  // non-portable cluster size (B200 allows 16)
 constexpr int kWarps = 16;
+constexpr int kRegU = 10;     // float64 rows up to 640 (10 double2 units per lane) in registers
 
 struct SvdTask {
   const void* a;   // [m][n] in (read only)
@@ -154,10 +155,18 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32)
   T* __restrict__ B = static_cast<T*>(t.b);
   T* __restrict__ Q = static_cast<T*>(t.q);
   const T* __restrict__ Ain = static_cast<const T*>(t.a);
+  // workspace row strides: float64 rows are padded to an even length (zero pad) so a row is
+  // a whole number of 16-byte double2 units -- the register path moves 16 B per lane access
+  const int ldb = CPLX ? n : n + (n & 1), ldq = CPLX ? m : m + (m & 1);
   // Q = I, B = A
-  for (int64_t x = (int64_t)gw * 32 + lane; x < (int64_t)m * m; x += (int64_t)NW * 32)
-    stcg(Q + x, (x / m == x % m) ? S::one() : S::zero());
-  for (int64_t x = (int64_t)gw * 32 + lane; x < (int64_t)m * n; x += (int64_t)NW * 32) stcg(B + x, Ain[x]);
+  for (int64_t x = (int64_t)gw * 32 + lane; x < (int64_t)m * ldq; x += (int64_t)NW * 32) {
+    const int64_t i = x / ldq, j = x - i * ldq;
+    stcg(Q + x, (i == j) ? S::one() : S::zero());
+  }
+  for (int64_t x = (int64_t)gw * 32 + lane; x < (int64_t)m * ldb; x += (int64_t)NW * 32) {
+    const int64_t i = x / ldb, j = x - i * ldb;
+    stcg(B + x, j < n ? Ain[i * n + j] : S::zero());
+  }
   cluster_sync_all();
   const int P = m + (m & 1);  // an odd row count gets a virtual zero row (its pairs are skipped)
   // rotation threshold on |cos(b_p, b_q)|: tol x the rounding level of a length-n dot product
@@ -177,12 +186,69 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32)
             a = b;
             b = x;
           }
-          T* ra = B + (int64_t)a * n;
-          T* rb = B + (int64_t)b * n;
-          T* qa = Q + (int64_t)a * m;
-          T* qb = Q + (int64_t)b * m;
+          T* ra = B + (int64_t)a * ldb;
+          T* rb = B + (int64_t)b * ldb;
+          T* qa = Q + (int64_t)a * ldq;
+          T* qb = Q + (int64_t)b * ldq;
           double c, s, pr, pi;
-          if (n <= 32 * RPL && m <= 32 * RPL) {
+          if constexpr (!CPLX) {
+            if (ldb <= 64 * kRegU && ldq <= 64 * kRegU) {
+              // float64 rows as double2 units in registers: one 16-byte access per lane and unit
+              const int nu = ldb >> 1, mu = ldq >> 1;
+              const double2* ra2 = reinterpret_cast<const double2*>(ra);
+              const double2* rb2 = reinterpret_cast<const double2*>(rb);
+              double2 x[kRegU], y[kRegU];
+              double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+              for (int u = 0; u < kRegU; ++u) {
+                const int j = lane + 32 * u;
+                x[u] = j < nu ? __ldcg(ra2 + j) : make_double2(0.0, 0.0);
+                y[u] = j < nu ? __ldcg(rb2 + j) : make_double2(0.0, 0.0);
+              }
+#pragma unroll
+              for (int u = 0; u < kRegU; ++u) {
+                al = fma(x[u].x, x[u].x, fma(x[u].y, x[u].y, al));
+                be = fma(y[u].x, y[u].x, fma(y[u].y, y[u].y, be));
+                ga = fma(x[u].x, y[u].x, fma(x[u].y, y[u].y, ga));
+              }
+              al = warp_sum(al);
+              be = warp_sum(be);
+              ga = warp_sum(ga);
+              if (!rotation(al, be, ga, 0.0, thresh, c, s, pr, pi)) continue;
+              const double sp = s * pr, cp = c * pr;  // real phase: +-1
+              double2* wa = reinterpret_cast<double2*>(ra);
+              double2* wb = reinterpret_cast<double2*>(rb);
+#pragma unroll
+              for (int u = 0; u < kRegU; ++u) {
+                const int j = lane + 32 * u;
+                if (j < nu) {
+                  __stcg(wa + j, make_double2(c * x[u].x - sp * y[u].x, c * x[u].y - sp * y[u].y));
+                  __stcg(wb + j, make_double2(s * x[u].x + cp * y[u].x, s * x[u].y + cp * y[u].y));
+                }
+              }
+              const double2* qa2 = reinterpret_cast<const double2*>(qa);
+              const double2* qb2 = reinterpret_cast<const double2*>(qb);
+#pragma unroll
+              for (int u = 0; u < kRegU; ++u) {
+                const int j = lane + 32 * u;
+                x[u] = j < mu ? __ldcg(qa2 + j) : make_double2(0.0, 0.0);
+                y[u] = j < mu ? __ldcg(qb2 + j) : make_double2(0.0, 0.0);
+              }
+              double2* va = reinterpret_cast<double2*>(qa);
+              double2* vb = reinterpret_cast<double2*>(qb);
+#pragma unroll
+              for (int u = 0; u < kRegU; ++u) {
+                const int j = lane + 32 * u;
+                if (j < mu) {
+                  __stcg(va + j, make_double2(c * x[u].x - sp * y[u].x, c * x[u].y - sp * y[u].y));
+                  __stcg(vb + j, make_double2(s * x[u].x + cp * y[u].x, s * x[u].y + cp * y[u].y));
+                }
+              }
+              ++nrot;
+              continue;
+            }
+          }
+          if (CPLX && n <= 32 * RPL && m <= 32 * RPL) {
             // rows held in registers: one L2 round trip for B's rows, one for Q's
             T x[RPL], y[RPL];
             double al = 0.0, be = 0.0, gre = 0.0, gim = 0.0;
@@ -276,7 +342,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32)
   T* __restrict__ VH = static_cast<T*>(t.vh);
   for (int i = gw; i < m; i += NW) {
     double x2 = 0.0;
-    for (int j = lane; j < n; j += 32) x2 += S::abs2(ldcg(B + (int64_t)i * n + j));
+    for (int j = lane; j < n; j += 32) x2 += S::abs2(ldcg(B + (int64_t)i * ldb + j));
     x2 = warp_sum(x2);
     if (lane == 0) __stcg(t.norm + i, sqrt(x2));
   }
@@ -298,8 +364,8 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32)
     if (si <= rank_tol * smax) deficient = true;
     if (lane == 0) t.s[rank] = si;
     const double inv = si > 0.0 ? 1.0 / si : 0.0;
-    for (int j = lane; j < n; j += 32) VH[(int64_t)rank * n + j] = S::scale(inv, ldcg(B + (int64_t)i * n + j));
-    for (int j = lane; j < m; j += 32) U[(int64_t)j * m + rank] = S::conj(ldcg(Q + (int64_t)i * m + j));
+    for (int j = lane; j < n; j += 32) VH[(int64_t)rank * n + j] = S::scale(inv, ldcg(B + (int64_t)i * ldb + j));
+    for (int j = lane; j < m; j += 32) U[(int64_t)j * m + rank] = S::conj(ldcg(Q + (int64_t)i * ldq + j));
   }
   if (deficient && lane == 0) atomicExch(t.status, -2);
   cluster_sync_all();

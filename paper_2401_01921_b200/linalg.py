@@ -191,11 +191,14 @@ def _factorise(mz):
         u = torch.empty((b, r, r), dtype=tdt, device=dev)
         sv = torch.empty((b, r), dtype=torch.float64, device=dev)
         vh = torch.empty((b, r, c), dtype=tdt, device=dev)
-        q = torch.empty((b, r, r), dtype=tdt, device=dev)
-        w = torch.empty((b, r, c), dtype=tdt, device=dev)  # rotated rows (a stays intact)
+        # workspaces: float64 rows padded to even length (16-byte rows in the kernel)
+        lw = c + (c & 1) if es == 8 else c
+        lq = r + (r & 1) if es == 8 else r
+        q = torch.empty((b, r, lq), dtype=tdt, device=dev)
+        w = torch.empty((b, r, lw), dtype=tdt, device=dev)  # rotated rows (a stays intact)
         st = torch.zeros(b, dtype=torch.int32, device=dev)
         for k in range(b):
-            jobs.append((a.data_ptr() + k * r * c * es, w.data_ptr() + k * r * c * es, q.data_ptr() + k * r * r * es,
+            jobs.append((a.data_ptr() + k * r * c * es, w.data_ptr() + k * r * lw * es, q.data_ptr() + k * r * lq * es,
                          u.data_ptr() + k * r * r * es, sv.data_ptr() + k * r * 8, vh.data_ptr() + k * r * c * es,
                          st.data_ptr() + 4 * k, r, c))
         recs.append((tall, u, sv, vh, q, st, (a, w)))

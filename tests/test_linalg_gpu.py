@@ -202,7 +202,8 @@ def test_jacobi_kernel_converges_without_fallback(cuda, dt):
         if dt == np.complex128:
             a = a + 1j * rng.standard_normal((m, n))
         ta = torch.from_numpy(a.astype(dt)).cuda()
-        bufs = [torch.empty_like(ta), torch.empty((m, m), dtype=ta.dtype, device="cuda"),
+        lw, lq = (n + (n & 1), m + (m & 1)) if dt == np.float64 else (n, m)  # padded workspaces
+        bufs = [torch.empty((m, lw), dtype=ta.dtype, device="cuda"), torch.empty((m, lq), dtype=ta.dtype, device="cuda"),
                 torch.empty((m, m), dtype=ta.dtype, device="cuda"), torch.empty(m, dtype=torch.float64, device="cuda"),
                 torch.empty_like(ta), torch.zeros(1, dtype=torch.int32, device="cuda")]
         keep.append((a, ta, bufs))

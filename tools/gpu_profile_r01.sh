@@ -8,3 +8,4 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:bs_ 
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:permute -c 4 -f -o gpurun_out/r01_permute python tools/prof_driver.py permute 64x64x64x64 f64 1032,3210,0213,3012 1 > gpurun_out/ncu_perm.log 2>&1; echo ncu5=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:jacobi -c 1 -f -o gpurun_out/r01_svd python tools/svd_probe3.py > gpurun_out/ncu_svd.log 2>&1; echo ncu6=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_sk -c 1 -f -o gpurun_out/r01_peps_step python tools/prof_driver.py peps_step 1 > gpurun_out/ncu_peps.log 2>&1; echo ncu7=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:jacobi -c 1 -f -o gpurun_out/r01_svd python tools/svd_probe3.py > gpurun_out/ncu_svd.log 2>&1; echo ncu8=$?
