@@ -244,12 +244,16 @@ def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, roof=True, s
         out_host = torch.empty(probe.shape, dtype=probe.dtype, pin_memory=True)
 
         # uploads in first-use order on the engine's copy stream: each contraction step
-        # waits only for its own operands, so R's copy runs under the A.L GEMM
+        # waits only for its own operands (and chunk by chunk for chunked ones), so R's copy
+        # runs under the A.L GEMM and the T2.R GEMM trails R's upload panel by panel
         first_use = tnb.tree_leaves(tnb.parse_order(order))
 
         def step():
             for nm in first_use:
-                tensors[nm].get_block_().upload_(pinned[nm])
+                # large operands in 4 chunks: each contraction step that consumes one runs its
+                # column panels as the chunks land (upload and GEMM overlap)
+                big = pinned[nm].numel() * pinned[nm].element_size() >= (8 << 20)
+                tensors[nm].get_block_().upload_(pinned[nm], chunks=4 if big else 1)  # (2-16 swept: 4 best)
             out = net.launch()
             out_host.copy_(out.get_block_().contiguous().storage(), non_blocking=True)
         for _ in range(max(1, warmup)):

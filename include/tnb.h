@@ -144,6 +144,17 @@ typedef struct {
 int tnb_svd_jacobi_batched(int dtype, int nsec, const TnbSvdSector* secs, int max_sweeps, double tol,
                            double rank_tol, void* stream);
 
+/* Same contraction writing a column panel of a wider row-major output: row i of
+ * the result lands at out + i * out_ld (out_ld >= the result's column count;
+ * 0 = packed). Used to pipeline a contraction with the chunked host upload of
+ * its right operand (each chunk of b's outermost free axis = one column panel). */
+int tnb_contract_dense_ld(const void* a, int dtype_a, int rank_a,
+                          const int64_t* shape_a, const int32_t* perm_a,
+                          const void* b, int dtype_b, int rank_b,
+                          const int64_t* shape_b, const int32_t* perm_b,
+                          int nc, const int32_t* a_axes, const int32_t* b_axes,
+                          void* out, int64_t out_ld, int cplx_mode, void* stream);
+
 /* ---- a3: zero-flux block enumeration (unitensor.py:31-45), host only ------
  * Bonds are given as flattened charge tables:
  *   nbonds, nsyms; nsec[b]; btype[b] (+1 IN, -1 OUT);

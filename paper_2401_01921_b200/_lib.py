@@ -19,7 +19,7 @@ CPLX_4M, CPLX_3M = 0, 1
 # exported symbols, kept in sync with include/tnb.h (tests check both directions)
 EXPORTS = (
     "tnb_version", "tnb_launch_count", "tnb_last_error", "tnb_device_count", "tnb_set_device",
-    "tnb_synchronize", "tnb_permute", "tnb_contract_dense",
+    "tnb_synchronize", "tnb_permute", "tnb_contract_dense", "tnb_contract_dense_ld",
     "tnb_zero_flux_blocks", "tnb_bs_contract", "tnb_bs_contract_masked", "tnb_optimal_order",
     "tnb_ktimer_enable", "tnb_ktimer_reset", "tnb_ktimer_read",
     "tnb_bs_plan", "tnb_bs_execute", "tnb_bs_plan_pairs", "tnb_copy2d_batched", "tnb_svd_jacobi_batched",
@@ -63,6 +63,9 @@ def _declare(lib):
         "tnb_contract_dense": ([_p, ctypes.c_int, ctypes.c_int, _pi64, _pi32,
                                 _p, ctypes.c_int, ctypes.c_int, _pi64, _pi32,
                                 ctypes.c_int, _pi32, _pi32, _p, ctypes.c_int, _p], ctypes.c_int),
+        "tnb_contract_dense_ld": ([_p, ctypes.c_int, ctypes.c_int, _pi64, _pi32,
+                                   _p, ctypes.c_int, ctypes.c_int, _pi64, _pi32,
+                                   ctypes.c_int, _pi32, _pi32, _p, _i64, ctypes.c_int, _p], ctypes.c_int),
         "tnb_zero_flux_blocks": ([ctypes.c_int, ctypes.c_int, _pi32, _pi32, _pi64, _pi32,
                                   _i64, _pi32, _pi64], ctypes.c_int),
         "tnb_bs_contract": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -178,7 +181,7 @@ _DENSE_ARGS = {}
 
 
 def contract_dense(a_ptr, a_dt, a_shape, a_perm, b_ptr, b_dt, b_shape, b_perm,
-                   a_axes, b_axes, out_ptr, cplx_mode, stream):
+                   a_axes, b_axes, out_ptr, cplx_mode, stream, out_ld=0):
     # the integer descriptor arrays of a contraction shape are marshalled once and reused
     # (a Network relaunched on same-shape operands re-marshals nothing)
     key = (tuple(a_shape), tuple(a_perm), tuple(b_shape), tuple(b_perm), tuple(a_axes), tuple(b_axes))
@@ -190,6 +193,12 @@ def contract_dense(a_ptr, a_dt, a_shape, a_perm, b_ptr, b_dt, b_shape, b_perm,
             _DENSE_ARGS.clear()
         _DENSE_ARGS[key] = args
     psa, ppa, psb, ppb, pxa, pxb = args[1]
+    if out_ld:
+        check(lib().tnb_contract_dense_ld(a_ptr, a_dt, len(a_shape), psa, ppa,
+                                          b_ptr, b_dt, len(b_shape), psb, ppb,
+                                          len(a_axes), pxa, pxb, out_ptr, int(out_ld), cplx_mode, stream),
+              "contract_dense_ld")
+        return
     check(lib().tnb_contract_dense(a_ptr, a_dt, len(a_shape), psa, ppa,
                                    b_ptr, b_dt, len(b_shape), psb, ppb,
                                    len(a_axes), pxa, pxb, out_ptr, cplx_mode, stream),

@@ -151,12 +151,39 @@ def _contract_dense(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds):
     dt = _result_dtype(A.dtype, B.dtype)
     out_shape = [A.shape[i] for i in a_free] + [B.shape[j] for j in b_free]
     out = DenseTensor.empty(out_shape, dt)
-    _lib.contract_dense(A.data_ptr, dense.dtype_code(A.dtype), A.storage_shape, A.perm,
-                        B.data_ptr, dense.dtype_code(B.dtype), B.storage_shape, B.perm,
-                        a_pos, b_pos, out.data_ptr, _CPLX_MODE, dense.stream_handle())
+    chunks = dense.pending_chunks(B)
+    k0 = B.perm.index(0) if B.rank else -1  # logical axis stored outermost
+    if chunks and b_free and b_free[0] == k0 and A.dtype == B.dtype:
+        _contract_dense_panels(A, B, a_pos, b_pos, b_free, out, chunks)
+    else:
+        _lib.contract_dense(A.data_ptr, dense.dtype_code(A.dtype), A.storage_shape, A.perm,
+                            B.data_ptr, dense.dtype_code(B.dtype), B.storage_shape, B.perm,
+                            a_pos, b_pos, out.data_ptr, _CPLX_MODE, dense.stream_handle())
     if not out_shape:
         return UniTensor.scalar(out)
     return UniTensor._assemble(out_bonds, out_labels, len(a_free), "", [out], None)
+
+
+def _contract_dense_panels(A, B, a_pos, b_pos, b_free, out, chunks):
+    """B is being uploaded in chunks along its outermost storage axis, which is its first
+    free axis: each chunk is a column panel [s0*inner, s1*inner) of the (row-major) output.
+    Launch one panel contraction per chunk, each waiting only for its own chunk's event."""
+    cur = torch.cuda.current_stream()
+    ncols = 1
+    for j in b_free:
+        ncols *= B.shape[j]
+    inner = ncols // B.storage_shape[0]
+    bstride = B.size // B.storage_shape[0]
+    es, oes = B.itemsize, out.itemsize
+    a_ptr, b_base, o_base = A.data_ptr, dense.raw_ptr(B), out.data_ptr
+    for (s0, s1), ev in chunks:
+        cur.wait_event(ev)
+        shp = (s1 - s0,) + tuple(B.storage_shape[1:])
+        _lib.contract_dense(a_ptr, dense.dtype_code(A.dtype), A.storage_shape, A.perm,
+                            b_base + s0 * bstride * es, dense.dtype_code(B.dtype), shp, B.perm,
+                            a_pos, b_pos, o_base + s0 * inner * oes, _CPLX_MODE, dense.stream_handle(),
+                            out_ld=ncols)
+    dense._owner(B)._tnb_ready = None  # every chunk is now ordered before this stream's work
 
 
 def _common_perm(t):

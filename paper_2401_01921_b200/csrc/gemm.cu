@@ -630,11 +630,13 @@ int run_dot(const void* A, const void* B, void* C, const GemmDesc& d, cudaStream
 
 template <bool CPLX, int MODE>
 int dispatch(const void* A, const void* B, void* C, GemmDesc& d, cudaStream_t st) {
-  if ((int64_t)d.M * d.N <= 16) return run_dot<CPLX>(A, B, C, d, st);
-  if (d.N <= 16 && d.K <= 16 && d.M >= 4096) return run_narrow<CPLX, 16, 16>(A, B, C, d, st);
+  // the memory-bound kernels write packed rows; a strided output (column panel) takes stream-K
+  const bool packed = d.out_ld == d.N;
+  if (packed && (int64_t)d.M * d.N <= 16) return run_dot<CPLX>(A, B, C, d, st);
+  if (packed && d.N <= 16 && d.K <= 16 && d.M >= 4096) return run_narrow<CPLX, 16, 16>(A, B, C, d, st);
   if constexpr (!CPLX)
-    if (d.N <= 16 && d.K <= 32 && d.M >= 4096) return run_narrow<CPLX, 16, 32>(A, B, C, d, st);
-  if (d.N <= 64 && d.K <= 64 && d.M >= 4096 && skinny_smem<CPLX>(d) <= 160 * 1024)
+    if (packed && d.N <= 16 && d.K <= 32 && d.M >= 4096) return run_narrow<CPLX, 16, 32>(A, B, C, d, st);
+  if (packed && d.N <= 64 && d.K <= 64 && d.M >= 4096 && skinny_smem<CPLX>(d) <= 160 * 1024)
     return run_skinny<CPLX>(A, B, C, d, st);
   if constexpr (!CPLX) {
     // tile shape with the least padding (N = 64 or M = 64 rows waste half a 128 x 128 tile)
@@ -665,7 +667,7 @@ __global__ void widen_kernel(const double* __restrict__ x, double2* __restrict__
 
 int contract_dense_device(const void* a, int dta, int ra, const int64_t* sa, const int32_t* pa, const void* b,
                           int dtb, int rb, const int64_t* sb, const int32_t* pb, int nc, const int32_t* aax,
-                          const int32_t* bax, void* out, int cplx_mode, cudaStream_t st) {
+                          const int32_t* bax, void* out, int64_t out_ld, int cplx_mode, cudaStream_t st) {
   if ((dta != TNB_F64 && dta != TNB_C128) || (dtb != TNB_F64 && dtb != TNB_C128))
     return fail(TNB_EUNSUP, "contract: only float64 and complex128 are supported on the GPU path (no CPU fallback)");
   Operand A, B;
@@ -793,7 +795,11 @@ int contract_dense_device(const void* a, int dta, int ra, const int64_t* sa, con
     d.kaff.ksA = d.kA.stride[d.kA.n - 1];
     d.kaff.ksB = d.kB.stride[d.kB.n - 1];
   }
-  d.out_ld = (int)N;
+  if (out_ld != 0 && (out_ld < N || out_ld >= (1ll << 31))) {
+    if (tmp) cudaFreeAsync(tmp, st);
+    return fail(TNB_EINVAL, "contract: out_ld must be 0 or >= the output column count");
+  }
+  d.out_ld = (int)(out_ld ? out_ld : N);
   d.a_mfast = 1;
   if (!(d.rowA.n > 0 && d.rowA.stride[d.rowA.n - 1] == 1 && d.rowA.dim[d.rowA.n - 1] >= 4) && d.kA.n > 0 &&
       d.kA.stride[d.kA.n - 1] == 1)
@@ -821,5 +827,18 @@ extern "C" int tnb_contract_dense(const void* a, int dtype_a, int rank_a, const 
       (nc > 0 && (!a_axes || !b_axes)) || !a || !b || !out)
     return tnb::fail(TNB_EINVAL, "contract: NULL argument");
   return tnb::contract_dense_device(a, dtype_a, rank_a, shape_a, perm_a, b, dtype_b, rank_b, shape_b, perm_b, nc,
-                                    a_axes, b_axes, out, cplx_mode, (cudaStream_t)stream);
+                                    a_axes, b_axes, out, 0, cplx_mode, (cudaStream_t)stream);
+}
+
+extern "C" int tnb_contract_dense_ld(const void* a, int dtype_a, int rank_a, const int64_t* shape_a,
+                                     const int32_t* perm_a, const void* b, int dtype_b, int rank_b,
+                                     const int64_t* shape_b, const int32_t* perm_b, int nc, const int32_t* a_axes,
+                                     const int32_t* b_axes, void* out, int64_t out_ld, int cplx_mode, void* stream) {
+  int rc = tnb::require_device();
+  if (rc) return rc;
+  if ((rank_a > 0 && (!shape_a || !perm_a)) || (rank_b > 0 && (!shape_b || !perm_b)) ||
+      (nc > 0 && (!a_axes || !b_axes)) || !a || !b || !out)
+    return tnb::fail(TNB_EINVAL, "contract: NULL argument");
+  return tnb::contract_dense_device(a, dtype_a, rank_a, shape_a, perm_a, b, dtype_b, rank_b, shape_b, perm_b, nc,
+                                    a_axes, b_axes, out, out_ld, cplx_mode, (cudaStream_t)stream);
 }

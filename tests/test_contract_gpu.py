@@ -183,3 +183,32 @@ def test_small_problem_tiles(cuda):
         A = UniTensor(storage.from_numpy(a), labels=["m", "k"])
         B = UniTensor(storage.from_numpy(b), labels=["k", "n"])
         assert rel_fro(contract(A, B).numpy(), a @ b) <= 1e-13
+
+
+def test_chunked_upload_pipelines_panels(cuda):
+    """upload_(..., chunks=k) + contraction: panel-by-panel GEMMs (each waiting for its own
+    chunk) give the same result as a plain contraction -- when the right operand's outermost
+    storage axis is its first free axis (panels), and when it is not (whole wait)."""
+    import torch
+    rng = np.random.default_rng(17)
+    a = rng.standard_normal((37, 6, 29))            # [vl, p, vr]
+    l0, l1 = rng.standard_normal((2, 64, 5, 37))    # [b, w, vl]
+    A = UniTensor(storage.from_numpy(a), labels=["vl", "p", "vr"])
+    L = UniTensor(storage.from_numpy(l0), labels=["b", "w", "vl"])
+    want = np.einsum("xpv,bwx->pvbw", a, l1)
+    for k in (1, 3, 4, 64):
+        L.get_block_().upload_(torch.from_numpy(l1).pin_memory(), chunks=k)
+        got = contract(A, L).numpy()
+        assert rel_fro(got, want) <= 1e-13, k
+        L.get_block_().upload_(torch.from_numpy(l0).pin_memory(), chunks=k)
+        assert rel_fro(contract(A, L).numpy(), np.einsum("xpv,bwx->pvbw", a, l0)) <= 1e-13
+    # outermost storage axis contracted (b is the contracted label here): whole-tensor wait
+    B = UniTensor(storage.from_numpy(l0), labels=["vr", "w", "z"])
+    B.get_block_().upload_(torch.from_numpy(rng.standard_normal((64, 5, 37))).pin_memory(), chunks=4)
+    A2 = UniTensor(storage.from_numpy(rng.standard_normal((3, 64))), labels=["y", "vr"])
+    ref = A2.get_block_().numpy() @ B.get_block_().numpy().reshape(64, -1)
+    assert rel_fro(contract(A2, B).numpy().reshape(3, -1), ref) <= 1e-13
+    # lazily permuted operand: outermost storage axis is not the first free logical axis
+    P = L.permute(["w", "b", "vl"])
+    P.get_block_().upload_(torch.from_numpy(l1).pin_memory(), chunks=4)
+    assert rel_fro(contract(A, P).numpy(), np.einsum("xpv,bwx->pvwb", a, l1)) <= 1e-13
