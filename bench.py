@@ -254,8 +254,7 @@ def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, roof=True, s
                 # column panels as the chunks land (upload and GEMM overlap)
                 big = pinned[nm].numel() * pinned[nm].element_size() >= (8 << 20)
                 tensors[nm].get_block_().upload_(pinned[nm], chunks=4 if big else 1)  # (2-16 swept: 4 best)
-            out = net.launch()
-            out_host.copy_(out.get_block_().contiguous().storage(), non_blocking=True)
+            net.launch(host_out=out_host)  # result streamed to the pinned host buffer
         for _ in range(max(1, warmup)):
             step()
         dist.barrier()

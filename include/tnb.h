@@ -70,6 +70,10 @@ const char* tnb_last_error(void);            /* thread-local, never NULL */
 int tnb_device_count(int* count);            /* 0 devices is not an error */
 int tnb_set_device(int device);
 int tnb_synchronize(void* stream);           /* waits; surfaces async faults */
+/* 2-D strided copy (cudaMemcpy2DAsync; kind: 1 H2D, 2 D2H, 3 D2D): streams a column
+ * panel of a row-major result to (pinned) host memory while later panels compute. */
+int tnb_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch,
+                       int64_t width, int64_t height, int kind, void* stream);
 
 /* ---- kernel timer (measurement; bench.py's roofline) ----------------------
  * While enabled, every libtnb kernel launch outside stream capture records a

@@ -19,7 +19,7 @@ CPLX_4M, CPLX_3M = 0, 1
 # exported symbols, kept in sync with include/tnb.h (tests check both directions)
 EXPORTS = (
     "tnb_version", "tnb_launch_count", "tnb_last_error", "tnb_device_count", "tnb_set_device",
-    "tnb_synchronize", "tnb_permute", "tnb_contract_dense", "tnb_contract_dense_ld",
+    "tnb_synchronize", "tnb_memcpy2d_async", "tnb_permute", "tnb_contract_dense", "tnb_contract_dense_ld",
     "tnb_zero_flux_blocks", "tnb_bs_contract", "tnb_bs_contract_masked", "tnb_optimal_order",
     "tnb_ktimer_enable", "tnb_ktimer_reset", "tnb_ktimer_read",
     "tnb_bs_plan", "tnb_bs_execute", "tnb_bs_plan_pairs", "tnb_copy2d_batched", "tnb_svd_jacobi_batched",
@@ -55,6 +55,7 @@ def _declare(lib):
         "tnb_device_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
         "tnb_set_device": ([ctypes.c_int], ctypes.c_int),
         "tnb_synchronize": ([_p], ctypes.c_int),
+        "tnb_memcpy2d_async": ([_p, _i64, _p, _i64, _i64, _i64, ctypes.c_int, _p], ctypes.c_int),
         "tnb_ktimer_enable": ([ctypes.c_int], ctypes.c_int),
         "tnb_ktimer_reset": ([], ctypes.c_int),
         "tnb_ktimer_read": ([ctypes.c_int, _pi64, ctypes.POINTER(ctypes.c_double),
@@ -135,6 +136,11 @@ def ktimer_read(family):
     n, ms, w = ctypes.c_int64(0), ctypes.c_double(0.0), ctypes.c_double(0.0)
     check(lib().tnb_ktimer_read(int(family), ctypes.byref(n), ctypes.byref(ms), ctypes.byref(w)), "ktimer_read")
     return int(n.value), float(ms.value), float(w.value)
+
+
+def memcpy2d_async(dst, dpitch, src, spitch, width, height, kind, stream):
+    check(lib().tnb_memcpy2d_async(dst, int(dpitch), src, int(spitch), int(width), int(height), int(kind), stream),
+          "memcpy2d_async")
 
 
 def last_error():

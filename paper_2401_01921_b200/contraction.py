@@ -176,6 +176,12 @@ def _contract_dense_panels(A, B, a_pos, b_pos, b_free, out, chunks):
     bstride = B.size // B.storage_shape[0]
     es, oes = B.itemsize, out.itemsize
     a_ptr, b_base, o_base = A.data_ptr, dense.raw_ptr(B), out.data_ptr
+    sink = _PANEL_SINK
+    if sink is not None and not (sink.tensor.numel() == out.size and
+                                 dense._NP_OF_TORCH.get(sink.tensor.dtype) == out.dtype):
+        sink = None
+    d2h = dense.download_stream() if sink is not None else None
+    rows = out.size // ncols
     for (s0, s1), ev in chunks:
         cur.wait_event(ev)
         shp = (s1 - s0,) + tuple(B.storage_shape[1:])
@@ -183,7 +189,28 @@ def _contract_dense_panels(A, B, a_pos, b_pos, b_free, out, chunks):
                             b_base + s0 * bstride * es, dense.dtype_code(B.dtype), shp, B.perm,
                             a_pos, b_pos, o_base + s0 * inner * oes, _CPLX_MODE, dense.stream_handle(),
                             out_ld=ncols)
+        if d2h is not None:  # stream this panel to the host while the next one computes
+            done = torch.cuda.Event()
+            done.record(cur)
+            d2h.wait_event(done)
+            _lib.memcpy2d_async(sink.tensor.data_ptr() + s0 * inner * oes, ncols * oes,
+                                o_base + s0 * inner * oes, ncols * oes, (s1 - s0) * inner * oes, rows, 2,
+                                d2h.cuda_stream)
+    if d2h is not None:
+        cur.wait_stream(d2h)  # the caller's stream sees the whole host result
+        sink.used = True
     dense._owner(B)._tnb_ready = None  # every chunk is now ordered before this stream's work
+
+
+class _Sink:
+    __slots__ = ("tensor", "used")
+
+    def __init__(self, tensor):
+        self.tensor, self.used = tensor, False
+
+
+# set by Network.launch(host_out=...) around the root contraction only
+_PANEL_SINK = None
 
 
 def _common_perm(t):

@@ -174,6 +174,18 @@ int tnb_ktimer_read(int family, int64_t* launches, double* ms, double* work) {
   return TNB_OK;
 }
 
+int tnb_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t height,
+                       int kind, void* stream) {
+  int rc = tnb::require_device();
+  if (rc) return rc;
+  if (!dst || !src || width < 0 || height < 0 || dpitch < width || spitch < width || kind < 0 || kind > 4)
+    return tnb::fail(TNB_EINVAL, "memcpy2d: bad arguments");
+  if (width == 0 || height == 0) return TNB_OK;
+  TNB_CUDA_CHECK(cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width, (size_t)height,
+                                   (cudaMemcpyKind)kind, (cudaStream_t)stream));
+  return TNB_OK;
+}
+
 int tnb_synchronize(void* stream) {
   int rc = tnb::require_device();
   if (rc) return rc;

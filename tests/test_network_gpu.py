@@ -7,7 +7,7 @@ import tnkit_np as oracle
 from tnb_testutil import load, rel_fro
 
 import paper_2401_01921_b200 as tnb
-from paper_2401_01921_b200 import IN, Bond, Network, Symmetry, UniTensor, contract_pair, storage
+from paper_2401_01921_b200 import IN, Bond, Network, Symmetry, UniTensor, contract_pair, parse_order, storage, tree_leaves
 
 pytestmark = pytest.mark.gpu
 
@@ -141,3 +141,29 @@ def test_peps_small_vs_left_fold(cuda):
         net2.put_tensor(nm, net._bindings[nm][0])
     ref = net2.launch().item()  # appearance-order fold
     assert abs(val - ref) <= 1e-10 * max(1.0, abs(ref))
+
+
+def test_launch_streams_result_to_host(cuda):
+    """Network.launch(host_out=...) with chunk-uploaded operands (panel GEMMs, each panel
+    streamed to the host as it completes) and without chunks: the host buffer holds the
+    oracle's result after a synchronize."""
+    import torch
+    inp = oracle.lawr_inputs(48, seed=21)
+    want, _ = oracle.launch(oracle.lawr_slots(), "b, q, b2", inp)
+    net = Network(oracle.LAWR_NET)
+    ts = {}
+    for nm, arr in inp.items():
+        t = UniTensor(storage.from_numpy(np.zeros_like(arr)), labels=[f"{nm}{i}" for i in range(arr.ndim)])
+        net.put_tensor(nm, t, t.labels)
+        ts[nm] = t
+    net.set_order(optimal=True)
+    host = torch.empty(want.size, dtype=torch.float64).pin_memory()
+    for chunks in (1, 4):
+        host.zero_()
+        for nm in tree_leaves(parse_order(net.get_order())):
+            ts[nm].get_block_().upload_(torch.from_numpy(np.ascontiguousarray(inp[nm])).pin_memory(), chunks=chunks)
+        out = net.launch(host_out=host)
+        torch.cuda.synchronize()
+        got = host.numpy().reshape(want.shape)
+        assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want), chunks
+        assert np.array_equal(out.numpy(), got)
