@@ -284,7 +284,8 @@ template <bool CPLX, int MODE>
 struct BsCfg {
   // 64x64 tiles suit the sector sizes; at this tile size the gather rate, not the DMMA
   // rate, is the limit, so two producer warpgroups feed the 16 math warps (measured: 4 math
-  // warps of 32x32 tiles, 1 or 2 CTAs per SM, were 15% slower)
+  // warps of 32x32 tiles at 1 or 2 CTAs per SM 15% slower; 8 math warps of 32x16 tiles + one
+  // producer warpgroup at 2 CTAs per SM 10% slower)
   static constexpr int BM = 64, BN = 64, BK = CPLX ? 8 : 16, WM = 4, WN = 4, STAGES = 8, NPROD = 256;
   using Core = SKCore<CPLX, MODE, BM, BN, BK, WM, WN, STAGES, NPROD>;
 };
