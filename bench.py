@@ -483,10 +483,11 @@ def gpu_lanczos(tnb, chi, dist):
     inp = ORACLE.hermitian_lawr_inputs(chi, seed=7)
     net, _ = lawr_network(tnb, inp)
     op = eig.NetworkMatvec(net.compile(), "A")
+    v0 = torch.from_numpy(np.ascontiguousarray(inp["A"]).reshape(-1)).cuda()  # DMRG: start from psi
 
     def run():
         try:
-            eig.lanczos(op, k=1, tol=1e-14, max_iter=LANCZOS_ITERS, seed=3)
+            eig.lanczos(op, k=1, v0=v0, tol=1e-14, max_iter=LANCZOS_ITERS, seed=3)
         except eig.ConvergenceError:
             pass
     run()
@@ -609,7 +610,7 @@ def cpu_lanczos(chi, iters=4):
         return np.ascontiguousarray(out).reshape(-1)
     t0 = time.perf_counter()
     try:
-        ORACLE.lanczos(mv, int(np.prod(shape)), k=1, tol=1e-14, max_iter=iters, seed=3)
+        ORACLE.lanczos(mv, int(np.prod(shape)), k=1, v0=inp["A"].reshape(-1), tol=1e-14, max_iter=iters, seed=3)
     except RuntimeError:
         pass
     dt = time.perf_counter() - t0

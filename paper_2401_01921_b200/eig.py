@@ -107,47 +107,55 @@ def lanczos(op, k=1, v0=None, tol=1e-12, max_iter=None, seed=None):
         q = random_start()
     q = q / torch.linalg.vector_norm(q)
     m_max = min(max_iter, n)
-    Q = torch.zeros((n, m_max + 1), dtype=tdt, device=dev)
-    Q[:, 0] = q
+    # Krylov basis stored as ROWS (contiguous vectors): the reorthogonalisation is two
+    # row-major GEMVs and every basis access is a contiguous vector
+    Qt = torch.zeros((m_max + 1, n), dtype=tdt, device=dev)
+    Qt[0] = q
     alphas, betas = [], []
     it = 0
     scale = 1.0
+
+    def ritz(count):
+        theta, y = scipy.linalg.eigh_tridiagonal(np.asarray(alphas), np.asarray(betas), select="i",
+                                                 select_range=(0, count - 1))
+        return theta, y
+
+    def vectors(mdim, y):
+        return Qt[:mdim].T @ torch.from_numpy(y.astype(op.dtype)).to(dev)
+
     while True:
-        w = op(Q[:, it])
-        alpha = float(torch.vdot(Q[:, it], w).real)
+        w = op(Qt[it])
+        alpha = float(torch.vdot(Qt[it], w).real)
         alphas.append(alpha)
         scale = max(scale, abs(alpha))
-        w = w - alpha * Q[:, it]
+        w = w - alpha * Qt[it]
         if it > 0:
-            w = w - betas[-1] * Q[:, it - 1]
-        basis = Q[:, :it + 1]
-        w = w - basis @ (basis.conj().T @ w)  # full reorthogonalisation
+            w = w - betas[-1] * Qt[it - 1]
+        basis = Qt[:it + 1]
+        w = w - basis.T @ (basis.conj() @ w)  # full reorthogonalisation
         beta = float(torch.linalg.vector_norm(w))
         mdim = it + 1
         if mdim >= k:
-            theta, y = scipy.linalg.eigh_tridiagonal(np.asarray(alphas), np.asarray(betas), select="i",
-                                                     select_range=(0, k - 1))
+            theta, y = ritz(k)
             resid = beta * np.abs(y[-1, :])
             if np.all(resid <= tol * np.maximum(1.0, np.abs(theta))) or mdim == n:
-                return theta, basis @ torch.from_numpy(y.astype(op.dtype)).to(dev)
+                return theta, vectors(mdim, y)
         if mdim >= m_max:
-            theta, y = scipy.linalg.eigh_tridiagonal(np.asarray(alphas), np.asarray(betas), select="i",
-                                                     select_range=(0, min(k, mdim) - 1))
+            theta, y = ritz(min(k, mdim))
             raise ConvergenceError(
                 f"lanczos did not converge within {max_iter} iterations "
                 f"(best residual {float(np.max(beta * np.abs(y[-1, :]))):.3e})",
-                eigenvalues=theta, eigenvectors=basis @ torch.from_numpy(y.astype(op.dtype)).to(dev))
+                eigenvalues=theta, eigenvectors=vectors(mdim, y))
         if beta <= 1e-13 * scale:
             w = random_start()
-            w = w - basis @ (basis.conj().T @ w)
+            w = w - basis.T @ (basis.conj() @ w)
             nw = float(torch.linalg.vector_norm(w))
             if nw < 1e-12:
-                theta, y = scipy.linalg.eigh_tridiagonal(np.asarray(alphas), np.asarray(betas), select="i",
-                                                         select_range=(0, min(k, mdim) - 1))
-                return theta, basis @ torch.from_numpy(y.astype(op.dtype)).to(dev)
+                theta, y = ritz(min(k, mdim))
+                return theta, vectors(mdim, y)
             betas.append(0.0)
-            Q[:, mdim] = w / nw
+            Qt[mdim] = w / nw
         else:
             betas.append(beta)
-            Q[:, mdim] = w / beta
+            Qt[mdim] = w / beta
         it += 1
