@@ -81,6 +81,9 @@ struct BsMeta {
   int qn_smem;          // qn tables fit in the pairing kernel's shared memory
   int sched_smem;       // bytes of schedule tables the GEMM stages in shared memory (0 = read from global)
   int desc_smem;        // the GEMM also stages the block descriptors (da, db) in shared memory
+  // the schedule tables (tile_kbeg, stiles, out_ptr, pairs, out_M, out_N) and then da, db lie
+  // back to back in the blob in exactly the shared-memory layout: one flat uint4 copy stages them
+  const uint4* img;
 };
 
 // Schedule tables the grouped GEMM reads on every segment / pair switch (dependent
@@ -292,9 +295,12 @@ struct BsCfg {
 
 // Per-call data pointers (A blocks, B blocks, output blocks) travel as a kernel
 // parameter when they fit, so a cached plan needs no per-call H2D copy.
-constexpr int kInlinePtrs = 1024;
+// Two sizes: the parameter block is copied at every launch, so small structures
+// (<= 128 blocks in all) do not pay for 8 KB of unused slots.
+constexpr int kInlinePtrs = 1024, kInlinePtrsSmall = 128;
+template <int NP>
 struct PtrTable {
-  const void* p[kInlinePtrs];
+  const void* p[NP];
 };
 
 struct BsSK {
@@ -306,9 +312,9 @@ struct BsSK {
 constexpr int kTraceW = 64;
 
 
-template <bool CPLX, int MODE, bool AMF, bool BNF>
+template <bool CPLX, int MODE, bool AMF, bool BNF, int NP>
 __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
-    bs_sk_kernel(const __grid_constant__ BsMeta m, const __grid_constant__ PtrTable pt, const BsSK sk) {
+    bs_sk_kernel(const __grid_constant__ BsMeta m, const __grid_constant__ PtrTable<NP> pt, const BsSK sk) {
   using Cfg = BsCfg<CPLX, MODE>;
   using Core = typename Cfg::Core;
   using Base = typename Core::Base;
@@ -326,6 +332,7 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(kOffB + 2 * BK);
   uint64_t* empty = full + STAGES;
 
+  const long long t_entry = sk.trace ? gtimer() : 0;
   const void* const* ptrs = m.ptrs ? m.ptrs : pt.p;
   const int tid = threadIdx.x;
   const int c = blockIdx.x;
@@ -351,24 +358,26 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
     int32_t* s_oM = reinterpret_cast<int32_t*>(q);
     q += al16((size_t)m.nout * 4);
     int32_t* s_oN = reinterpret_cast<int32_t*>(q);
-    for (int x = tid; x <= m.ntiles; x += blockDim.x) s_kbeg[x] = kbeg[x];
-    for (int x = tid; x < m.ntiles; x += blockDim.x) s_tiles[x] = tiles[x];
-    for (int x = tid; x <= m.nout; x += blockDim.x) s_optr[x] = optr[x];
-    for (int x = tid; x < 2 * m.max_pairs; x += blockDim.x) s_pairs[x] = pairs[x];
-    for (int x = tid; x < m.nout; x += blockDim.x) {
-      s_oM[x] = oM[x];
-      s_oN[x] = oN[x];
+    {
+      // one flat copy of the blob's image of this region: all loads of a thread are
+      // independent (a cold-L2 round trip once, not once per table)
+      uint4* dst = reinterpret_cast<uint4*>(smem + al16(Core::kSmem));
+      const int n16 = m.sched_smem / 16, nt = blockDim.x;
+      for (int x = tid; x < n16; x += 4 * nt) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (x + u * nt < n16) v[u] = __ldg(m.img + x + u * nt);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (x + u * nt < n16) dst[x + u * nt] = v[u];
+      }
     }
     if (m.desc_smem) {
       // block descriptors: read on every pair switch by the producers
       q += al16((size_t)m.nout * 4);
-      uint4* s_d = reinterpret_cast<uint4*>(q);
-      const int na16 = (int)(sizeof(BlockDesc) * m.na / 16), nb16 = (int)(sizeof(BlockDesc) * m.nb / 16);
-      const uint4* ga = reinterpret_cast<const uint4*>(m.da);
-      const uint4* gb = reinterpret_cast<const uint4*>(m.db);
-      for (int x = tid; x < na16 + nb16; x += blockDim.x) s_d[x] = x < na16 ? ga[x] : gb[x - na16];
-      DA = reinterpret_cast<const BlockDesc*>(s_d);
-      DB = reinterpret_cast<const BlockDesc*>(s_d + na16);
+      DA = reinterpret_cast<const BlockDesc*>(q);
+      DB = DA + m.na;
     }
     kbeg = s_kbeg;
     tiles = s_tiles;
@@ -604,14 +613,24 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
   uint32_t gi = 0;
   long long* tr_ = (sk.trace && tid == 0) ? sk.trace + (size_t)c * kTraceW : nullptr;
   int nseg = 0;
-  if (tr_) tr_[0] = gtimer();
+  if (tr_) {
+    tr_[0] = gtimer();
+    tr_[kTraceW - 1] = t_entry;
+  }
   for (int64_t e = it1; e > it0;) {
     const int t = tile_of(e - 1);
     const int64_t tstart = kbeg[t], tend = kbeg[t + 1];
     const int64_t sb = it0 > tstart ? it0 : tstart;
     Base::zero(acc);
-    Core::consume(As, Bs, full, empty, gi, (int)(e - sb), acc);
-    if (tr_ && nseg < 15) tr_[4 + 4 * nseg] = gtimer();
+    {
+      // fragments of this warp's 16x16 tile that lie inside the output block
+      const TileRef tr = tiles[t];
+      const int warp = tid >> 5;
+      const int r0 = tr.m0 + (warp / Cfg::WN) * Core::WTM, c0 = tr.n0 + (warp % Cfg::WN) * Core::WTN;
+      const int mfa = (oM[tr.o] - r0 + 7) >> 3, nfa = (oN[tr.o] - c0 + 7) >> 3;
+      Core::consume(As, Bs, full, empty, gi, (int)(e - sb), acc, mfa, nfa);
+    }
+    if (tr_ && nseg < 14) tr_[4 + 4 * nseg] = gtimer();
     if (e < tend) {
       Core::publish(sk.ws, sk.flags, c, acc);
     } else {
@@ -620,7 +639,7 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
       const int M = oM[tr.o], N = oN[tr.o];
       Base::store(static_cast<T*>(const_cast<void*>(ptrs[m.na + m.nb + tr.o])), N, tr.m0, tr.n0, M, N, acc);
     }
-    if (tr_ && nseg < 15) {
+    if (tr_ && nseg < 14) {
       tr_[5 + 4 * nseg] = gtimer();
       tr_[6 + 4 * nseg] = t;
       tr_[7 + 4 * nseg] = e - sb;
@@ -700,10 +719,12 @@ PlanCache g_cache;
 constexpr int kMaxBsCtas = 2048;  // flags region: one int per persistent CTA
 constexpr size_t kBsPartialOff = 16384;
 
-template <bool CPLX, int MODE, bool AMF, bool BNF>
-int launch_bs_one(const BsMeta& meta, const PtrTable* pt, BsSK sk, bool capturing, cudaStream_t st) {
+template <bool CPLX, int MODE, bool AMF, bool BNF, int NP>
+int launch_bs_one(const BsMeta& meta, const void* const* hp, int nptr, BsSK sk, bool capturing, cudaStream_t st) {
   using Core = typename BsCfg<CPLX, MODE>::Core;
-  auto kern = bs_sk_kernel<CPLX, MODE, AMF, BNF>;
+  auto kern = bs_sk_kernel<CPLX, MODE, AMF, BNF, NP>;
+  PtrTable<NP> pt;
+  for (int x = 0; x < nptr && x < NP; ++x) pt.p[x] = hp[x];
   const size_t smem = al16(Core::kSmem) + (size_t)meta.sched_smem;
   static size_t configured = 0;
   static size_t occ_smem = 0;
@@ -741,7 +762,7 @@ int launch_bs_one(const BsMeta& meta, const PtrTable* pt, BsSK sk, bool capturin
   }
   {
     KTimer kt(TNB_KF_BS_GEMM, st, 0.0);
-    kern<<<G, Core::NT, smem, st>>>(meta, *pt, sk);
+    kern<<<G, Core::NT, smem, st>>>(meta, pt, sk);
   }
   count_launch();
   TNB_CUDA_CHECK(cudaGetLastError());
@@ -760,7 +781,7 @@ int launch_bs_one(const BsMeta& meta, const PtrTable* pt, BsSK sk, bool capturin
 
 // Caller holds g_cache.mu.
 template <bool CPLX, int MODE>
-int launch_bs(const Plan& plan, const BsMeta& meta, const PtrTable* pt, cudaStream_t st) {
+int launch_bs(const Plan& plan, const BsMeta& meta, const void* const* hp, int nptr, cudaStream_t st) {
   if (meta.ntiles == 0) return TNB_OK;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   TNB_CUDA_CHECK(cudaStreamIsCapturing(st, &cs));
@@ -768,10 +789,20 @@ int launch_bs(const Plan& plan, const BsMeta& meta, const PtrTable* pt, cudaStre
   if (!capturing && g_cache.ws_ev && g_cache.ws_stream != st) TNB_CUDA_CHECK(cudaStreamWaitEvent(st, g_cache.ws_ev, 0));
   BsSK sk;
   int rc;
-  if (plan.amf && plan.bnf) rc = launch_bs_one<CPLX, MODE, true, true>(meta, pt, sk, capturing, st);
-  else if (plan.amf) rc = launch_bs_one<CPLX, MODE, true, false>(meta, pt, sk, capturing, st);
-  else if (plan.bnf) rc = launch_bs_one<CPLX, MODE, false, true>(meta, pt, sk, capturing, st);
-  else rc = launch_bs_one<CPLX, MODE, false, false>(meta, pt, sk, capturing, st);
+  const bool small = meta.ptrs || nptr <= kInlinePtrsSmall;
+  constexpr int S = kInlinePtrsSmall, L = kInlinePtrs;
+  if (plan.amf && plan.bnf)
+    rc = small ? launch_bs_one<CPLX, MODE, true, true, S>(meta, hp, nptr, sk, capturing, st)
+               : launch_bs_one<CPLX, MODE, true, true, L>(meta, hp, nptr, sk, capturing, st);
+  else if (plan.amf)
+    rc = small ? launch_bs_one<CPLX, MODE, true, false, S>(meta, hp, nptr, sk, capturing, st)
+               : launch_bs_one<CPLX, MODE, true, false, L>(meta, hp, nptr, sk, capturing, st);
+  else if (plan.bnf)
+    rc = small ? launch_bs_one<CPLX, MODE, false, true, S>(meta, hp, nptr, sk, capturing, st)
+               : launch_bs_one<CPLX, MODE, false, true, L>(meta, hp, nptr, sk, capturing, st);
+  else
+    rc = small ? launch_bs_one<CPLX, MODE, false, false, S>(meta, hp, nptr, sk, capturing, st)
+               : launch_bs_one<CPLX, MODE, false, false, L>(meta, hp, nptr, sk, capturing, st);
   if (rc) return rc;
   if (!capturing) {
     if (!g_cache.ws_ev) TNB_CUDA_CHECK(cudaEventCreateWithFlags(&g_cache.ws_ev, cudaEventDisableTiming));
@@ -972,16 +1003,21 @@ int bs_plan_locked(int dtype, int na, int nb, int nout, int rank_a, int rank_b, 
       off = o + bytes;
       return o;
     };
+    // the GEMM's shared-memory image first (see BsMeta::img; same order and padding as
+    // sched_bytes), then the pairing kernel's inputs and scratch
+    const size_t o_kbeg = take(al16((size_t)(tiles.size() + 1) * 4)), o_stiles = take(sizeof(TileRef) * tiles.size()),
+                 o_optr = take(al16((size_t)(nout + 1) * 4)), o_pairs = take(al16((size_t)meta.max_pairs * 8)),
+                 o_oM = take(al16((size_t)nout * 4)), o_oN = take(al16((size_t)nout * 4)),
+                 o_da = take(sizeof(BlockDesc) * na), o_db = take(sizeof(BlockDesc) * nb);
     const size_t o_aqn = take((size_t)na * rank_a * 4), o_bqn = take((size_t)nb * rank_b * 4),
-                 o_oqn = take((size_t)nout * ro * 4), o_oM = take((size_t)nout * 4), o_oN = take((size_t)nout * 4),
-                 o_da = take(sizeof(BlockDesc) * na), o_db = take(sizeof(BlockDesc) * nb),
-                 o_tiles = take(sizeof(TileRef) * tiles.size()),
+                 o_oqn = take((size_t)nout * ro * 4), o_tiles = take(sizeof(TileRef) * tiles.size()),
                  o_mask = take(panel_mask ? (size_t)npanels : 0);
     const size_t upload = off;
-    const size_t o_optr = take((size_t)(nout + 1) * 4), o_err = take(16 + 16 * 8), o_pairs = take((size_t)meta.max_pairs * 8),
-                 o_kbeg = take((size_t)(tiles.size() + 1) * 4), o_tcnt = take((size_t)tiles.size() * 4),
-                 o_stiles = take(sizeof(TileRef) * tiles.size());
+    const size_t o_err = take(16 + 16 * 8), o_tcnt = take((size_t)tiles.size() * 4);
     const size_t total = off;
+    if (o_oM - o_kbeg != sched_bytes((int)tiles.size(), nout, meta.max_pairs) - 2 * al16((size_t)nout * 4) ||
+        o_da != o_kbeg + sched_bytes((int)tiles.size(), nout, meta.max_pairs))
+      return fail(TNB_EUNSUP, "bs_contract: schedule image layout mismatch");
     std::vector<unsigned char> h(upload);
     memcpy(h.data() + o_aqn, a_qn, (size_t)na * rank_a * 4);
     memcpy(h.data() + o_bqn, b_qn, (size_t)nb * rank_b * 4);
@@ -1011,6 +1047,7 @@ int bs_plan_locked(int dtype, int na, int nb, int nout, int rank_a, int rank_b, 
     meta.tile_kbeg = reinterpret_cast<int32_t*>(dblob + o_kbeg);
     meta.tile_cnt = reinterpret_cast<int32_t*>(dblob + o_tcnt);
     meta.stiles = reinterpret_cast<TileRef*>(dblob + o_stiles);
+    meta.img = reinterpret_cast<const uint4*>(dblob + o_kbeg);
     meta.ptrs = nullptr;
     meta.qn_smem = 1;
     size_t pair_smem = pair_smem_bytes(meta);
@@ -1064,11 +1101,12 @@ int bs_execute_locked(Plan& plan, const void* const* a_ptrs, const void* const* 
   int rc = TNB_OK;
   // ---- per-call data pointers
   const int nptr = na + nb + nout;
-  PtrTable pt;
+  std::vector<const void*> hv;
   if (nptr <= kInlinePtrs) {
-    for (int i = 0; i < na; ++i) pt.p[i] = a_ptrs[i];
-    for (int j = 0; j < nb; ++j) pt.p[na + j] = b_ptrs[j];
-    for (int o = 0; o < nout; ++o) pt.p[na + nb + o] = out_ptrs[o];
+    hv.resize(nptr);
+    for (int i = 0; i < na; ++i) hv[i] = a_ptrs[i];
+    for (int j = 0; j < nb; ++j) hv[na + j] = b_ptrs[j];
+    for (int o = 0; o < nout; ++o) hv[na + nb + o] = out_ptrs[o];
     meta.ptrs = nullptr;
   } else {
     if (g_cache.stage_ev) TNB_CUDA_CHECK(cudaEventSynchronize(g_cache.stage_ev));
@@ -1089,8 +1127,10 @@ int bs_execute_locked(Plan& plan, const void* const* a_ptrs, const void* const* 
     TNB_CUDA_CHECK(cudaEventRecord(g_cache.stage_ev, st));
     meta.ptrs = static_cast<const void* const*>(dptr);
   }
-  if (plan.dtype == TNB_F64) rc = launch_bs<false, 0>(plan, meta, &pt, st);
-  else rc = launch_bs<true, 0>(plan, meta, &pt, st);
+  const void* const* hp = meta.ptrs ? nullptr : hv.data();
+  const int nin = meta.ptrs ? 0 : nptr;
+  if (plan.dtype == TNB_F64) rc = launch_bs<false, 0>(plan, meta, hp, nin, st);
+  else rc = launch_bs<true, 0>(plan, meta, hp, nin, st);
   if (meta.ptrs) cudaFreeAsync(const_cast<void*>(static_cast<const void*>(meta.ptrs)), st);
   if (rc != TNB_OK) return rc;
   return TNB_OK;

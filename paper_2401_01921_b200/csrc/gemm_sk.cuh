@@ -88,8 +88,16 @@ struct SKCore {
   }
 
   // Math warps: accumulate nk consecutive ring stages (gi = running stage counter).
+  // mfa/nfa (< MF/NF on edge tiles): this warp's 8-row / 8-column fragments that hold
+  // real output; the rest are padding and skip their DMMAs (warp-uniform).
   __device__ __forceinline__ static void consume(const T* As, const T* Bs, uint64_t* full, uint64_t* empty, uint32_t& gi, int nk,
-                                 Acc& acc) {
+                                 Acc& acc, int mfa = MF, int nfa = NF) {
+    if (mfa >= MF && nfa >= NF) consume_impl<false>(As, Bs, full, empty, gi, nk, acc, MF, NF);
+    else consume_impl<true>(As, Bs, full, empty, gi, nk, acc, mfa, nfa);
+  }
+  template <bool PRED>
+  __device__ __forceinline__ static void consume_impl(const T* As, const T* Bs, uint64_t* full, uint64_t* empty, uint32_t& gi,
+                                                      int nk, Acc& acc, int mfa, int nfa) {
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int wm = warp / WARPS_N, wn = warp % WARPS_N;
@@ -99,6 +107,11 @@ struct SKCore {
     for (int kt = 0; kt < nk; ++kt, ++gi) {
       const int s = (int)(gi % STAGES);
       detail::mbar_wait(&full[s], (uint32_t)((gi / STAGES) & 1));
+      if (PRED && (mfa <= 0 || nfa <= 0)) {  // all-padding warp tile: release the stage only
+        __syncwarp();
+        if (lane == 0) detail::mbar_arrive(&empty[s]);
+        continue;
+      }
       const T* as = As + s * BK * LDA;
       const T* bs = Bs + s * BK * LDB;
 #pragma unroll
@@ -113,7 +126,8 @@ struct SKCore {
 #pragma unroll
           for (int i = 0; i < MF; ++i)
 #pragma unroll
-            for (int j = 0; j < NF; ++j) dmma(acc[0][i][j][0], acc[0][i][j][1], af[i], bf[j]);
+            for (int j = 0; j < NF; ++j)
+              if (!PRED || (i < mfa && j < nfa)) dmma(acc[0][i][j][0], acc[0][i][j][1], af[i], bf[j]);
         } else {
           double2 af[MF], bf[NF];
 #pragma unroll
@@ -126,6 +140,7 @@ struct SKCore {
               const double ain = dneg(af[i].y);
 #pragma unroll
               for (int j = 0; j < NF; ++j) {
+                if (PRED && !(i < mfa && j < nfa)) continue;
                 dmma(acc[0][i][j][0], acc[0][i][j][1], af[i].x, bf[j].x);
                 dmma(acc[0][i][j][0], acc[0][i][j][1], ain, bf[j].y);
                 dmma(acc[1][i][j][0], acc[1][i][j][1], af[i].x, bf[j].y);
@@ -141,6 +156,7 @@ struct SKCore {
               const double asum = af[i].x + af[i].y;
 #pragma unroll
               for (int j = 0; j < NF; ++j) {
+                if (PRED && !(i < mfa && j < nfa)) continue;
                 dmma(acc[0][i][j][0], acc[0][i][j][1], af[i].x, bf[j].x);
                 dmma(acc[1][i][j][0], acc[1][i][j][1], af[i].y, bf[j].y);
                 dmma(acc[2][i][j][0], acc[2][i][j][1], asum, bsum[j]);
