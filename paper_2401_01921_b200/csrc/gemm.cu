@@ -22,6 +22,7 @@
 // L.A.W.R) go to a separate memory-bound kernel.
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <cstring>
 #include <vector>
 
@@ -523,6 +524,50 @@ struct Tiled {
   }
 };
 
+// Persistent stream-K workspace (eager launches): partials, then one flag per CTA.
+struct SkWorkspace {
+  std::mutex mu;
+  void* mem = nullptr;
+  size_t flags_off = 0;  // bytes of partials
+  int nflags = 0;
+  int device = -1;
+  cudaEvent_t ev = nullptr;
+  cudaStream_t last = nullptr;
+  int acquire(size_t partial_bytes, int G, cudaStream_t st) {
+    int dev = 0;
+    TNB_CUDA_CHECK(cudaGetDevice(&dev));
+    if (dev != device || partial_bytes > flags_off || G > nflags) {
+      if (mem) {
+        TNB_CUDA_CHECK(cudaDeviceSynchronize());
+        cudaFree(mem);
+        mem = nullptr;
+      }
+      if (ev && dev != device) {
+        cudaEventDestroy(ev);
+        ev = nullptr;
+      }
+      flags_off = std::max(partial_bytes, flags_off);
+      nflags = std::max(G, std::max(nflags, 1024));
+      TNB_CUDA_CHECK(cudaMalloc(&mem, flags_off + (size_t)nflags * 4));
+      TNB_CUDA_CHECK(cudaMemset(static_cast<char*>(mem) + flags_off, 0, (size_t)nflags * 4));
+      device = dev;
+      last = nullptr;
+    }
+    if (!ev) TNB_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    if (last && last != st) TNB_CUDA_CHECK(cudaStreamWaitEvent(st, ev, 0));
+    return TNB_OK;
+  }
+  int release(cudaStream_t st) {
+    TNB_CUDA_CHECK(cudaEventRecord(ev, st));
+    last = st;
+    return TNB_OK;
+  }
+};
+SkWorkspace& sk_workspace() {
+  static SkWorkspace* w = new SkWorkspace();  // never destroyed (process-lifetime device memory)
+  return *w;
+}
+
 // Host side of the stream-K kernel: one CTA per SM, workspace for split tiles.
 template <bool CPLX, int MODE, int BM, int BN, int BK, int WM, int WN, int ST>
 struct StreamK {
@@ -545,6 +590,12 @@ struct StreamK {
     TNB_CUDA_CHECK(cudaGetLastError());
     return TNB_OK;
   }
+  static int dispatch(const void* A, const void* B, void* C, const GemmDesc& d, const SKParams& sk, cudaStream_t st) {
+    if (d.a_mfast && d.b_nfast) return launch_one<true, true>(A, B, C, d, sk, st);
+    if (d.a_mfast) return launch_one<true, false>(A, B, C, d, sk, st);
+    if (d.b_nfast) return launch_one<false, true>(A, B, C, d, sk, st);
+    return launch_one<false, false>(A, B, C, d, sk, st);
+  }
   static int run(const void* A, const void* B, void* C, GemmDesc d, cudaStream_t st) {
     d.tiles_m = (d.M + BM - 1) / BM;
     d.tiles_n = (d.N + BN - 1) / BN;
@@ -555,20 +606,35 @@ struct StreamK {
     if ((int64_t)d.tiles_m * d.tiles_n >= (1ll << 31)) return fail(TNB_EUNSUP, "contract: too many tiles");
     // >= 4 k-tiles per CTA: tiny problems do not pay for many partial hand-offs
     sk.G = (int)std::max<int64_t>(1, std::min<int64_t>(sk.total / 4, sms()));
-    size_t ws_bytes = (size_t)sk.G * Core::ACCN * Core::NMATH * 8;
-    void* mem = nullptr;
-    TNB_CUDA_CHECK(cudaMallocAsync(&mem, ws_bytes + (size_t)sk.G * 4 + 64, st));
-    sk.ws = static_cast<double*>(mem);
-    sk.flags = reinterpret_cast<int*>(static_cast<char*>(mem) + ws_bytes);
-    cudaError_t e = cudaMemsetAsync(sk.flags, 0, (size_t)sk.G * 4, st);
-    int rc = TNB_OK;
-    if (e != cudaSuccess) rc = cuda_fail(e, "contract: workspace memset");
-    else if (d.a_mfast && d.b_nfast) rc = launch_one<true, true>(A, B, C, d, sk, st);
-    else if (d.a_mfast) rc = launch_one<true, false>(A, B, C, d, sk, st);
-    else if (d.b_nfast) rc = launch_one<false, true>(A, B, C, d, sk, st);
-    else rc = launch_one<false, false>(A, B, C, d, sk, st);
-    cudaFreeAsync(mem, st);
-    return rc;
+    const size_t ws_bytes = (size_t)sk.G * Core::ACCN * Core::NMATH * 8;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    TNB_CUDA_CHECK(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone) {
+      // graph capture: the graph owns its workspace (a graph replays independently of
+      // eager launches on other streams); flags zeroed by a memset node
+      void* mem = nullptr;
+      TNB_CUDA_CHECK(cudaMallocAsync(&mem, ws_bytes + (size_t)sk.G * 4 + 64, st));
+      sk.ws = static_cast<double*>(mem);
+      sk.flags = reinterpret_cast<int*>(static_cast<char*>(mem) + ws_bytes);
+      sk.clear = 0;
+      cudaError_t e = cudaMemsetAsync(sk.flags, 0, (size_t)sk.G * 4, st);
+      int rc = e != cudaSuccess ? cuda_fail(e, "contract: workspace memset") : dispatch(A, B, C, d, sk, st);
+      cudaFreeAsync(mem, st);
+      return rc;
+    }
+    // eager: one persistent workspace per process whose flags the owners reset, so a
+    // launch needs no allocation and no memset; launches from different streams are
+    // serialised on it through an event
+    SkWorkspace& w = sk_workspace();
+    std::lock_guard<std::mutex> lk(w.mu);
+    int rc = w.acquire(ws_bytes, sk.G, st);
+    if (rc) return rc;
+    sk.ws = static_cast<double*>(w.mem);
+    sk.flags = reinterpret_cast<int*>(static_cast<char*>(w.mem) + w.flags_off);
+    sk.clear = 1;
+    rc = dispatch(A, B, C, d, sk, st);
+    if (rc) return rc;
+    return w.release(st);
   }
 };
 

@@ -33,7 +33,8 @@ struct SKParams {
   int G;           // persistent CTAs
   int64_t total;   // tiles * KT
   double* ws;      // [G][ACCN][NMATH] register partials
-  int* flags;      // [G], zeroed before the launch
+  int* flags;      // [G], zero before the launch
+  int clear;       // owners reset the flags they consume (persistent workspace, no memset)
 };
 
 namespace detail {
@@ -369,7 +370,7 @@ struct SKCore {
       if (kt1 < KT) {
         publish(sk.ws, sk.flags, c, acc);
       } else {
-        if (kt0 > 0) absorb(sk.ws, sk.flags, detail::sk_cta_of(sk.total, sk.G, tile * (int64_t)KT), c, acc, false);
+        if (kt0 > 0) absorb(sk.ws, sk.flags, detail::sk_cta_of(sk.total, sk.G, tile * (int64_t)KT), c, acc, sk.clear != 0);
         Base::store(C, d.out_ld, m0, n0, d.M, d.N, acc);
       }
       e = sb;
