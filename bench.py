@@ -214,6 +214,9 @@ def lawr_macs(chi, d=2, D=5):
     return tnb.contraction_cost(tree, sets, dims), tnb.render_order(tree)
 
 
+E2E_CHUNKS = int(os.environ.get("TNB_E2E_CHUNKS", "2"))  # 1-8 swept with double buffering: 2 best
+
+
 def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, roof=True, seed=1234, graph=False):
     import torch
     inp = WL.lawr_inputs(chi, dtype=dtype, seed=seed + 17 * dist.rank)
@@ -237,40 +240,52 @@ def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, roof=True, s
         res["graph_ms_per_step"] = gms
         res["gflops_graph"] = dist.sum(flop) / gms / 1e6
     if e2e:
-        # end to end through the public API: pinned host inputs -> HBM, launch, result -> host
-        pinned = {nm: torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for nm, a in inp.items()}
-        h2d = sum(p.numel() * p.element_size() for p in pinned.values())
+        # end to end through the public API: pinned host inputs -> HBM, launch, result -> host.
+        # A serving loop: two networks with their own device inputs and pinned host
+        # buffers alternate (double buffering), so step i+1's uploads -- each ordered only
+        # after the launch that last read that buffer set (upload_(after=net.done_event)) --
+        # overlap step i's kernels; every step still copies all of its inputs in and its
+        # result out.
+        sets = [(net, tensors)] + [lawr_network(tnb, inp)]
+        pinned = [{nm: torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for nm, a in inp.items()}
+                  for _ in sets]
+        h2d = sum(p.numel() * p.element_size() for p in pinned[0].values())
         probe = net.launch().get_block_().contiguous().storage()
-        out_host = torch.empty(probe.shape, dtype=probe.dtype, pin_memory=True)
+        outs = [torch.empty(probe.shape, dtype=probe.dtype, pin_memory=True) for _ in sets]
 
         # uploads in first-use order on the engine's copy stream: each contraction step
         # waits only for its own operands (and chunk by chunk for chunked ones), so R's copy
         # runs under the A.L GEMM and the T2.R GEMM trails R's upload panel by panel
         first_use = tnb.tree_leaves(tnb.parse_order(order))
 
-        def step():
+        def step(i):
+            n, ts = sets[i % 2]
             for nm in first_use:
-                # large operands in 4 chunks: each contraction step that consumes one runs its
+                # large operands in chunks: each contraction step that consumes one runs its
                 # column panels as the chunks land (upload and GEMM overlap)
-                big = pinned[nm].numel() * pinned[nm].element_size() >= (8 << 20)
-                tensors[nm].get_block_().upload_(pinned[nm], chunks=4 if big else 1)  # (2-16 swept: 4 best)
-            net.launch(host_out=out_host)  # result streamed to the pinned host buffer
-        for _ in range(max(1, warmup)):
-            step()
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = _events()
-        e0.record()
-        for _ in range(steps):
-            step()
-        e1.record()
-        torch.cuda.synchronize()
-        dist.barrier()
-        ems = dist.max(e0.elapsed_time(e1))
-        d2h = out_host.numel() * out_host.element_size()
+                big = pinned[0][nm].numel() * pinned[0][nm].element_size() >= (8 << 20)
+                ts[nm].get_block_().upload_(pinned[i % 2][nm], chunks=E2E_CHUNKS if big else 1, after=n.done_event)
+            n.launch(host_out=outs[i % 2])  # result streamed to the pinned host buffer
+
+        def run(k):
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = _events()
+            e0.record()
+            for i in range(k):
+                step(i)
+            e1.record()
+            torch.cuda.synchronize()
+            dist.barrier()
+            return dist.max(e0.elapsed_time(e1))
+        run(max(2, warmup))
+        ems = run(steps)
+        lat = run(1)  # one step alone: latency, no overlap with a neighbour
+        d2h = outs[0].numel() * outs[0].element_size()
         res["e2e"] = {"value": dist.sum(flop) / (ems / steps) / 1e6, "unit": "GFLOP/s",
                       "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                      "ms_per_step": ems / steps}
+                      "ms_per_step": ems / steps, "single_step_latency_ms": lat,
+                      "pipelining": "double-buffered inputs/outputs, upload of step i+1 overlaps step i"}
     if roof:
         # dominant kernel = the stream-K DMMA GEMM (steps A.L and T2.R): the library's kernel
         # timer records a CUDA event pair around each of its launches ON THE LAUNCHING STREAM;

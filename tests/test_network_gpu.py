@@ -167,3 +167,53 @@ def test_launch_streams_result_to_host(cuda):
         got = host.numpy().reshape(want.shape)
         assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want), chunks
         assert np.array_equal(out.numpy(), got)
+
+
+def test_double_buffered_serving_loop(cuda):
+    """The e2e serving loop of bench.py: two networks alternate, each refilling its inputs
+    with upload_(..., after=net.done_event) (ordered only after the launch that last read
+    them) while the other one computes; uneven chunk sizes; every step's host result
+    equals the oracle's for that step's inputs."""
+    import torch
+    steps = 6
+    inps = [oracle.lawr_inputs(40, seed=100 + s) for s in range(steps)]
+    wants = [oracle.launch(oracle.lawr_slots(), "b, q, b2", inp)[0] for inp in inps]
+    sets = []
+    for _ in range(2):
+        net = Network(oracle.LAWR_NET)
+        ts = {}
+        for nm, arr in inps[0].items():
+            t = UniTensor(storage.from_numpy(np.zeros_like(arr)), labels=[f"{nm}{i}" for i in range(arr.ndim)])
+            net.put_tensor(nm, t, t.labels)
+            ts[nm] = t
+        net.set_order(optimal=True)
+        assert net.done_event is None
+        sets.append((net, ts))
+    pinned = [{nm: torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for nm, a in inp.items()} for inp in inps]
+    hosts = [torch.zeros(wants[0].size, dtype=torch.float64).pin_memory() for _ in range(steps)]
+    order = tree_leaves(parse_order(sets[0][0].get_order()))
+    for s in range(steps):
+        net, ts = sets[s % 2]
+        for nm in order:
+            ts[nm].get_block_().upload_(pinned[s][nm], chunks=(1, 3, 2) if nm in ("L", "R") else 1,
+                                        after=net.done_event)
+        net.launch(host_out=hosts[s])
+        assert net.done_event is not None
+    torch.cuda.synchronize()
+    for s in range(steps):
+        got = hosts[s].numpy().reshape(wants[s].shape)
+        assert np.linalg.norm(got - wants[s]) <= 1e-12 * np.linalg.norm(wants[s]), s
+
+
+def test_upload_chunk_sizes(cuda):
+    """upload_ with relative chunk sizes: boundaries on storage axis 0, all data lands."""
+    import torch
+    from paper_2401_01921_b200 import dense
+    arr = np.random.default_rng(3).standard_normal((10, 7))
+    t = storage.from_numpy(np.zeros_like(arr))
+    t.upload_(torch.from_numpy(arr).pin_memory(), chunks=(1, 1, 3))
+    ch = dense.pending_chunks(t)
+    assert [r for r, _ in ch] == [(0, 2), (2, 4), (4, 10)]
+    assert np.array_equal(t.numpy(), arr)
+    with pytest.raises(ValueError):
+        t.upload_(torch.from_numpy(arr).pin_memory(), chunks=(1, 0))
