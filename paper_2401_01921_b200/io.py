@@ -42,12 +42,25 @@ def _bond_to_json(b):
             "sectors": [[list(q), d] for q, d in b.sectors]}
 
 
+_SECTORS = {}  # (syms, raw sectors) -> validated (sectors, syms, dim); tuples only (immutable)
+
+
 def _bond_from_json(d):
     btype = BondType[d["btype"]]
-    if d["sectors"]:
-        return Bond(btype=btype, sectors=[(tuple(q), deg) for q, deg in d["sectors"]],
-                    syms=[symmetry_from_str(t) for t in d["syms"]])
-    return Bond(d["dim"], btype)
+    if not d["sectors"]:
+        return Bond(d["dim"], btype)
+    key = (tuple(d["syms"]), tuple((tuple(q), deg) for q, deg in d["sectors"]))
+    hit = _SECTORS.get(key)
+    if hit is None:
+        ref = Bond(btype=btype, sectors=list(key[1]), syms=[symmetry_from_str(t) for t in d["syms"]])
+        hit = (ref.sectors, ref.syms, ref.dim)
+        if len(_SECTORS) >= 1024:
+            _SECTORS.clear()
+        _SECTORS[key] = hit
+    # a fresh Bond per load (bonds have in-place mutators); the validated fields are shared
+    b = Bond.__new__(Bond)
+    b.btype, (b.sectors, b.syms, b.dim), b._offsets = btype, hit, None
+    return b
 
 
 def _segments(blocks, itemsize, packed_to_slab):

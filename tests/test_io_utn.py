@@ -92,3 +92,29 @@ def test_lazily_permuted_blocks_are_materialised_on_save(cuda, tmp_path):
     s.save(g)
     with pytest.raises(ValueError, match="Qn indices"):
         UniTensor.load(g)
+
+
+@pytest.mark.gpu
+def test_truncated_payload_rejected(cuda, tmp_path):
+    raw = open(os.path.join(GOLD, "u1.utn"), "rb").read()
+    cut = tmp_path / "cut.utn"
+    cut.write_bytes(raw[:-9])
+    with pytest.raises(ValueError, match="truncated"):
+        tio.load_unitensor(cut)
+
+
+@pytest.mark.gpu
+def test_large_payload_multi_chunk(cuda, tmp_path, monkeypatch):
+    """Payload spanning several pinned chunk buffers, not a multiple of the chunk size:
+    the double-buffered read/copy pipeline reassembles it bit for bit."""
+    from paper_2401_01921_b200 import UniTensor, storage
+    monkeypatch.setattr(tio, "_CHUNK", 3 << 20)
+    saved = list(tio._PINNED)
+    tio._PINNED.clear()
+    arr = np.random.default_rng(5).standard_normal((1000, 1234))  # 9.9 MB
+    t = UniTensor(storage.from_numpy(arr), labels=["a", "b"], name="big")
+    p = tmp_path / "big.utn"
+    tio.save_unitensor(t, p)
+    back = tio.load_unitensor(p)
+    tio._PINNED[:] = saved
+    assert back.name == "big" and np.array_equal(back.get_block_().numpy(), arr)
