@@ -186,6 +186,12 @@ def permute(src_ptr, dst_ptr, elem_size, shape, perm, stream):
 _DENSE_ARGS = {}
 
 
+def dense_args(a_shape, a_perm, b_shape, b_perm, a_axes, b_axes):
+    """Marshalled descriptor arrays of a dense contraction: (keep-alive arrays, pointers)."""
+    arrs = [_arr64(a_shape), _arr32(a_perm), _arr64(b_shape), _arr32(b_perm), _arr32(a_axes), _arr32(b_axes)]
+    return arrs, [p for _, p in arrs]
+
+
 def contract_dense(a_ptr, a_dt, a_shape, a_perm, b_ptr, b_dt, b_shape, b_perm,
                    a_axes, b_axes, out_ptr, cplx_mode, stream, out_ld=0):
     # the integer descriptor arrays of a contraction shape are marshalled once and reused
@@ -193,8 +199,7 @@ def contract_dense(a_ptr, a_dt, a_shape, a_perm, b_ptr, b_dt, b_shape, b_perm,
     key = (tuple(a_shape), tuple(a_perm), tuple(b_shape), tuple(b_perm), tuple(a_axes), tuple(b_axes))
     args = _DENSE_ARGS.get(key)
     if args is None:
-        arrs = [_arr64(a_shape), _arr32(a_perm), _arr64(b_shape), _arr32(b_perm), _arr32(a_axes), _arr32(b_axes)]
-        args = (arrs, [p for _, p in arrs])
+        args = dense_args(a_shape, a_perm, b_shape, b_perm, a_axes, b_axes)
         if len(_DENSE_ARGS) >= 4096:
             _DENSE_ARGS.clear()
         _DENSE_ARGS[key] = args

@@ -159,9 +159,16 @@ def _contract_dense(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds):
         _lib.contract_dense(A.data_ptr, dense.dtype_code(A.dtype), A.storage_shape, A.perm,
                             B.data_ptr, dense.dtype_code(B.dtype), B.storage_shape, B.perm,
                             a_pos, b_pos, out.data_ptr, _CPLX_MODE, dense.stream_handle())
+        if _RECORD is not None:
+            _RECORD.append((A, B, tuple(a_pos), tuple(b_pos), tuple(out_shape), dt, out,
+                            out_bonds, out_labels, len(a_free)))
     if not out_shape:
         return UniTensor.scalar(out)
     return UniTensor._assemble(out_bonds, out_labels, len(a_free), "", [out], None)
+
+
+# set (to a list) by Network.launch while it records a dense launch program
+_RECORD = None
 
 
 def _contract_dense_panels(A, B, a_pos, b_pos, b_free, out, chunks):

@@ -217,3 +217,55 @@ def test_upload_chunk_sizes(cuda):
     assert np.array_equal(t.numpy(), arr)
     with pytest.raises(ValueError):
         t.upload_(torch.from_numpy(arr).pin_memory(), chunks=(1, 0))
+
+
+def test_launch_replay_program_matches_and_tracks_changes(cuda, monkeypatch):
+    """Repeated dense launches replay the recorded steps (no order search, no validation
+    pass, no per-step Python layout work) while the bindings keep their signature; any
+    change -- in-place permute of a bound tensor, rebinding, relabelling, order change --
+    falls back to the full launch and re-records. Results equal the oracle each time."""
+    from paper_2401_01921_b200 import blueprint
+    inp = oracle.lawr_inputs(24, seed=5)
+    want, _ = oracle.launch(oracle.lawr_slots(), "b, q, b2", inp)
+    net = Network(oracle.LAWR_NET)
+    ts = {}
+    for nm, arr in inp.items():
+        t = UniTensor(storage.from_numpy(arr), labels=[f"{nm}{i}" for i in range(arr.ndim)])
+        net.put_tensor(nm, t, t.labels)
+        ts[nm] = t
+    net.set_order(optimal=True)
+    first = net.launch()
+    assert net._program is not None
+    calls = []
+    real = blueprint._execute
+    monkeypatch.setattr(blueprint, "_execute", lambda *a: calls.append(1) or real(*a))
+    for _ in range(3):
+        out = net.launch()
+        assert rel_fro(out.numpy(), want) <= 1e-12
+        assert out.labels == first.labels and out.rowrank == first.rowrank and out.shape == first.shape
+    assert not calls, "replay expected"
+    assert net.get_order() == "(((A,L),W),R)"
+    # in-place permute of a bound tensor (storage unchanged, logical axes swapped back by the binding order)
+    L = ts["L"]
+    L2 = UniTensor(storage.from_numpy(np.ascontiguousarray(inp["L"].transpose(2, 1, 0))), labels=["L2", "L1", "L0"])
+    net.put_tensor("L", L2, ["L0", "L1", "L2"])
+    out = net.launch()
+    assert calls and rel_fro(out.numpy(), want) <= 1e-12
+    calls.clear()
+    out = net.launch()
+    assert not calls and rel_fro(out.numpy(), want) <= 1e-12
+    # mutate a bound tensor in place: A's block permuted lazily in place -> signature changes
+    A = ts["A"]
+    A.permute_([2, 1, 0])
+    out = net.launch()  # binding order names the labels, so the result is unchanged
+    assert calls and rel_fro(out.numpy(), want) <= 1e-12
+    # a different dtype on rebinding: complex W
+    calls.clear()
+    Wc = UniTensor(storage.from_numpy(inp["W"].astype(np.complex128) * (1 + 1j)),
+                   labels=[f"W{i}" for i in range(4)])
+    net.put_tensor("W", Wc, Wc.labels)
+    out = net.launch()
+    assert calls and rel_fro(out.numpy(), want * (1 + 1j)) <= 1e-12
+    calls.clear()
+    out = net.launch()
+    assert not calls and rel_fro(out.numpy(), want * (1 + 1j)) <= 1e-12
