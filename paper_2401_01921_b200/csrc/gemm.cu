@@ -406,6 +406,12 @@ struct Operand {
   std::vector<int64_t> ldim, lstride;  // logical
 };
 
+double prod_dims(const Operand& o) {
+  double p = 1;
+  for (auto x : o.ldim) p *= (double)x;
+  return p;
+}
+
 int make_operand(int rank, const int64_t* shape, const int32_t* perm, Operand& o) {
   if (rank < 0 || rank > TNB_MAX_RANK) return fail(TNB_EINVAL, "contract: rank out of range");
   std::vector<int64_t> ss(rank, 1);
@@ -787,10 +793,18 @@ int contract_dense_device(const void* a, int dta, int ra, const int64_t* sa, con
   const bool a_kfast = !(!rowA.empty() && rowA.back().stride == 1 && rowA.back().dim >= 4);
   const bool b_kfast = !(!colB.empty() && colB.back().stride == 1 && colB.back().dim >= 4);
   const bool k_memorder = a_kfast != b_kfast && ka_raw.size() > 1;
-  if (k_memorder) {
+  // Both operands gathered along K: walk K in the LARGER operand's memory order. Its
+  // sectors are then consumed whole within a k-tile; the smaller one's partly used
+  // sectors are revisited by the next k-tiles while still in L2. (T2.R of L.A.W.R: the
+  // 84 MB T2 holds (w2, q) pairs 16 B apart; walking w2 outermost used half of each 32 B
+  // sector per pass and read T2 from DRAM ~6x -- 559 MB per launch; in T2's order 136 MB.)
+  const bool both_gathered = a_kfast && b_kfast && ka_raw.size() > 1;
+  if (k_memorder || both_gathered) {
     std::vector<size_t> idx(ka_raw.size());
     for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
-    const std::vector<Digit>& key = a_kfast ? ka_raw : kb_raw;
+    bool by_a = a_kfast;
+    if (both_gathered) by_a = A.ldim.size() && B.ldim.size() ? prod_dims(A) >= prod_dims(B) : true;
+    const std::vector<Digit>& key = by_a ? ka_raw : kb_raw;
     std::stable_sort(idx.begin(), idx.end(), [&](size_t x, size_t y) { return key[x].stride > key[y].stride; });
     std::vector<Digit> ka2, kb2;
     for (size_t i : idx) {
@@ -818,7 +832,7 @@ int contract_dense_device(const void* a, int dta, int ra, const int64_t* sa, con
   // the one k-gathered operand (its smallest-stride digit innermost: coalescing beats
   // the cheaper affine address path; e.g. the PEPS a* step, innermost dn at stride 2
   // interleaved with the free s axis of the same rows).
-  const bool keep_order = k_memorder;
+  const bool keep_order = k_memorder || both_gathered;
   if (kA.size() > 1 && !keep_order) {
     int best = -1;
     int64_t best_score = -1;
@@ -860,6 +874,15 @@ int contract_dense_device(const void* a, int dta, int ra, const int64_t* sa, con
     d.kaff.ok = (d.kA.dim[d.kA.n - 1] % 32 == 0) ? 2 : 1;  // k-tiles of 16 (or 32) stay affine
     d.kaff.ksA = d.kA.stride[d.kA.n - 1];
     d.kaff.ksB = d.kB.stride[d.kB.n - 1];
+  } else if (d.kA.n == 2 && d.kA.dim[1] <= 16) {
+    // two K digits, the inner one not a multiple of 16: offsets are periodic in k
+    d.kaff.ok = 3;
+    d.kaff.D0 = d.kA.dim[1];
+    d.kaff.div0 = FastDiv((uint32_t)d.kA.dim[1]);
+    d.kaff.s1A = d.kA.stride[0];
+    d.kaff.s1B = d.kB.stride[0];
+    d.kaff.s0A = d.kA.stride[1];
+    d.kaff.s0B = d.kB.stride[1];
   }
   if (out_ld != 0 && (out_ld < N || out_ld >= (1ll << 31))) {
     if (tmp) cudaFreeAsync(tmp, st);

@@ -336,8 +336,13 @@ __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sy
 // the innermost contracted digit has extent divisible by BK (the host orders the K
 // digits so that this holds whenever possible).
 struct KAffine {
-  int ok;              // 1: affine k-tiles for both operands
+  int ok;              // 1/2: affine k-tiles (16 / 32 wide) for both operands; 3: periodic (below)
   int64_t ksA, ksB;    // strides of the innermost K digit
+  // ok == 3: K = (outer digit) x (inner digit of D0 < 16 or not a multiple of 16):
+  // offset(k) = (k / D0) * s1 + (k % D0) * s0 -- k-tiles need no offset table
+  int D0;
+  FastDiv div0;
+  int64_t s1A, s1B, s0A, s0B;
 };
 
 template <bool CPLX, int MODE, int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int REG_MATH,
@@ -407,7 +412,7 @@ struct TileCoreWS {
       };
       // affine fast path: per-element offsets rowOff + kk*ks live in registers for the
       // whole tile; per k-tile one group_offset per operand and one 64-bit add per element
-      const bool all_affine = kaff.ok && ((kend - kbeg) % BK == 0);
+      const bool all_affine = (kaff.ok == 1 || kaff.ok == 2) && ((kend - kbeg) % BK == 0);
       if (all_affine) {
         // distinct rows / cols touched by this thread (compile-time structure of the
         // mapping): M-fast -> one row, K-fast -> 4 rows (one per i % 4)

@@ -70,8 +70,9 @@ struct SKCore {
   static constexpr int NACC = CPLX ? (MODE == 1 ? 3 : 2) : 1;
   static constexpr int ACCN = NACC * MF * NF * 2;
   static constexpr int EA = (BM * BK) / NPROD, EB = (BN * BK) / NPROD;
+  static constexpr int kMaxPeriod = 16;  // periodic-K offset tables: D0 <= 16 phases
   static constexpr size_t kSmem = (size_t)STAGES * BK * (LDA + LDB) * ES + (size_t)(BM + BN) * 8 +
-                                  (size_t)2 * 2 * BK * 8 + (size_t)2 * STAGES * 8;
+                                  (size_t)2 * 2 * BK * 8 + (size_t)2 * STAGES * 8 + (size_t)2 * kMaxPeriod * BK * 8;
   static_assert(NMATH % 128 == 0, "math warps must form whole warpgroups");
   static_assert((BM * BK) % NPROD == 0 && (BN * BK) % NPROD == 0, "tile/producer mismatch");
   using Acc = typename Base::Acc;
@@ -212,6 +213,8 @@ struct SKCore {
     int64_t* kOffB = kOffA + 2 * BK;  // [2][BK]
     uint64_t* full = reinterpret_cast<uint64_t*>(kOffB + 2 * BK);
     uint64_t* empty = full + STAGES;
+    int64_t* perA = reinterpret_cast<int64_t*>(empty + STAGES);  // [D0][BK] periodic-K offsets
+    int64_t* perB = perA + kMaxPeriod * BK;
     const int tid = threadIdx.x;
     const int c = blockIdx.x;
     const int64_t it0 = detail::sk_begin(sk.total, sk.G, c), it1 = detail::sk_begin(sk.total, sk.G, c + 1);
@@ -241,6 +244,16 @@ struct SKCore {
       const uint32_t sAbase = smem_u32(As), sBbase = smem_u32(Bs);
       constexpr uint32_t stA = BK * LDA * ES, stB = BK * LDB * ES;
       uint32_t gi = 0;  // stage counter (per CTA < 2^32)
+      if (d.kaff.ok == 3) {
+        // periodic K (two digits, inner width D0): offset(k0 + kk) = (k0 / D0) * s1 + per[k0 % D0][kk]
+        const int D0 = d.kaff.D0;
+        for (int x = p; x < D0 * BK; x += NPROD) {
+          const int r = x / BK, kk = x - r * BK, t = r + kk, q = t / D0, rr = t - q * D0;
+          perA[x] = (int64_t)q * d.kaff.s1A + (int64_t)rr * d.kaff.s0A;
+          perB[x] = (int64_t)q * d.kaff.s1B + (int64_t)rr * d.kaff.s0B;
+        }
+        detail::named_sync(1, NPROD);
+      }
       // segments in REVERSE range order: a CTA first publishes the partial of the tile it
       // shares with its successor and finishes (as owner) the tile it shares with its
       // predecessor last, so no CTA waits on one that is still early in its range
@@ -272,7 +285,42 @@ struct SKCore {
         for (int kt = kt0; kt < kt1; ++kt, ++gi) {
           const int s = (int)(gi % STAGES);
           const int k0 = kt * BK;
-          if (d.kaff.ok >= (BK + 15) / 16 && k0 + BK <= d.K) {
+          if (d.kaff.ok == 3 && k0 + BK <= d.K) {
+            // periodic K: two digits, the inner one not a multiple of 16 wide
+            const uint32_t q0 = d.kaff.div0.div((uint32_t)k0);
+            const int r0 = k0 - (int)q0 * d.kaff.D0;
+            const T* pa = A + (int64_t)q0 * d.kaff.s1A;
+            const T* pb = B + (int64_t)q0 * d.kaff.s1B;
+            const int64_t* pra = perA + r0 * BK;
+            const int64_t* prb = perB + r0 * BK;
+            if (gi >= STAGES) detail::mbar_wait(&empty[s], (uint32_t)(((gi / STAGES) & 1) ^ 1));
+#pragma unroll
+            for (int i = 0; i < EA; ++i) {
+              int m, kk;
+              mapA(i, m, kk);
+              const int64_t ro = rA[i % RA];
+              const bool v = ro >= 0;
+              const T* src = v ? pa + ro + pra[kk] : A;
+              const uint32_t dst = sAbase + s * stA + (uint32_t)(kk * LDA + m) * ES;
+              if constexpr (CPLX)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
+              else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0));
+            }
+#pragma unroll
+            for (int i = 0; i < EB; ++i) {
+              int n, kk;
+              mapB(i, n, kk);
+              const int64_t co = rB[i % RB];
+              const bool v = co >= 0;
+              const T* src = v ? pb + co + prb[kk] : B;
+              const uint32_t dst = sBbase + s * stB + (uint32_t)(kk * LDB + n) * ES;
+              if constexpr (CPLX)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
+              else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0));
+            }
+          } else if (d.kaff.ok >= 1 && d.kaff.ok <= 2 && d.kaff.ok >= (BK + 15) / 16 && k0 + BK <= d.K) {
             const T* pa = A + group_offset(d.kA, k0);
             const T* pb = B + group_offset(d.kB, k0);
             if (gi >= STAGES) detail::mbar_wait(&empty[s], (uint32_t)(((gi / STAGES) & 1) ^ 1));
