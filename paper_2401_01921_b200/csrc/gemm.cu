@@ -22,6 +22,7 @@
 // L.A.W.R) go to a separate memory-bound kernel.
 #include <algorithm>
 #include <cstdlib>
+#include <cstdint>
 #include <mutex>
 #include <cstring>
 #include <vector>
@@ -602,10 +603,29 @@ struct StreamK {
     if (d.b_nfast) return launch_one<false, true>(A, B, C, d, sk, st);
     return launch_one<false, false>(A, B, C, d, sk, st);
   }
+  // Whole BM-row (BN-col) tiles of this operand are one contiguous 16-byte aligned run per
+  // k: the innermost free digit is unit-stride and a multiple of the tile, and every other
+  // free / contracted stride and the base keep 16-byte alignment.
+  static bool bulk_ok(const void* X, const Group& free, const Group& k, int tile, bool fast) {
+    constexpr int ES = CPLX ? 16 : 8;
+    if (!fast || free.n < 1 || free.stride[free.n - 1] != 1 || free.dim[free.n - 1] % tile) return false;
+    if (reinterpret_cast<uintptr_t>(X) % 16) return false;
+    for (int q = 0; q < free.n; ++q)
+      if ((free.stride[q] * ES) % 16) return false;
+    for (int q = 0; q < k.n; ++q)
+      if ((k.stride[q] * ES) % 16) return false;
+    return true;
+  }
   static int run(const void* A, const void* B, void* C, GemmDesc d, cudaStream_t st) {
     d.tiles_m = (d.M + BM - 1) / BM;
     d.tiles_n = (d.N + BN - 1) / BN;
     d.splitk = 1;
+    {
+      static const bool nobulk = getenv("TNB_NO_BULK") != nullptr;  // A/B switch for measurements
+      const bool kfast_path = (d.kaff.ok >= 1 && d.kaff.ok <= 2 && d.kaff.ok >= (BK + 15) / 16) || d.kaff.ok == 3;
+      d.bulkA = !nobulk && kfast_path && bulk_ok(A, d.rowA, d.kA, BM, d.a_mfast);
+      d.bulkB = !nobulk && kfast_path && bulk_ok(B, d.colB, d.kB, BN, d.b_nfast);
+    }
     SKParams sk;
     sk.KT = (d.K + BK - 1) / BK;
     sk.total = (int64_t)d.tiles_m * d.tiles_n * sk.KT;

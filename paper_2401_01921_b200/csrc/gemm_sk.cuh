@@ -24,6 +24,9 @@ struct GemmDesc {
   int k_per_split;
   int a_mfast, b_nfast;
   int out_ld;
+  // 1: every BM-row tile of A (BN-col tile of B) is one contiguous, 16-byte aligned run per
+  // k: whole k-rows of the tile move by bulk copies instead of per-element cp.async
+  int bulkA, bulkB;
   KAffine kaff;
   Group rowA, kA, kB, colB;
 };
@@ -202,6 +205,30 @@ struct SKCore {
     }
   }
 
+  // Producer warp 0: the k-rows of a stage whose tile is contiguous per k go by bulk copy
+  // (TMA engine; one copy per k-row: A rows by lanes 0..BK-1, B rows by lanes 16..16+BK-1),
+  // completing as transaction bytes on full[s]. The k offset of row kk is per[kk] (periodic
+  // K) or kk * ks (affine K).
+  __device__ __forceinline__ static void bulk_rows(const GemmDesc& d, int s, const T* pa, const T* pb,
+                                                   const int64_t* rowOffA, const int64_t* colOffB, const int64_t* pra,
+                                                   const int64_t* prb, int64_t ksA, int64_t ksB, uint64_t* full,
+                                                   uint32_t sAbase, uint32_t sBbase) {
+    const int p = threadIdx.x - NMATH;
+    if (p >= 32) return;
+    constexpr uint32_t stA = BK * LDA * ES, stB = BK * LDB * ES;
+    if (p == 0)
+      detail::mbar_expect_tx(&full[s], (uint32_t)((d.bulkA ? BK * BM * ES : 0) + (d.bulkB ? BK * BN * ES : 0)));
+    __syncwarp();
+    if (d.bulkA && p < BK) {
+      const T* src = pa + rowOffA[0] + (pra ? pra[p] : (int64_t)p * ksA);
+      detail::bulk_load(sAbase + s * stA + (uint32_t)(p * LDA) * ES, src, BM * ES, &full[s]);
+    }
+    if (d.bulkB && p >= 16 && p < 16 + BK) {
+      const int kk = p - 16;
+      const T* src = pb + colOffB[0] + (prb ? prb[kk] : (int64_t)kk * ksB);
+      detail::bulk_load(sBbase + s * stB + (uint32_t)(kk * LDB) * ES, src, BN * ES, &full[s]);
+    }
+  }
   template <bool AMF, bool BNF>
   __device__ static void run(unsigned char* smem, const T* __restrict__ A, const T* __restrict__ B,
                              T* __restrict__ C, const GemmDesc& d, const SKParams& sk) {
@@ -294,6 +321,8 @@ struct SKCore {
             const int64_t* pra = perA + r0 * BK;
             const int64_t* prb = perB + r0 * BK;
             if (gi >= STAGES) detail::mbar_wait(&empty[s], (uint32_t)(((gi / STAGES) & 1) ^ 1));
+            if (d.bulkA | d.bulkB) bulk_rows(d, s, pa, pb, rowOffA, colOffB, pra, prb, 0, 0, full, sAbase, sBbase);
+            if (!d.bulkA)
 #pragma unroll
             for (int i = 0; i < EA; ++i) {
               int m, kk;
@@ -307,6 +336,7 @@ struct SKCore {
               else
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0));
             }
+if (!d.bulkB)
 #pragma unroll
             for (int i = 0; i < EB; ++i) {
               int n, kk;
@@ -324,6 +354,9 @@ struct SKCore {
             const T* pa = A + group_offset(d.kA, k0);
             const T* pb = B + group_offset(d.kB, k0);
             if (gi >= STAGES) detail::mbar_wait(&empty[s], (uint32_t)(((gi / STAGES) & 1) ^ 1));
+            if (d.bulkA | d.bulkB)
+              bulk_rows(d, s, pa, pb, rowOffA, colOffB, nullptr, nullptr, d.kaff.ksA, d.kaff.ksB, full, sAbase, sBbase);
+            if (!d.bulkA)
 #pragma unroll
             for (int i = 0; i < EA; ++i) {
               int m, kk;
@@ -337,6 +370,7 @@ struct SKCore {
               else
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0));
             }
+if (!d.bulkB)
 #pragma unroll
             for (int i = 0; i < EB; ++i) {
               int n, kk;
