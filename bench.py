@@ -402,14 +402,28 @@ def gpu_c4_batch(tnb, n_total, steps, warmup, flush, dist):
     mine = [i for i in range(n_total) if i % dist.world == dist.rank]
     pairs = [c4_tensors(tnb, seed=777 + 2 * i) for i in mine]
 
-    def step():
+    def step():  # one grouped launch over the output tiles of all of this rank's contractions
+        tnb.contract_batched(pairs)
+
+    def step_pairwise():
         for A, E in pairs:
             tnb.contract(A, E)
     for _ in range(warmup):
         step()
+        step_pairwise()
     ms = time_steps(step, steps, flush, dist) / steps
+    ms_pw = time_steps(step_pairwise, steps, flush, dist) / steps
+    tnb._lib.ktimer_reset()
+    tnb._lib.ktimer_enable(True)
+    time_steps(step, steps, flush, dist)
+    tnb._lib.ktimer_enable(False)
+    n_k, ms_k, _ = tnb._lib.ktimer_read(tnb._lib.KF_BS_GEMM)
+    tnb._lib.ktimer_reset()
+    kms = dist.max(ms_k / max(steps, 1))
     return {"ms_per_step": ms, "instances": n_total, "per_rank": len(mine),
-            "gflops": 2 * C4_MACS * n_total / ms / 1e6}
+            "gflops": 2 * C4_MACS * n_total / ms / 1e6, "api": "contract_batched (tnb_bs_execute_batched)",
+            "bs_gemm_kernel_ms": kms, "bs_gemm_kernel_tflops": 2 * C4_MACS * len(mine) / kms / 1e9 if kms else 0.0,
+            "ms_per_step_pairwise": ms_pw, "gflops_pairwise": 2 * C4_MACS * n_total / ms_pw / 1e6}
 
 
 def gpu_lawr_batch(tnb, n_total, chi, dtype, steps, warmup, flush, dist):
@@ -763,7 +777,11 @@ def main():
         def w_c4b():
             cb = gpu_c4_batch(tnb, 64, max(3, args.steps // 2), args.warmup, flush, dist)
             return {"value": round(cb["gflops"], 2), "unit": "GFLOP/s",
-                    "scaling": "strong (64 contractions sharded over ranks)", **cb}
+                    "scaling": "strong (64 contractions sharded over ranks)", **cb,
+                    "roofline": {"bound": "tensor", "achieved": round(cb["bs_gemm_kernel_tflops"], 3),
+                                 "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                 "frac": round(cb["bs_gemm_kernel_tflops"] / FP64_PEAK_TFLOPS, 4),
+                                 "kernel": "bs_sk_kernel, batched (one launch per rank)", "peak_source": PEAK_SOURCE}}
 
         def w_c3b():
             bt = gpu_lawr_batch(tnb, 64, 512, np.complex128, max(2, args.steps // 4), 1, flush, dist)

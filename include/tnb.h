@@ -246,6 +246,14 @@ int tnb_bs_execute(int64_t plan_id, const void* const* a_ptrs, const void* const
                    void* const* out_ptrs, void* stream);
 int tnb_bs_plan_pairs(int64_t plan_id, int64_t max_pairs, int32_t* pairs_out, int64_t* npairs,
                       void* stream);
+/* nbatch independent contractions of ONE plan's structure (e.g. the equal-structure
+ * sites of a sweep) in one grouped stream-K launch over all their output tiles:
+ * a_ptrs[nbatch][na], b_ptrs[nbatch][nb], out_ptrs[nbatch][nout] (row-major). Each
+ * contraction's result is the one tnb_bs_execute gives (same per-tile pair order). Not
+ * for panel-masked plans (TNB_EUNSUP). No reference counterpart: contract.py:137-167
+ * runs one pair at a time; this is the batched form of the same arithmetic. */
+int tnb_bs_execute_batched(int64_t plan_id, int64_t nbatch, const void* const* a_ptrs,
+                           const void* const* b_ptrs, void* const* out_ptrs, void* stream);
 
 /* ---- a14: optimal contraction order DP (contract.py:271-343), host only ---
  * n tensors (n <= 16). Labels are interned to ints: nlab[t] labels for tensor

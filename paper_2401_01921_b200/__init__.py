@@ -16,7 +16,7 @@ from . import dense as storage
 from ._lib import EngineError, EngineUnavailable
 from .blueprint import Network
 from .charges import IN, OUT, REGULAR, Bond, BondType, Symmetry
-from .contraction import (block_pairs, brute_force_order, contract, contract_pair, contraction_cost,
+from .contraction import (block_pairs, brute_force_order, contract, contract_batched, contract_pair, contraction_cost,
                           execute_tree, find_optimal_order, get_complex_mode, parse_order, render_order,
                           set_complex_mode, tree_leaves)
 from .dense import (Bool, Complex128, DenseTensor, Float64, Int64, arange, eye, from_numpy, kron, normal, ones,
@@ -33,7 +33,7 @@ __all__ = [
     "load_unitensor", "save_unitensor",
     "Bond", "BondType", "IN", "OUT", "REGULAR", "Bool", "Complex128", "DenseTensor", "ElementProxy", "Float64",
     "Int64", "Network", "Symmetry", "UniTensor", "EngineError", "EngineUnavailable", "arange", "block_pairs",
-    "brute_force_order", "contract", "Contract", "contract_pair", "contraction_cost", "execute_tree", "eye",
+    "brute_force_order", "contract", "Contract", "contract_batched", "contract_pair", "contraction_cost", "execute_tree", "eye",
     "find_optimal_order", "from_numpy", "get_complex_mode", "kron", "normal", "ones", "parse_order", "random",
     "render_order", "set_complex_mode", "storage", "tree_leaves", "uniform", "zeros", "eig", "graphs", "parallel", "workloads",
 ]

@@ -22,7 +22,7 @@ EXPORTS = (
     "tnb_synchronize", "tnb_memcpy2d_async", "tnb_permute", "tnb_contract_dense", "tnb_contract_dense_ld",
     "tnb_zero_flux_blocks", "tnb_bs_contract", "tnb_bs_contract_masked", "tnb_optimal_order",
     "tnb_ktimer_enable", "tnb_ktimer_reset", "tnb_ktimer_read",
-    "tnb_bs_plan", "tnb_bs_execute", "tnb_bs_plan_pairs", "tnb_copy2d_batched", "tnb_svd_jacobi_batched",
+    "tnb_bs_plan", "tnb_bs_execute", "tnb_bs_execute_batched", "tnb_bs_plan_pairs", "tnb_copy2d_batched", "tnb_svd_jacobi_batched",
 )
 
 # kernel families of the kernel timer (TNB_KF_* in include/tnb.h)
@@ -83,6 +83,7 @@ def _declare(lib):
                          _pi32, _pi64, _pi32, _pi32, _pi64, _pi32,
                          ctypes.c_int, _pi32, _pi32, _pi32, _pi64, _i64, _p, _pi64, _pi64, _p], ctypes.c_int),
         "tnb_bs_execute": ([_i64, _p, _p, _p, _p], ctypes.c_int),
+        "tnb_bs_execute_batched": ([_i64, _i64, _p, _p, _p, _p], ctypes.c_int),
         "tnb_bs_plan_pairs": ([_i64, _i64, _pi32, _pi64, _p], ctypes.c_int),
         "tnb_copy2d_batched": ([_p, _p, _i64, _p, _p], ctypes.c_int),
         "tnb_svd_jacobi_batched": ([ctypes.c_int, ctypes.c_int, _p, ctypes.c_int, ctypes.c_double,
@@ -298,6 +299,21 @@ class BsPlan:
         if rc == TNB_EINVAL and "stale" in last_error():
             return False
         check(rc, "bs_execute")
+        return True
+
+    def execute_batched(self, a_ptrs, b_ptrs, out_ptrs, stream):
+        """nbatch contractions of this structure in one launch; a_ptrs is [nbatch][na] etc.
+        (nested sequences of device addresses). Returns False if the plan went stale."""
+        nbatch = len(out_ptrs)
+        a = np.ascontiguousarray(np.asarray(a_ptrs, dtype=np.uint64).reshape(nbatch, self.na))
+        b = np.ascontiguousarray(np.asarray(b_ptrs, dtype=np.uint64).reshape(nbatch, self.nb))
+        o = np.ascontiguousarray(np.asarray(out_ptrs, dtype=np.uint64).reshape(nbatch, self.nout))
+        vp = ctypes.c_void_p
+        rc = lib().tnb_bs_execute_batched(self.id, nbatch, a.ctypes.data_as(vp), b.ctypes.data_as(vp),
+                                          o.ctypes.data_as(vp), stream)
+        if rc == TNB_EINVAL and "stale" in last_error():
+            return False
+        check(rc, "bs_execute_batched")
         return True
 
     def pairs(self, stream):

@@ -229,6 +229,10 @@ def _common_perm(t):
 
 
 def _widen(blocks, dt):
+    if blocks:
+        o = blocks[0]._slab
+        if o is not None and dense._NP_OF_TORCH[o.dtype] == dt and all(b._slab is o for b in blocks):
+            return blocks  # one slab of the target dtype: nothing to widen
     return [b if b.dtype == dt else b.astype(dt) for b in blocks]
 
 
@@ -249,7 +253,7 @@ def _contract_blocks(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds, 
     # every output block is fully written by the kernel (with a panel mask: the panels
     # of this rank; parallel.gather_panels fills the rest)
     oblk, _ = _slab_blocks(shapes, dt, zero=False)
-    aptrs, bptrs, optrs = [x.data_ptr for x in ablk], [x.data_ptr for x in bblk], [x.data_ptr for x in oblk]
+    aptrs, bptrs, optrs = dense.block_ptrs(ablk), dense.block_ptrs(bblk), [x._p0 for x in oblk]
     if not plan.execute(aptrs, bptrs, optrs, dense.stream_handle()):
         _BS_PLANS.clear()  # the library flushed its plan cache: re-plan this structure
         plan, _ = _bs_plan(dt, a, ablk, aperm, b, bblk, bperm, a_pos, b_pos, out_bonds, qns, panel_mask)
@@ -272,13 +276,73 @@ def _bs_plan(dt, a, ablk, aperm, b, bblk, bperm, a_pos, b_pos, out_bonds, qns, p
     hit = _BS_PLANS.get(key)
     if hit is not None:
         return hit
-    shapes = [tuple(x.sectors[k][1] for x, k in zip(out_bonds, qn)) for qn in qns]
+    shapes = tuple(tuple(x.sectors[k][1] for x, k in zip(out_bonds, qn)) for qn in qns)
     plan = _lib.bs_plan(dense.dtype_code(dt), a._qns, list(a_sh), aperm, b._qns, list(b_sh), bperm, a_pos, b_pos,
                         qns, shapes, dense.stream_handle(), panel_mask=panel_mask)
     if len(_BS_PLANS) >= 512:
         _BS_PLANS.clear()
     _BS_PLANS[key] = (plan, shapes)
     return plan, shapes
+
+
+def contract_batched(pairs):
+    """``[contract_pair(a, b) for a, b in pairs]`` for block-sparse pairs that share ONE block
+    structure (same labels, qn tuples, block shapes, storage perms, dtypes: e.g. the
+    equal-structure sites of a sweep), as ONE grouped stream-K launch over the output tiles
+    of all of them (``tnb_bs_execute_batched``); each result equals the single-pair
+    contraction (same per-tile pair order). Dense pairs, scalar results and mixed
+    structures are contracted pair by pair (mixed structures raise ValueError). The
+    reference has no batched call; this is the batched form of contract.py:137-167."""
+    pairs = [tuple(p) for p in pairs]
+    if not pairs:
+        return []
+    for p in pairs:
+        if len(p) != 2 or not isinstance(p[0], UniTensor) or not isinstance(p[1], UniTensor):
+            raise TypeError("contract_batched expects (UniTensor, UniTensor) pairs")
+    a0, b0 = pairs[0]
+    if not (a0.is_sym and b0.is_sym) or len(pairs) == 1:
+        return [contract_pair(a, b) for a, b in pairs]
+    a_pos, b_pos, a_free, b_free, out_labels, out_bonds = _pair_layout(a0, b0)
+    if not out_bonds:
+        return [contract_pair(a, b) for a, b in pairs]
+    dt = _result_dtype(a0.dtype, b0.dtype)
+    from .labeled import _slab_blocks, zero_flux_combos
+    if not all(x.syms == out_bonds[0].syms for x in out_bonds):
+        raise ValueError("all bonds must carry the same symmetries")
+    qns = zero_flux_combos(out_bonds)
+    if not qns:
+        raise ValueError("no valid blocks: no combination of these bonds' sectors has zero flux")
+
+    def structure(a, b):
+        ablk, aperm = _common_perm(a)
+        bblk, bperm = _common_perm(b)
+        sig = (a.dtype, b.dtype, tuple(a._qns), tuple(b._qns), tuple(x.storage_shape for x in ablk),
+               tuple(x.storage_shape for x in bblk), tuple(aperm), tuple(bperm))
+        return sig, _widen(ablk, dt), aperm, _widen(bblk, dt), bperm
+
+    sig0, ablk0, aperm, bblk0, bperm = structure(a0, b0)
+    plan, shapes = _bs_plan(dt, a0, ablk0, aperm, b0, bblk0, bperm, a_pos, b_pos, out_bonds, qns)
+    aps, bps, ops, outs = [], [], [], []
+    for k, (a, b) in enumerate(pairs):
+        if k == 0:
+            ablk, bblk, lay = ablk0, bblk0, (a_pos, b_pos, a_free, b_free, out_labels, out_bonds)
+        else:
+            lay = _pair_layout(a, b)  # the reference's checks, per pair, before any arithmetic
+            sig, ablk, _, bblk, _ = structure(a, b)
+            if (sig != sig0 or lay[0] != a_pos or lay[1] != b_pos or lay[4] != out_labels
+                    or lay[5] != out_bonds):
+                raise ValueError(f"contract_batched: pair {k} does not share the block structure of pair 0")
+        oblk, _ = _slab_blocks(shapes, dt, zero=False)
+        aps.append(dense.block_ptrs(ablk))
+        bps.append(dense.block_ptrs(bblk))
+        ops.append([x._p0 for x in oblk])
+        outs.append(UniTensor._assemble(lay[5], lay[4], len(lay[2]), "", oblk, qns))
+    if not plan.execute_batched(aps, bps, ops, dense.stream_handle()):
+        _BS_PLANS.clear()
+        plan, _ = _bs_plan(dt, a0, ablk0, aperm, b0, bblk0, bperm, a_pos, b_pos, out_bonds, qns)
+        if not plan.execute_batched(aps, bps, ops, dense.stream_handle()):
+            raise _lib.EngineError("block-sparse plan went stale twice")
+    return outs
 
 
 def block_pairs(a, b):

@@ -84,6 +84,9 @@ struct BsMeta {
   // the schedule tables (tile_kbeg, stiles, out_ptr, pairs, out_M, out_N) and then da, db lie
   // back to back in the blob in exactly the shared-memory layout: one flat uint4 copy stages them
   const uint4* img;
+  // batched execute: nbatch contractions of this structure in one launch (tile space
+  // nbatch x ntiles; pointer table [nbatch][na + nb + nout] in device memory)
+  int nbatch;
 };
 
 // Schedule tables the grouped GEMM reads on every segment / pair switch (dependent
@@ -387,7 +390,9 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
     oN = s_oN;
   }
   __syncthreads();
-  const int64_t total = kbeg[m.ntiles];
+  const int64_t per = kbeg[m.ntiles];  // k-iterations of one contraction
+  const int64_t total = per * m.nbatch;
+  const int NPI = m.na + m.nb + m.nout;  // pointers per batch item
   // stream-K participants: >= 4 k-iterations each, so no participant has an empty range
   // (an owner waits on EVERY participant between a tile's first CTA and itself)
   const int G = (int)min((int64_t)gridDim.x, max(total / 4, (int64_t)1));
@@ -400,6 +405,12 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
     }
   }
   __syncthreads();
+  // batch item of a flattened k-iteration, and the item's first k-iteration
+  auto item_of = [&](int64_t x, int64_t& base) {
+    const int b = m.nbatch == 1 ? 0 : (int)(x / per);
+    base = (int64_t)b * per;
+    return b;
+  };
   // largest tile t with kbeg[t] <= x (skips empty tiles, whose kbeg equals the next one's)
   auto tile_of = [&](int64_t x) {
     int lo = 0, hi = m.ntiles - 1;
@@ -429,8 +440,11 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
     constexpr uint32_t stA = BK * LDA * ES, stB = BK * LDB * ES;
     uint32_t gi = 0;  // stage counter (per CTA < 2^32)
     for (int64_t e = it1; e > it0;) {
-      const int t = tile_of(e - 1);
-      const int64_t tstart = kbeg[t];
+      int64_t bbase;
+      const int bi = item_of(e - 1, bbase);
+      const void* const* bptrs = ptrs + (size_t)bi * NPI;
+      const int t = tile_of(e - 1 - bbase);
+      const int64_t tstart = bbase + kbeg[t];
       const int64_t sb = it0 > tstart ? it0 : tstart;
       const TileRef tr = tiles[t];
       const int M = oM[tr.o], N = oN[tr.o];
@@ -447,8 +461,8 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
           pbase += nkt;
           continue;
         }
-        const T* A = static_cast<const T*>(ptrs[i]);
-        const T* B = static_cast<const T*>(ptrs[m.na + j]);
+        const T* A = static_cast<const T*>(bptrs[i]);
+        const T* B = static_cast<const T*>(bptrs[m.na + j]);
         detail::named_sync(1, NPROD);  // previous pair's table reads are done
         for (int x = p; x < BM + BN; x += NPROD) {
           if (x < BM) rowOffA[x] = (tr.m0 + x < M) ? group_offset(da.free_g, tr.m0 + x) : -1;
@@ -603,12 +617,14 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
   typename Core::Acc acc;
   // tiles whose output block has no pair (or whose rank owns them but K is empty) are zeros
   Base::zero(acc);
-  for (int t = c; t < m.ntiles; t += gridDim.x) {
+  for (int bt = c; bt < m.ntiles * m.nbatch; bt += gridDim.x) {
+    const int bi = bt / m.ntiles, t = bt - bi * m.ntiles;
     if (kbeg[t + 1] != kbeg[t]) continue;
     const TileRef tr = tiles[t];
     if (m.mask && !m.mask[tr.panel]) continue;
     const int M = oM[tr.o], N = oN[tr.o];
-    Base::store(static_cast<T*>(const_cast<void*>(ptrs[m.na + m.nb + tr.o])), N, tr.m0, tr.n0, M, N, acc);
+    Base::store(static_cast<T*>(const_cast<void*>(ptrs[(size_t)bi * NPI + m.na + m.nb + tr.o])), N, tr.m0, tr.n0, M, N,
+                acc);
   }
   uint32_t gi = 0;
   long long* tr_ = (sk.trace && tid == 0) ? sk.trace + (size_t)c * kTraceW : nullptr;
@@ -618,8 +634,10 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
     tr_[kTraceW - 1] = t_entry;
   }
   for (int64_t e = it1; e > it0;) {
-    const int t = tile_of(e - 1);
-    const int64_t tstart = kbeg[t], tend = kbeg[t + 1];
+    int64_t bbase;
+    const int bi = item_of(e - 1, bbase);
+    const int t = tile_of(e - 1 - bbase);
+    const int64_t tstart = bbase + kbeg[t], tend = bbase + kbeg[t + 1];
     const int64_t sb = it0 > tstart ? it0 : tstart;
     Base::zero(acc);
     {
@@ -637,7 +655,8 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
       if (sb > tstart) Core::absorb(sk.ws, sk.flags, detail::sk_cta_of(total, G, tstart), c, acc, true);
       const TileRef tr = tiles[t];
       const int M = oM[tr.o], N = oN[tr.o];
-      Base::store(static_cast<T*>(const_cast<void*>(ptrs[m.na + m.nb + tr.o])), N, tr.m0, tr.n0, M, N, acc);
+      Base::store(static_cast<T*>(const_cast<void*>(ptrs[(size_t)bi * NPI + m.na + m.nb + tr.o])), N, tr.m0, tr.n0,
+                  M, N, acc);
     }
     if (tr_ && nseg < 14) {
       tr_[5 + 4 * nseg] = gtimer();
@@ -879,6 +898,7 @@ int bs_plan_locked(int dtype, int na, int nb, int nout, int rank_a, int rank_b, 
     plan.dtype = dtype;
     BsMeta& meta = plan.meta;
     memset(&meta, 0, sizeof(meta));
+    meta.nbatch = 1;
     meta.na = na;
     meta.nb = nb;
     meta.nout = nout;
@@ -1095,18 +1115,27 @@ Plan* plan_of(int64_t id) {
 
 // Caller holds g_cache.mu. One grouped GEMM launch with this call's data pointers.
 int bs_execute_locked(Plan& plan, const void* const* a_ptrs, const void* const* b_ptrs, void* const* out_ptrs,
-                      cudaStream_t st) {
+                      cudaStream_t st, int64_t nbatch = 1) {
   BsMeta meta = plan.meta;
   const int na = meta.na, nb = meta.nb, nout = meta.nout;
   int rc = TNB_OK;
-  // ---- per-call data pointers
-  const int nptr = na + nb + nout;
+  if (nbatch < 1) return fail(TNB_EINVAL, "bs_execute: nbatch must be >= 1");
+  if ((int64_t)meta.ntiles * nbatch >= (1ll << 31) ||
+      (int64_t)(meta.ntiles + 1) * nbatch * 1024 >= (1ll << 40))
+    return fail(TNB_EUNSUP, "bs_execute: batch too large");
+  meta.nbatch = (int)nbatch;
+  // ---- per-call data pointers ([nbatch][na + nb + nout])
+  const int nptr1 = na + nb + nout;
+  const int64_t nptr = (int64_t)nptr1 * nbatch;
   std::vector<const void*> hv;
   if (nptr <= kInlinePtrs) {
     hv.resize(nptr);
-    for (int i = 0; i < na; ++i) hv[i] = a_ptrs[i];
-    for (int j = 0; j < nb; ++j) hv[na + j] = b_ptrs[j];
-    for (int o = 0; o < nout; ++o) hv[na + nb + o] = out_ptrs[o];
+    for (int64_t q = 0; q < nbatch; ++q) {
+      const void** h = hv.data() + q * nptr1;
+      for (int i = 0; i < na; ++i) h[i] = a_ptrs[q * na + i];
+      for (int j = 0; j < nb; ++j) h[na + j] = b_ptrs[q * nb + j];
+      for (int o = 0; o < nout; ++o) h[na + nb + o] = out_ptrs[q * nout + o];
+    }
     meta.ptrs = nullptr;
   } else {
     if (g_cache.stage_ev) TNB_CUDA_CHECK(cudaEventSynchronize(g_cache.stage_ev));
@@ -1118,9 +1147,12 @@ int bs_execute_locked(Plan& plan, const void* const* a_ptrs, const void* const* 
     }
     if (!g_cache.stage_ev) TNB_CUDA_CHECK(cudaEventCreateWithFlags(&g_cache.stage_ev, cudaEventDisableTiming));
     const void** hp = static_cast<const void**>(g_cache.stage);
-    for (int i = 0; i < na; ++i) hp[i] = a_ptrs[i];
-    for (int j = 0; j < nb; ++j) hp[na + j] = b_ptrs[j];
-    for (int o = 0; o < nout; ++o) hp[na + nb + o] = out_ptrs[o];
+    for (int64_t q = 0; q < nbatch; ++q) {
+      const void** h = hp + q * nptr1;
+      for (int i = 0; i < na; ++i) h[i] = a_ptrs[q * na + i];
+      for (int j = 0; j < nb; ++j) h[na + j] = b_ptrs[q * nb + j];
+      for (int o = 0; o < nout; ++o) h[na + nb + o] = out_ptrs[q * nout + o];
+    }
     void* dptr = nullptr;
     TNB_CUDA_CHECK(cudaMallocAsync(&dptr, bytes, st));
     TNB_CUDA_CHECK(cudaMemcpyAsync(dptr, hp, bytes, cudaMemcpyHostToDevice, st));
@@ -1128,7 +1160,7 @@ int bs_execute_locked(Plan& plan, const void* const* a_ptrs, const void* const* 
     meta.ptrs = static_cast<const void* const*>(dptr);
   }
   const void* const* hp = meta.ptrs ? nullptr : hv.data();
-  const int nin = meta.ptrs ? 0 : nptr;
+  const int nin = meta.ptrs ? 0 : (int)nptr;
   if (plan.dtype == TNB_F64) rc = launch_bs<false, 0>(plan, meta, hp, nin, st);
   else rc = launch_bs<true, 0>(plan, meta, hp, nin, st);
   if (meta.ptrs) cudaFreeAsync(const_cast<void*>(static_cast<const void*>(meta.ptrs)), st);
@@ -1197,6 +1229,21 @@ extern "C" int tnb_bs_execute(int64_t plan_id, const void* const* a_ptrs, const 
   if ((plan->meta.na && !a_ptrs) || (plan->meta.nb && !b_ptrs) || !out_ptrs)
     return fail(TNB_EINVAL, "bs_execute: NULL pointer table");
   return bs_execute_locked(*plan, a_ptrs, b_ptrs, out_ptrs, (cudaStream_t)stream);
+}
+
+extern "C" int tnb_bs_execute_batched(int64_t plan_id, int64_t nbatch, const void* const* a_ptrs,
+                                      const void* const* b_ptrs, void* const* out_ptrs, void* stream) {
+  using namespace tnb;
+  int rc = require_device();
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(g_cache.mu);
+  Plan* plan = plan_of(plan_id);
+  if (!plan) return fail(TNB_EINVAL, "bs_execute_batched: stale or unknown plan id (plan cache was flushed)");
+  if ((plan->meta.na && !a_ptrs) || (plan->meta.nb && !b_ptrs) || !out_ptrs)
+    return fail(TNB_EINVAL, "bs_execute_batched: NULL pointer table");
+  if (plan->meta.mask && nbatch != 1)
+    return fail(TNB_EUNSUP, "bs_execute_batched: panel-masked plans run one contraction per launch");
+  return bs_execute_locked(*plan, a_ptrs, b_ptrs, out_ptrs, (cudaStream_t)stream, nbatch);
 }
 
 extern "C" int tnb_bs_plan_pairs(int64_t plan_id, int64_t max_pairs, int32_t* pairs_out, int64_t* npairs,

@@ -186,3 +186,53 @@ def test_one_shot_abi_matches_plan_execute(cuda):
     torch.cuda.synchronize()
     assert torch.equal(slab[:ref._blocks[0]._slab.numel()], ref._blocks[0]._slab)
     assert trip.tolist() == block_pairs(A, E).tolist()
+
+
+def test_contract_batched_equals_pairwise(cuda):
+    """contract_batched: ONE grouped launch over the output tiles of several equal-structure
+    block-sparse contractions (full C4 size); every result matches its own contract_pair
+    to 1e-13 relative (same per-tile pair order; the batch changes the stream-K split, so
+    partial sums are added at different k boundaries)."""
+    import bench
+    pairs = [bench.c4_tensors(tnb, seed=900 + 2 * i) for i in range(5)]
+    outs = tnb.contract_batched(pairs)
+    assert len(outs) == 5
+    for (A, E), got in zip(pairs, outs):
+        want = tnb.contract_pair(A, E)
+        assert got.labels == want.labels and got._qns == want._qns
+        for gb, wb in zip(got.get_blocks_(), want.get_blocks_()):
+            g, w = gb.numpy(), wb.numpy()
+            assert g.shape == w.shape
+            assert np.linalg.norm(g - w) <= 1e-13 * max(np.linalg.norm(w), 1e-300)
+
+
+def test_contract_batched_small_structures_and_errors(cuda):
+    """Several small U1 structures: batched == pairwise; pointer tables both inline (few
+    blocks) and device-staged (many items); mixed structures raise ValueError."""
+    u1 = Symmetry.u1()
+    V = Bond(btype=IN, sectors=[(-1, 3), (0, 4), (1, 2)], syms=[u1])
+    P = Bond(btype=IN, sectors=[(1, 1), (-1, 1)], syms=[u1])
+    def mk(seed, V=V):
+        A = UniTensor([V, P, V.redirect()], labels=["vl", "p", "vr"])
+        E = UniTensor([V, P.redirect(), V.redirect()], labels=["vr", "p", "x"])
+        tnb.random.normal_(A, seed=seed)
+        tnb.random.normal_(E, seed=seed + 1)
+        return A, E
+    for n in (2, 40):  # 2 x 15 pointers: 1 KB parameter table; 40 x 15: the 8 KB one
+        pairs = [mk(50 + 2 * i) for i in range(n)]
+        outs = tnb.contract_batched(pairs)
+        for (A, E), got in zip(pairs, outs):
+            want = tnb.contract_pair(A, E)
+            for gb, wb in zip(got.get_blocks_(), want.get_blocks_()):
+                assert np.linalg.norm(gb.numpy() - wb.numpy()) <= 1e-13 * max(np.linalg.norm(wb.numpy()), 1e-300)
+    many = [mk(300 + 2 * i) for i in range(80)]  # 80 x 15 = 1200 pointers: device table
+    outs = tnb.contract_batched(many)
+    for (A, E), got in zip(many[::13], outs[::13]):
+        want = tnb.contract_pair(A, E)
+        for gb, wb in zip(got.get_blocks_(), want.get_blocks_()):
+            assert np.linalg.norm(gb.numpy() - wb.numpy()) <= 1e-13 * max(np.linalg.norm(wb.numpy()), 1e-300)
+    V2 = Bond(btype=IN, sectors=[(-1, 3), (0, 5), (1, 2)], syms=[u1])
+    with pytest.raises(ValueError, match="block structure"):
+        tnb.contract_batched([mk(1), mk(3, V=V2)])
+    with pytest.raises(TypeError):
+        tnb.contract_batched([(1, 2)])
