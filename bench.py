@@ -178,19 +178,29 @@ class L2Flush:
 
 def time_steps(fn, steps, flush, dist):
     """Device time of `steps` calls of fn, each bracketed by its own events; L2 flushed
-    (untimed) before every call; barrier + synchronize around the region; max over ranks."""
+    (untimed) before every call; barrier + synchronize around the region; max over ranks.
+    Python's cyclic GC is collected before and paused during the region (as timeit does): a
+    generation-2 pass over a large heap is a 10-40 ms host stall unrelated to the work."""
+    import gc
     import torch
     pairs = []
     dist.barrier()
+    gc.collect()
     torch.cuda.synchronize()
-    for _ in range(steps):
-        flush()
-        e0, e1 = _events()
-        e0.record()
-        fn()
-        e1.record()
-        pairs.append((e0, e1))
-    torch.cuda.synchronize()
+    was = gc.isenabled()
+    gc.disable()
+    try:
+        for _ in range(steps):
+            flush()
+            e0, e1 = _events()
+            e0.record()
+            fn()
+            e1.record()
+            pairs.append((e0, e1))
+        torch.cuda.synchronize()
+    finally:
+        if was:
+            gc.enable()
     dist.barrier()
     total_ms = sum(a.elapsed_time(b) for a, b in pairs)
     return dist.max(total_ms)
@@ -268,14 +278,20 @@ def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, roof=True, s
             n.launch(host_out=outs[i % 2])  # result streamed to the pinned host buffer
 
         def run(k):
+            import gc
             dist.barrier()
+            gc.collect()
             torch.cuda.synchronize()
-            e0, e1 = _events()
-            e0.record()
-            for i in range(k):
-                step(i)
-            e1.record()
-            torch.cuda.synchronize()
+            gc.disable()  # as in time_steps
+            try:
+                e0, e1 = _events()
+                e0.record()
+                for i in range(k):
+                    step(i)
+                e1.record()
+                torch.cuda.synchronize()
+            finally:
+                gc.enable()
             dist.barrier()
             return dist.max(e0.elapsed_time(e1))
         run(max(2, warmup))
@@ -410,8 +426,9 @@ def gpu_c4_batch(tnb, n_total, steps, warmup, flush, dist):
             tnb.contract(A, E)
     for _ in range(warmup):
         step()
-        step_pairwise()
     ms = time_steps(step, steps, flush, dist) / steps
+    for _ in range(warmup):
+        step_pairwise()
     ms_pw = time_steps(step_pairwise, steps, flush, dist) / steps
     tnb._lib.ktimer_reset()
     tnb._lib.ktimer_enable(True)
@@ -728,7 +745,8 @@ def main():
             "ms_per_step": round(head["ms_per_step"], 5), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1), reference recipe)",
             "config": {"workload": "lawr_f64_chi1024", "chi": 1024, "d": 2, "D": 5, "order": head["order"],
-                       "l2": "flushed before every timed step (256 MiB write + 256 MiB read, untimed)", "parallelism":
+                       "l2": "flushed before every timed step (256 MiB write + 256 MiB read, untimed)",
+                       "python_gc": "collected before, paused during timed regions (as timeit)", "parallelism":
                        f"replicas x{dist.world}"},
             "e2e": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in head["e2e"].items()},
             "roofline": head["roofline"], "gpu_launches": int(head["launches_per_step"] * args.steps),
@@ -812,6 +830,9 @@ def main():
                          ("lawr_batch64_c128_chi512", w_c3b), ("peps_chi256_D8", w_peps),
                          ("svd_truncate_two_site_c4", w_svd), ("lanczos_lawr_chi1024", w_lanczos),
                          ("utn_load_c4", w_utn)]:
+            only = os.environ.get("TNB_BENCH_ONLY")  # dev: comma-separated subset of secondary workloads
+            if only and name not in only.split(","):
+                continue
             try:
                 wl[name] = fn()
             except Exception as e:  # noqa: BLE001

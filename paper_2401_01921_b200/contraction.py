@@ -306,7 +306,7 @@ def contract_batched(pairs):
     if not out_bonds:
         return [contract_pair(a, b) for a, b in pairs]
     dt = _result_dtype(a0.dtype, b0.dtype)
-    from .labeled import _slab_blocks, zero_flux_combos
+    from .labeled import _slab_blocks_batch, zero_flux_combos
     if not all(x.syms == out_bonds[0].syms for x in out_bonds):
         raise ValueError("all bonds must carry the same symmetries")
     qns = zero_flux_combos(out_bonds)
@@ -322,6 +322,8 @@ def contract_batched(pairs):
 
     sig0, ablk0, aperm, bblk0, bperm = structure(a0, b0)
     plan, shapes = _bs_plan(dt, a0, ablk0, aperm, b0, bblk0, bperm, a_pos, b_pos, out_bonds, qns)
+    # all outputs in one allocation (one allocator call per batch; the results share its lifetime)
+    out_blocks = _slab_blocks_batch(shapes, dt, len(pairs))
     aps, bps, ops, outs = [], [], [], []
     for k, (a, b) in enumerate(pairs):
         if k == 0:
@@ -332,7 +334,7 @@ def contract_batched(pairs):
             if (sig != sig0 or lay[0] != a_pos or lay[1] != b_pos or lay[4] != out_labels
                     or lay[5] != out_bonds):
                 raise ValueError(f"contract_batched: pair {k} does not share the block structure of pair 0")
-        oblk, _ = _slab_blocks(shapes, dt, zero=False)
+        oblk = out_blocks[k]
         aps.append(dense.block_ptrs(ablk))
         bps.append(dense.block_ptrs(bblk))
         ops.append([x._p0 for x in oblk])

@@ -723,9 +723,14 @@ struct PlanCache {
   std::vector<Plan> plans;
   uint32_t gen = 1;  // bumped when the cache is flushed: stale plan ids are rejected
   int device = -1;
-  void* stage = nullptr;  // pinned staging for large pointer tables
-  size_t stage_cap = 0;
-  cudaEvent_t stage_ev = nullptr;
+  // pinned staging for large pointer tables: a ring of slots, each reusable once the copy
+  // out of it has run (its event), so the host does not wait on the previous call's copy
+  static constexpr int kRing = 8;
+  void* stage[kRing] = {};
+  size_t stage_cap[kRing] = {};
+  cudaEvent_t stage_ev[kRing] = {};
+  int stage_next = 0;
+  std::vector<void*> captured_stage;  // pinned tables baked into captured graphs (kept alive)
   // stream-K partials + flags, shared by all plans of this device. Launches are
   // serialised through ws_ev when they come from different streams.
   void* ws = nullptr;
@@ -1138,15 +1143,30 @@ int bs_execute_locked(Plan& plan, const void* const* a_ptrs, const void* const* 
     }
     meta.ptrs = nullptr;
   } else {
-    if (g_cache.stage_ev) TNB_CUDA_CHECK(cudaEventSynchronize(g_cache.stage_ev));
-    size_t bytes = (size_t)nptr * sizeof(void*);
-    if (g_cache.stage_cap < bytes) {
-      if (g_cache.stage) cudaFreeHost(g_cache.stage);
-      g_cache.stage_cap = std::max(bytes, (size_t)1 << 16);
-      TNB_CUDA_CHECK(cudaMallocHost(&g_cache.stage, g_cache.stage_cap));
+    const size_t bytes = (size_t)nptr * sizeof(void*);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    TNB_CUDA_CHECK(cudaStreamIsCapturing(st, &cs));
+    const bool capturing = cs != cudaStreamCaptureStatusNone;
+    void* host = nullptr;
+    int slot = -1;
+    if (capturing) {
+      // a captured copy re-reads its source at every replay: give it its own buffer
+      TNB_CUDA_CHECK(cudaMallocHost(&host, bytes));
+      g_cache.captured_stage.push_back(host);
+    } else {
+      slot = g_cache.stage_next;
+      g_cache.stage_next = (slot + 1) % PlanCache::kRing;
+      if (g_cache.stage_ev[slot]) TNB_CUDA_CHECK(cudaEventSynchronize(g_cache.stage_ev[slot]));
+      if (g_cache.stage_cap[slot] < bytes) {
+        if (g_cache.stage[slot]) cudaFreeHost(g_cache.stage[slot]);
+        g_cache.stage_cap[slot] = std::max(bytes, (size_t)1 << 16);
+        TNB_CUDA_CHECK(cudaMallocHost(&g_cache.stage[slot], g_cache.stage_cap[slot]));
+      }
+      if (!g_cache.stage_ev[slot])
+        TNB_CUDA_CHECK(cudaEventCreateWithFlags(&g_cache.stage_ev[slot], cudaEventDisableTiming));
+      host = g_cache.stage[slot];
     }
-    if (!g_cache.stage_ev) TNB_CUDA_CHECK(cudaEventCreateWithFlags(&g_cache.stage_ev, cudaEventDisableTiming));
-    const void** hp = static_cast<const void**>(g_cache.stage);
+    const void** hp = static_cast<const void**>(host);
     for (int64_t q = 0; q < nbatch; ++q) {
       const void** h = hp + q * nptr1;
       for (int i = 0; i < na; ++i) h[i] = a_ptrs[q * na + i];
@@ -1156,7 +1176,7 @@ int bs_execute_locked(Plan& plan, const void* const* a_ptrs, const void* const* 
     void* dptr = nullptr;
     TNB_CUDA_CHECK(cudaMallocAsync(&dptr, bytes, st));
     TNB_CUDA_CHECK(cudaMemcpyAsync(dptr, hp, bytes, cudaMemcpyHostToDevice, st));
-    TNB_CUDA_CHECK(cudaEventRecord(g_cache.stage_ev, st));
+    if (slot >= 0) TNB_CUDA_CHECK(cudaEventRecord(g_cache.stage_ev[slot], st));
     meta.ptrs = static_cast<const void* const*>(dptr);
   }
   const void* const* hp = meta.ptrs ? nullptr : hv.data();
