@@ -23,7 +23,6 @@ import torch
 
 from . import _lib, dense
 from .charges import Bond, BondType, symmetry_from_str
-from .dense import DenseTensor
 from .labeled import UniTensor
 
 MAGIC = b"TNXU\x00"
