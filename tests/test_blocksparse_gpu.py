@@ -236,3 +236,28 @@ def test_contract_batched_small_structures_and_errors(cuda):
         tnb.contract_batched([mk(1), mk(3, V=V2)])
     with pytest.raises(TypeError):
         tnb.contract_batched([(1, 2)])
+
+
+def test_contract_batched_complex_and_permuted(cuda):
+    """Batched execute on complex128 blocks and on lazily permuted operands (shared perm)."""
+    u1 = Symmetry.u1()
+    V = Bond(btype=IN, sectors=[(-2, 2), (-1, 3), (0, 5), (1, 4), (2, 1)], syms=[u1])
+    P = Bond(btype=IN, sectors=[(1, 1), (-1, 1)], syms=[u1])
+
+    def mk(seed, dtype):
+        A = UniTensor([V, P, V.redirect()], labels=["vl", "p", "vr"], dtype=dtype)
+        E = UniTensor([V, P.redirect(), V.redirect()], labels=["vr", "p", "x"], dtype=dtype)
+        trandom.normal_(A, seed=seed)
+        trandom.normal_(E, seed=seed + 1)
+        return A, E
+
+    for dtype in (storage.Float64, storage.Complex128):
+        pairs = [mk(70 + 2 * i, dtype) for i in range(6)]
+        pairs = [(A.permute(["vr", "vl", "p"]), E) for A, E in pairs]  # lazy, same perm for all
+        outs = tnb.contract_batched(pairs)
+        for (A, E), got in zip(pairs, outs):
+            want = tnb.contract_pair(A, E)
+            assert got.labels == want.labels
+            for gb, wb in zip(got.get_blocks_(), want.get_blocks_()):
+                w = wb.numpy()
+                assert np.linalg.norm(gb.numpy() - w) <= 1e-13 * max(np.linalg.norm(w), 1e-300)
