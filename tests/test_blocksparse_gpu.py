@@ -261,3 +261,34 @@ def test_contract_batched_complex_and_permuted(cuda):
             for gb, wb in zip(got.get_blocks_(), want.get_blocks_()):
                 w = wb.numpy()
                 assert np.linalg.norm(gb.numpy() - w) <= 1e-13 * max(np.linalg.norm(w), 1e-300)
+
+
+def test_contract_batched_graph_capture_large_table(cuda):
+    """A batched contraction whose pointer table exceeds the kernel parameter (device table
+    staged from pinned memory) captured in a CUDA graph: replays reproduce the eager result
+    even after later eager calls reused the staging ring."""
+    import torch
+    from paper_2401_01921_b200 import graphs
+    u1 = Symmetry.u1()
+    V = Bond(btype=IN, sectors=[(-1, 3), (0, 4), (1, 2)], syms=[u1])
+    P = Bond(btype=IN, sectors=[(1, 1), (-1, 1)], syms=[u1])
+
+    def mk(seed):
+        A = UniTensor([V, P, V.redirect()], labels=["vl", "p", "vr"])
+        E = UniTensor([V, P.redirect(), V.redirect()], labels=["vr", "p", "x"])
+        trandom.normal_(A, seed=seed)
+        trandom.normal_(E, seed=seed + 1)
+        return A, E
+
+    pairs = [mk(400 + 2 * i) for i in range(80)]  # 80 x 15 = 1200 pointers > 1024
+    want = [o.get_blocks_()[1].numpy() for o in tnb.contract_batched(pairs)]
+    holder = {}
+    g = graphs.capture(lambda: holder.__setitem__("outs", tnb.contract_batched(pairs)), warmup=1)
+    other = [mk(900 + 2 * i) for i in range(80)]
+    for _ in range(10):  # cycle the eager staging ring past its 8 slots
+        tnb.contract_batched(other)
+    g.replay()
+    torch.cuda.synchronize()
+    for k in (0, 37, 79):
+        got = holder["outs"][k].get_blocks_()[1].numpy()
+        assert np.linalg.norm(got - want[k]) <= 1e-13 * np.linalg.norm(want[k])
