@@ -292,3 +292,60 @@ def test_contract_batched_graph_capture_large_table(cuda):
     for k in (0, 37, 79):
         got = holder["outs"][k].get_blocks_()[1].numpy()
         assert np.linalg.norm(got - want[k]) <= 1e-13 * np.linalg.norm(want[k])
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_block_sparse_pairs_vs_oracle(cuda, seed):
+    """Randomised structures: U1 / Z2 / Z3 / U1 x Z2 bonds with random sectors and
+    degeneracies, rank-3/4 operands sharing one or two legs (opposite directions), a
+    random lazy permute of each operand; pairing triples bit-exact and every output block
+    within 1e-12 (relative Frobenius) of the oracle's _contract_pair_blocks restatement."""
+    from paper_2401_01921_b200.charges import OUT
+    rng = np.random.default_rng(1000 + seed)
+    sym_sets = [[Symmetry.u1()], [Symmetry.zn(2)], [Symmetry.zn(3)], [Symmetry.u1(), Symmetry.zn(2)]]
+    syms = sym_sets[seed % len(sym_sets)]
+
+    def rand_q():
+        return tuple(int(rng.integers(-2, 3)) if s.modulus == 0 else int(rng.integers(0, s.modulus)) for s in syms)
+
+    def rand_bond(btype):
+        qs = [tuple(0 for _ in syms)]  # the identity charge on every bond: zero flux is reachable
+        while len(qs) < int(rng.integers(2, 5)):
+            q = rand_q()
+            if q not in qs:
+                qs.append(q)
+        return Bond(btype=btype, sectors=[(q, int(rng.integers(1, 5))) for q in qs], syms=syms)
+
+    ra, rb = int(rng.integers(3, 5)), int(rng.integers(3, 5))
+    nsh = int(rng.integers(1, 3))
+    a_bonds = [rand_bond(IN if rng.random() < 0.5 else OUT) for _ in range(ra)]
+    shared = list(rng.choice(ra, size=nsh, replace=False))
+    b_bonds = [a_bonds[i].redirect() for i in shared] + [rand_bond(IN if rng.random() < 0.5 else OUT)
+                                                         for _ in range(rb - nsh)]
+    a_labels = [f"a{i}" for i in range(ra)]
+    b_labels = [a_labels[i] for i in shared] + [f"b{i}" for i in range(rb - nsh)]
+    try:
+        A = UniTensor(a_bonds, labels=a_labels)
+        B = UniTensor(b_bonds, labels=b_labels)
+    except ValueError:
+        pytest.skip("no zero-flux block for this draw")
+    trandom.normal_(A, seed=seed)
+    trandom.normal_(B, seed=seed + 100)
+    A = A.permute(list(rng.permutation(a_labels)))
+    B = B.permute(list(rng.permutation(b_labels)))
+    try:
+        out = contract(A, B)
+    except ValueError as e:
+        assert "no valid blocks" in str(e)
+        pytest.skip("output has no zero-flux block")
+    a_np = [blk.numpy() for blk in A.get_blocks_()]
+    b_np = [blk.numpy() for blk in B.get_blocks_()]
+    want, triples = oracle.contract_blocks(A._qns, a_np, A.labels, B._qns, b_np, B.labels, out._qns)
+    got_pairs = [tuple(int(x) for x in r) for r in block_pairs(A, B)]
+    assert got_pairs == [tuple(t) for t in triples]
+    shapes = [blk.shape for blk in out.get_blocks_()]
+    want = oracle.finish_blocks(want, shapes, np.float64)
+    for blk, w in zip(out.get_blocks_(), want):
+        g = blk.numpy()
+        assert g.shape == w.shape
+        assert rel_fro(g, w) <= 1e-12 or np.linalg.norm(w) == 0 and np.abs(g).max() == 0
