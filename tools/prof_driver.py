@@ -67,3 +67,16 @@ if __name__ == "__main__":
     elif what == "c4":
         c4(int(sys.argv[2]))
     print("done")
+
+
+def c4_batch(n, iters):
+    sys.path.insert(0, ROOT)
+    import bench
+    pairs = [bench.c4_tensors(tnb, seed=777 + 2 * i) for i in range(n)]
+    for _ in range(iters):
+        tnb.contract_batched(pairs)
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__" and sys.argv[1] == "c4_batch":
+    c4_batch(int(sys.argv[2]), int(sys.argv[3]))
