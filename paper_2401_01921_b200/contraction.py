@@ -221,9 +221,10 @@ _PANEL_SINK = None
 
 
 def _common_perm(t):
-    perms = {blk.perm for blk in t._blocks}
-    if len(perms) == 1:
-        return t._blocks, next(iter(perms))
+    blks = t._blocks
+    p0 = blks[0]._perm if blks else ()
+    if all(blk._perm == p0 for blk in blks):
+        return blks, p0
     # blocks were permuted individually (put_block_/contiguous_ on one block): materialise
     return [blk.contiguous() for blk in t._blocks], tuple(range(t.rank))
 
@@ -316,8 +317,8 @@ def contract_batched(pairs):
     def structure(a, b):
         ablk, aperm = _common_perm(a)
         bblk, bperm = _common_perm(b)
-        sig = (a.dtype, b.dtype, tuple(a._qns), tuple(b._qns), tuple(x.storage_shape for x in ablk),
-               tuple(x.storage_shape for x in bblk), tuple(aperm), tuple(bperm))
+        sig = (a.dtype, b.dtype, a._qns, b._qns, [x._sshape for x in ablk], [x._sshape for x in bblk],
+               tuple(aperm), tuple(bperm))
         return sig, _widen(ablk, dt), aperm, _widen(bblk, dt), bperm
 
     sig0, ablk0, aperm, bblk0, bperm = structure(a0, b0)
