@@ -114,3 +114,18 @@ def test_device_lanczos_matches_reference_golden(cuda):
             v = vecs[:, j].contiguous()
             r = op(v) - vals[j] * v
             assert float(torch.linalg.vector_norm(r)) <= 1e-8 * max(1.0, abs(vals[j]))
+
+
+def test_device_lanczos_complex_hermitian(cuda):
+    """complex128 Hermitian operators (the reference's LinOp dtype argument): lowest Ritz
+    values equal eigvalsh, eigenvectors satisfy the residual bound."""
+    rng = np.random.default_rng(7)
+    for dim, k in [(30, 1), (120, 2)]:
+        a = rng.standard_normal((dim, dim)) + 1j * rng.standard_normal((dim, dim))
+        a = (a + a.conj().T) / 2
+        ad = torch.from_numpy(a).cuda()
+        vals, vecs = lanczos(LinOp(dim, matvec=lambda v: ad @ v, dtype=np.complex128), k=k, tol=1e-12, seed=3)
+        assert np.allclose(vals, np.linalg.eigvalsh(a)[:k], atol=1e-10)
+        for i in range(k):
+            r = torch.linalg.vector_norm(ad @ vecs[:, i] - vals[i] * vecs[:, i])
+            assert float(r) <= 1e-8
