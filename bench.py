@@ -825,7 +825,7 @@ def main():
             return {"value": round(ut["gbs"], 3), "unit": "GB/s (payload / host wall)", **ut}
 
         # each secondary workload is isolated: a failure is recorded, the headline line still prints
-        for name, fn in [("lawr_c128_chi1024", w_c3), ("lawr_f64_chi128", w_c1), ("permute_sweep", w_perm),
+        for name, fn in [("permute_sweep", w_perm), ("lawr_c128_chi1024", w_c3), ("lawr_f64_chi128", w_c1),
                          ("blocksparse_c4", w_c4), ("blocksparse_c4_batch64", w_c4b),
                          ("lawr_batch64_c128_chi512", w_c3b), ("peps_chi256_D8", w_peps),
                          ("svd_truncate_two_site_c4", w_svd), ("lanczos_lawr_chi1024", w_lanczos),
