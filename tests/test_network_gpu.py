@@ -269,3 +269,58 @@ def test_launch_replay_program_matches_and_tracks_changes(cuda, monkeypatch):
     calls.clear()
     out = net.launch()
     assert not calls and rel_fro(out.numpy(), want * (1 + 1j)) <= 1e-12
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_networks_vs_oracle(cuda, seed):
+    """Random tree-shaped networks (3-6 tensors, ranks 1-4, dims 2-9, some open legs) with the
+    optimal order: the DP order string equals the oracle's and the contracted result equals
+    the oracle's launch within 1e-12 (f64; every other seed complex128)."""
+    rng = np.random.default_rng(2000 + seed)
+    n = int(rng.integers(3, 7))
+    names = [f"T{i}" for i in range(n)]
+    labels = {nm: [] for nm in names}
+    dims = {}
+    lab = 0
+    for i in range(1, n):  # spanning tree: tensor i bonds to a random earlier tensor
+        j = int(rng.integers(0, i))
+        l = f"e{lab}"
+        lab += 1
+        labels[names[i]].append(l)
+        labels[names[j]].append(l)
+        dims[l] = int(rng.integers(2, 10))
+    for _ in range(int(rng.integers(0, n))):  # extra loops between distinct tensors
+        i, j = rng.choice(n, size=2, replace=False)
+        if len(labels[names[i]]) < 4 and len(labels[names[j]]) < 4:
+            l = f"e{lab}"
+            lab += 1
+            labels[names[i]].append(l)
+            labels[names[j]].append(l)
+            dims[l] = int(rng.integers(2, 6))
+    opens = []
+    for nm in names:  # open legs
+        if len(labels[nm]) < 4 and rng.random() < 0.4:
+            l = f"o{nm}"
+            labels[nm].append(l)
+            dims[l] = int(rng.integers(2, 6))
+            opens.append(l)
+    dtype = np.complex128 if seed % 2 else np.float64
+    arrays = {}
+    for k, nm in enumerate(names):
+        shp = [dims[l] for l in labels[nm]]
+        a = oracle.normal(shp, seed=100 * seed + k)
+        if dtype == np.complex128:
+            a = a + 1j * oracle.normal(shp, seed=100 * seed + 50 + k)
+        arrays[nm] = a
+    tout = ", ".join(opens)
+    lines = [f"{nm}: {', '.join(labels[nm])}" for nm in names] + [f"TOUT: {tout}"]
+    want, tree = oracle.launch([(nm, labels[nm]) for nm in names], tout, arrays)
+    net = Network(lines)
+    for nm in names:
+        t = UniTensor(storage.from_numpy(arrays[nm]), labels=[f"x{i}" for i in range(arrays[nm].ndim)])
+        net.put_tensor(nm, t, t.labels)
+    net.set_order(optimal=True)
+    out = net.launch()
+    assert net.get_order() == oracle.render_order(tree)
+    got = out.numpy() if opens else np.asarray(out.item())
+    assert rel_fro(got, want) <= 1e-12
