@@ -46,6 +46,9 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
@@ -183,9 +186,10 @@ struct SKCore {
     double* w = ws + (size_t)c * ACCN * NMATH;
 #pragma unroll
     for (int r = 0; r < ACCN; ++r) __stcg(w + (size_t)r * NMATH + tid, flat[r]);
-    __threadfence();
-    detail::named_sync(2, NMATH);
-    if (tid == 0) detail::st_release(flags + c, 1);
+    // per warp: the warp barrier orders its lanes' stores before lane 0's gpu-scope release
+    // (cumulative), so no CTA-wide barrier or per-thread fence: each warp moves on at once
+    __syncwarp();
+    if ((tid & 31) == 0) detail::red_release_add(flags + c, 1);
   }
   // The owner adds the partials of CTAs first..c-1 in CTA order (fixed summation
   // order). With clear, each consumed flag is reset (every CTA publishes at most
@@ -195,7 +199,7 @@ struct SKCore {
     double* flat = &acc[0][0][0][0];
     for (int cc = first; cc < c; ++cc) {
       if (tid == 0)
-        while (detail::ld_acquire(flags + cc) == 0) {
+        while (detail::ld_acquire(flags + cc) < NMATH / 32) {  // every math warp of CTA cc published
         }
       detail::named_sync(2, NMATH);
       const double* w = ws + (size_t)cc * ACCN * NMATH;
