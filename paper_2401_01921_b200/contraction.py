@@ -326,6 +326,10 @@ def contract_batched(pairs):
     # all outputs in one allocation (one allocator call per batch; the results share its lifetime)
     out_blocks = _slab_blocks_batch(shapes, dt, len(pairs))
     aps, bps, ops, outs = [], [], [], []
+    # converted (_widen) or materialised (_common_perm) operand blocks must outlive the
+    # launch: only their raw pointers travel in the tables, and the caching allocator would
+    # otherwise hand their memory to the next pair's conversion before the kernel runs
+    keep = []
     for k, (a, b) in enumerate(pairs):
         if k == 0:
             ablk, bblk, lay = ablk0, bblk0, (a_pos, b_pos, a_free, b_free, out_labels, out_bonds)
@@ -336,6 +340,7 @@ def contract_batched(pairs):
                     or lay[5] != out_bonds):
                 raise ValueError(f"contract_batched: pair {k} does not share the block structure of pair 0")
         oblk = out_blocks[k]
+        keep.append((ablk, bblk))
         aps.append(dense.block_ptrs(ablk))
         bps.append(dense.block_ptrs(bblk))
         ops.append([x._p0 for x in oblk])
@@ -345,6 +350,7 @@ def contract_batched(pairs):
         plan, _ = _bs_plan(dt, a0, ablk0, aperm, b0, bblk0, bperm, a_pos, b_pos, out_bonds, qns)
         if not plan.execute_batched(aps, bps, ops, dense.stream_handle()):
             raise _lib.EngineError("block-sparse plan went stale twice")
+    del keep  # the launch is queued on the stream: the allocator reuses these only after it
     return outs
 
 

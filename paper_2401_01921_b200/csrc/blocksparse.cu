@@ -715,14 +715,16 @@ struct Plan {
   size_t o_optr = 0, o_pairs = 0;
   int dtype = 0;
   bool amf = true, bnf = true;  // operand gather orientation (coalescing only)
+  bool captured = false;         // executed under stream capture: a graph points into dblob
 };
 
+// One cache per device (plans, workspace, staging ring and events are device objects);
+// all caches are guarded by one mutex, g_bs_mu.
 struct PlanCache {
-  std::mutex mu;
   std::unordered_map<std::string, int64_t> index;  // structure key -> slot in plans
   std::vector<Plan> plans;
   uint32_t gen = 1;  // bumped when the cache is flushed: stale plan ids are rejected
-  int device = -1;
+  std::vector<unsigned char*> retained;  // dblobs of flushed plans that captured graphs still read
   // pinned staging for large pointer tables: a ring of slots, each reusable once the copy
   // out of it has run (its event), so the host does not wait on the previous call's copy
   static constexpr int kRing = 8;
@@ -730,7 +732,6 @@ struct PlanCache {
   size_t stage_cap[kRing] = {};
   cudaEvent_t stage_ev[kRing] = {};
   int stage_next = 0;
-  std::vector<void*> captured_stage;  // pinned tables baked into captured graphs (kept alive)
   // stream-K partials + flags, shared by all plans of this device. Launches are
   // serialised through ws_ev when they come from different streams.
   void* ws = nullptr;
@@ -738,7 +739,20 @@ struct PlanCache {
   cudaEvent_t ws_ev = nullptr;
   cudaStream_t ws_stream = nullptr;
 };
-PlanCache g_cache;
+std::mutex g_bs_mu;
+constexpr int kMaxDevices = 64;
+PlanCache* g_caches[kMaxDevices] = {};
+
+// The current device's cache (caller holds g_bs_mu).
+PlanCache& cur_cache() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+    cudaGetLastError();
+    dev = 0;
+  }
+  if (!g_caches[dev]) g_caches[dev] = new PlanCache();  // process lifetime (device memory)
+  return *g_caches[dev];
+}
 
 constexpr int kMaxBsCtas = 2048;  // flags region: one int per persistent CTA
 constexpr size_t kBsPartialOff = 16384;
@@ -765,19 +779,31 @@ int launch_bs_one(const BsMeta& meta, const void* const* hp, int nptr, BsSK sk, 
   const int G = std::min(sm_count() * occ, kMaxBsCtas);
   // workspace: flags (self-resetting) at offset 0, register partials after kBsPartialOff
   const size_t need = kBsPartialOff + (size_t)G * Core::ACCN * Core::NMATH * 8;
-  if (g_cache.ws_bytes < need) {
-    if (g_cache.ws) {
-      TNB_CUDA_CHECK(cudaDeviceSynchronize());
-      cudaFree(g_cache.ws);
-      g_cache.ws = nullptr;
-      g_cache.ws_bytes = 0;
+  void* graph_ws = nullptr;
+  if (capturing) {
+    // the graph owns its workspace (stream-ordered allocation node + flag memset node):
+    // a replay never shares flags/partials with eager launches or other graphs, and a
+    // later eager call that grows the shared workspace cannot free memory a graph reads
+    TNB_CUDA_CHECK(cudaMallocAsync(&graph_ws, need, st));
+    TNB_CUDA_CHECK(cudaMemsetAsync(graph_ws, 0, kBsPartialOff, st));
+    sk.flags = static_cast<int*>(graph_ws);
+    sk.ws = reinterpret_cast<double*>(static_cast<char*>(graph_ws) + kBsPartialOff);
+  } else {
+    PlanCache& C = cur_cache();
+    if (C.ws_bytes < need) {
+      if (C.ws) {
+        TNB_CUDA_CHECK(cudaDeviceSynchronize());
+        cudaFree(C.ws);
+        C.ws = nullptr;
+        C.ws_bytes = 0;
+      }
+      TNB_CUDA_CHECK(cudaMalloc(&C.ws, need));
+      TNB_CUDA_CHECK(cudaMemset(C.ws, 0, need));
+      C.ws_bytes = need;
     }
-    TNB_CUDA_CHECK(cudaMalloc(&g_cache.ws, need));
-    TNB_CUDA_CHECK(cudaMemset(g_cache.ws, 0, need));
-    g_cache.ws_bytes = need;
+    sk.flags = static_cast<int*>(C.ws);
+    sk.ws = reinterpret_cast<double*>(static_cast<char*>(C.ws) + kBsPartialOff);
   }
-  sk.flags = static_cast<int*>(g_cache.ws);
-  sk.ws = reinterpret_cast<double*>(static_cast<char*>(g_cache.ws) + kBsPartialOff);
   sk.trace = nullptr;
   static const char* trace_path = getenv("TNB_BS_TRACE");
   if (trace_path && !capturing) {
@@ -789,7 +815,11 @@ int launch_bs_one(const BsMeta& meta, const void* const* hp, int nptr, BsSK sk, 
     kern<<<G, Core::NT, smem, st>>>(meta, pt, sk);
   }
   count_launch();
-  TNB_CUDA_CHECK(cudaGetLastError());
+  {
+    cudaError_t e = cudaGetLastError();
+    if (graph_ws) cudaFreeAsync(graph_ws, st);
+    if (e != cudaSuccess) return cuda_fail(e, "bs_contract: grouped GEMM launch");
+  }
   if (sk.trace) {
     std::vector<long long> h((size_t)G * kTraceW);
     TNB_CUDA_CHECK(cudaMemcpyAsync(h.data(), sk.trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
@@ -807,10 +837,9 @@ int launch_bs_one(const BsMeta& meta, const void* const* hp, int nptr, BsSK sk, 
 template <bool CPLX, int MODE>
 int launch_bs(const Plan& plan, const BsMeta& meta, const void* const* hp, int nptr, cudaStream_t st) {
   if (meta.ntiles == 0) return TNB_OK;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  TNB_CUDA_CHECK(cudaStreamIsCapturing(st, &cs));
-  const bool capturing = cs != cudaStreamCaptureStatusNone;
-  if (!capturing && g_cache.ws_ev && g_cache.ws_stream != st) TNB_CUDA_CHECK(cudaStreamWaitEvent(st, g_cache.ws_ev, 0));
+  const bool capturing = tnb::capturing(st);
+  PlanCache& C = cur_cache();
+  if (!capturing && C.ws_ev && C.ws_stream != st) TNB_CUDA_CHECK(cudaStreamWaitEvent(st, C.ws_ev, 0));
   BsSK sk;
   int rc;
   const bool small = meta.ptrs || nptr <= kInlinePtrsSmall;
@@ -829,9 +858,9 @@ int launch_bs(const Plan& plan, const BsMeta& meta, const void* const* hp, int n
                : launch_bs_one<CPLX, MODE, false, false, L>(meta, hp, nptr, sk, capturing, st);
   if (rc) return rc;
   if (!capturing) {
-    if (!g_cache.ws_ev) TNB_CUDA_CHECK(cudaEventCreateWithFlags(&g_cache.ws_ev, cudaEventDisableTiming));
-    TNB_CUDA_CHECK(cudaEventRecord(g_cache.ws_ev, st));
-    g_cache.ws_stream = st;
+    if (!C.ws_ev) TNB_CUDA_CHECK(cudaEventCreateWithFlags(&C.ws_ev, cudaEventDisableTiming));
+    TNB_CUDA_CHECK(cudaEventRecord(C.ws_ev, st));
+    C.ws_stream = st;
   }
   return TNB_OK;
 }
@@ -882,19 +911,17 @@ int bs_plan_locked(int dtype, int na, int nb, int nout, int rank_a, int rank_b, 
       append(key, panel_mask, (size_t)npanels);
     }
   }
-  int dev = 0;
-  TNB_CUDA_CHECK(cudaGetDevice(&dev));
-  if (g_cache.device != dev) {
-    g_cache.plans.clear();  // plans are per device (one process normally drives one GPU)
-    g_cache.index.clear();
-    ++g_cache.gen;
-    g_cache.device = dev;
-  }
+  PlanCache& g_cache = cur_cache();
   auto hit = g_cache.index.find(key);
   if (hit == g_cache.index.end()) {
     if (g_cache.plans.size() >= 256) {
       TNB_CUDA_CHECK(cudaDeviceSynchronize());
-      for (auto& pl : g_cache.plans) cudaFree(pl.dblob);
+      // plans a captured graph launched stay allocated: the graph's kernel nodes hold
+      // pointers into their dblob for as long as the graph lives
+      for (auto& pl : g_cache.plans) {
+        if (pl.captured) g_cache.retained.push_back(pl.dblob);
+        else cudaFree(pl.dblob);
+      }
       g_cache.plans.clear();
       g_cache.index.clear();
       ++g_cache.gen;
@@ -1112,6 +1139,7 @@ int bs_plan_locked(int dtype, int na, int nb, int nout, int rank_a, int rank_b, 
 }
 
 Plan* plan_of(int64_t id) {
+  PlanCache& g_cache = cur_cache();
   const uint32_t gen = (uint32_t)((uint64_t)id >> 32);
   const int64_t slot = id & 0xffffffffll;
   if (gen != g_cache.gen || slot < 0 || slot >= (int64_t)g_cache.plans.size()) return nullptr;
@@ -1144,16 +1172,17 @@ int bs_execute_locked(Plan& plan, const void* const* a_ptrs, const void* const* 
     meta.ptrs = nullptr;
   } else {
     const size_t bytes = (size_t)nptr * sizeof(void*);
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    TNB_CUDA_CHECK(cudaStreamIsCapturing(st, &cs));
-    const bool capturing = cs != cudaStreamCaptureStatusNone;
+    const bool capturing = tnb::capturing(st);
+    PlanCache& g_cache = cur_cache();
     void* host = nullptr;
     int slot = -1;
     if (capturing) {
-      // a captured copy re-reads its source at every replay: give it its own buffer
-      TNB_CUDA_CHECK(cudaMallocHost(&host, bytes));
-      g_cache.captured_stage.push_back(host);
+      // a captured copy re-reads its source at every replay: its own pinned buffer, owned
+      // (and eventually freed) by the graph
+      rc = capture_pinned(st, bytes, &host);
+      if (rc) return rc;
     } else {
+      release_deferred_host();
       slot = g_cache.stage_next;
       g_cache.stage_next = (slot + 1) % PlanCache::kRing;
       if (g_cache.stage_ev[slot]) TNB_CUDA_CHECK(cudaEventSynchronize(g_cache.stage_ev[slot]));
@@ -1179,6 +1208,7 @@ int bs_execute_locked(Plan& plan, const void* const* a_ptrs, const void* const* 
     if (slot >= 0) TNB_CUDA_CHECK(cudaEventRecord(g_cache.stage_ev[slot], st));
     meta.ptrs = static_cast<const void* const*>(dptr);
   }
+  if (tnb::capturing(st)) plan.captured = true;
   const void* const* hp = meta.ptrs ? nullptr : hv.data();
   const int nin = meta.ptrs ? 0 : (int)nptr;
   if (plan.dtype == TNB_F64) rc = launch_bs<false, 0>(plan, meta, hp, nin, st);
@@ -1233,7 +1263,7 @@ extern "C" int tnb_bs_plan(int dtype, int na, int nb, int nout, int rank_a, int 
   int rc = require_device();
   if (rc) return rc;
   if (!plan_id) return fail(TNB_EINVAL, "bs_plan: plan_id is NULL");
-  std::lock_guard<std::mutex> lock(g_cache.mu);
+  std::lock_guard<std::mutex> lock(g_bs_mu);
   return bs_plan_locked(dtype, na, nb, nout, rank_a, rank_b, a_qn, a_shape, a_perm, b_qn, b_shape, b_perm, nc, a_axes,
                         b_axes, out_qn, out_shape, npanels, panel_mask, (cudaStream_t)stream, plan_id, npairs);
 }
@@ -1243,7 +1273,7 @@ extern "C" int tnb_bs_execute(int64_t plan_id, const void* const* a_ptrs, const 
   using namespace tnb;
   int rc = require_device();
   if (rc) return rc;
-  std::lock_guard<std::mutex> lock(g_cache.mu);
+  std::lock_guard<std::mutex> lock(g_bs_mu);
   Plan* plan = plan_of(plan_id);
   if (!plan) return fail(TNB_EINVAL, "bs_execute: stale or unknown plan id (plan cache was flushed)");
   if ((plan->meta.na && !a_ptrs) || (plan->meta.nb && !b_ptrs) || !out_ptrs)
@@ -1256,7 +1286,7 @@ extern "C" int tnb_bs_execute_batched(int64_t plan_id, int64_t nbatch, const voi
   using namespace tnb;
   int rc = require_device();
   if (rc) return rc;
-  std::lock_guard<std::mutex> lock(g_cache.mu);
+  std::lock_guard<std::mutex> lock(g_bs_mu);
   Plan* plan = plan_of(plan_id);
   if (!plan) return fail(TNB_EINVAL, "bs_execute_batched: stale or unknown plan id (plan cache was flushed)");
   if ((plan->meta.na && !a_ptrs) || (plan->meta.nb && !b_ptrs) || !out_ptrs)
@@ -1272,7 +1302,7 @@ extern "C" int tnb_bs_plan_pairs(int64_t plan_id, int64_t max_pairs, int32_t* pa
   int rc = require_device();
   if (rc) return rc;
   if (!pairs_out) return fail(TNB_EINVAL, "bs_plan_pairs: pairs_out is NULL");
-  std::lock_guard<std::mutex> lock(g_cache.mu);
+  std::lock_guard<std::mutex> lock(g_bs_mu);
   Plan* plan = plan_of(plan_id);
   if (!plan) return fail(TNB_EINVAL, "bs_plan_pairs: stale or unknown plan id");
   return bs_pairs_locked(*plan, max_pairs, pairs_out, npairs, (cudaStream_t)stream);
@@ -1290,7 +1320,7 @@ extern "C" int tnb_bs_contract_masked(int dtype, int na, int nb, int nout, int r
   int rc = require_device();
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  std::lock_guard<std::mutex> lock(g_cache.mu);
+  std::lock_guard<std::mutex> lock(g_bs_mu);
   int64_t id = 0;
   rc = bs_plan_locked(dtype, na, nb, nout, rank_a, rank_b, a_qn, a_shape, a_perm, b_qn, b_shape, b_perm, nc, a_axes,
                       b_axes, out_qn, out_shape, npanels, panel_mask, st, &id, npairs);

@@ -109,6 +109,53 @@ int sm_count() {
   return g_sms > 0 ? g_sms : 148;
 }
 
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cs != cudaStreamCaptureStatusNone;
+}
+
+namespace {
+std::mutex g_deferred_mu;
+std::vector<void*> g_deferred;
+void CUDART_CB queue_host_free(void* p) {
+  std::lock_guard<std::mutex> lk(g_deferred_mu);
+  g_deferred.push_back(p);
+}
+}  // namespace
+
+void release_deferred_host() {
+  std::vector<void*> q;
+  {
+    std::lock_guard<std::mutex> lk(g_deferred_mu);
+    q.swap(g_deferred);
+  }
+  for (void* p : q) cudaFreeHost(p);
+}
+
+int capture_pinned(cudaStream_t st, size_t bytes, void** out) {
+  *out = nullptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaGraph_t graph = nullptr;
+  TNB_CUDA_CHECK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, nullptr, nullptr));
+  if (cs != cudaStreamCaptureStatusActive || !graph) return fail(TNB_EINVAL, "capture_pinned: stream is not capturing");
+  void* p = nullptr;
+  TNB_CUDA_CHECK(cudaMallocHost(&p, bytes));
+  cudaUserObject_t obj = nullptr;
+  cudaError_t e = cudaUserObjectCreate(&obj, p, queue_host_free, 1, cudaUserObjectNoDestructorSync);
+  if (e != cudaSuccess) {
+    cudaFreeHost(p);
+    return cuda_fail(e, "capture_pinned: cudaUserObjectCreate");
+  }
+  // the graph takes over our reference: p lives until the graph and every exec made from it die
+  TNB_CUDA_CHECK(cudaGraphRetainUserObject(graph, obj, 1, cudaGraphUserObjectMove));
+  *out = p;
+  return TNB_OK;
+}
+
 }  // namespace tnb
 
 extern "C" {

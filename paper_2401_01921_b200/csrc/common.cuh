@@ -25,6 +25,19 @@ int cuda_fail(cudaError_t e, const char* what);
 int require_device();
 int sm_count();
 
+// True iff `st` is being captured into a CUDA graph.
+bool capturing(cudaStream_t st);
+
+// Pinned host memory owned by the graph being captured on `st`: a captured memcpy node
+// re-reads its host source at every replay, so the source must live as long as the
+// graph. The buffer is tied to the graph with a cudaUserObject; when the last graph
+// (or instantiated graph) referencing it is destroyed, the pointer is queued and freed
+// by the next release_deferred_host() call (CUDA API calls are not allowed inside a
+// user-object destructor).
+int capture_pinned(cudaStream_t st, size_t bytes, void** out);
+// Frees queued graph-owned host buffers. Call only outside stream capture.
+void release_deferred_host();
+
 // Counts every kernel this library launches (tnb_launch_count); bench.py reports it.
 void count_launch(int n = 1);
 

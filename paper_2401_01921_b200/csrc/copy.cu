@@ -10,6 +10,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cstring>
+
 #include "common.cuh"
 
 namespace tnb {
@@ -97,15 +99,32 @@ extern "C" int tnb_copy2d_batched(const void* src, void* dst, int64_t nseg, cons
     std::copy(row0.begin(), row0.end(), tab->row0);
   } else {
     const size_t sb = sizeof(TnbCopy2D) * (size_t)nseg, rb = sizeof(int64_t) * ((size_t)nseg + 1);
+    // eager: pageable sources are staged before cudaMemcpyAsync returns. Under capture the
+    // memcpy node re-reads its source at every replay, so the table goes to pinned memory
+    // owned by the graph.
+    const void* src_tab = nullptr;
+    std::vector<unsigned char> packed;
+    if (capturing(st)) {
+      void* pin = nullptr;
+      int rc2 = capture_pinned(st, sb + rb, &pin);
+      if (rc2) {
+        delete tab;
+        return rc2;
+      }
+      src_tab = pin;
+    } else {
+      release_deferred_host();
+      packed.resize(sb + rb);
+      src_tab = packed.data();
+    }
+    memcpy(const_cast<void*>(src_tab), segs, sb);
+    memcpy(static_cast<char*>(const_cast<void*>(src_tab)) + sb, row0.data(), rb);
     cudaError_t e = cudaMallocAsync(&dmem, sb + rb, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(dmem, segs, sb, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(static_cast<char*>(dmem) + sb, row0.data(), rb, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dmem, src_tab, sb + rb, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) {
       delete tab;
       return cuda_fail(e, "copy2d: segment table upload");
     }
-    // pageable sources: the copies above are staged before cudaMemcpyAsync returns
     gsegs = static_cast<TnbCopy2D*>(dmem);
     grow0 = reinterpret_cast<int64_t*>(static_cast<char*>(dmem) + sb);
   }

@@ -171,6 +171,52 @@ def _read_to_device(f, staging, nbytes, path):
             evs[b].synchronize()  # buffers are reused by the next load
 
 
+def payload_nbytes(ut):
+    """Bytes of the packed payload of ``ut``: every block's C-order elements concatenated in
+    block order (the ``.utn`` payload layout, io.py:56-80)."""
+    return sum(b.size for b in ut.get_blocks_()) * ut.dtype.itemsize
+
+
+def upload_payload_(ut, host):
+    """Fill every block of ``ut`` from a host payload (pinned CPU tensor or numpy array in
+    the packed ``.utn`` layout, same dtype): one host->device copy into a staging buffer and
+    one ``tnb_copy2d_batched`` scatter to the blocks' places in the slab, both queued on the
+    current stream (asynchronous for pinned input). Blocks must be stored contiguously
+    (a freshly built or loaded tensor)."""
+    blocks = ut.get_blocks_()
+    if any(not b.is_contiguous for b in blocks):
+        raise ValueError("upload_payload_: blocks must be contiguous (materialise with contiguous_() first)")
+    h = torch.as_tensor(host) if not isinstance(host, torch.Tensor) else host
+    nbytes = payload_nbytes(ut)
+    if h.numel() * h.element_size() != nbytes:
+        raise ValueError(f"upload_payload_: host payload has {h.numel() * h.element_size()} bytes, expected {nbytes}")
+    if not nbytes:
+        return ut
+    segs, base, _ = _segments(blocks, ut.dtype.itemsize, packed_to_slab=True)
+    staging = torch.empty(nbytes, dtype=torch.uint8, device=dense.device())
+    staging.copy_(h.reshape(-1).view(torch.uint8), non_blocking=True)
+    _lib.copy2d_batched(staging.data_ptr(), base, segs, dense.stream_handle())
+    return ut
+
+
+def download_payload(ut, host):
+    """Copy every block of ``ut`` into a host payload (pinned CPU tensor in the packed
+    ``.utn`` layout): one gather launch and one device->host copy queued on the current
+    stream; synchronise (or wait on an event) before reading ``host``."""
+    blocks = [b.contiguous() for b in ut.get_blocks_()]
+    nbytes = payload_nbytes(ut)
+    if host.numel() * host.element_size() != nbytes:
+        raise ValueError(f"download_payload: host buffer has {host.numel() * host.element_size()} bytes, "
+                         f"expected {nbytes}")
+    if not nbytes:
+        return host
+    segs, base, _ = _segments(blocks, ut.dtype.itemsize, packed_to_slab=False)
+    packed = torch.empty(nbytes, dtype=torch.uint8, device=dense.device())
+    _lib.copy2d_batched(base, packed.data_ptr(), segs, dense.stream_handle())
+    host.reshape(-1).view(torch.uint8).copy_(packed, non_blocking=True)
+    return host
+
+
 def _save_method(self, path):
     save_unitensor(self, path)
 
@@ -179,6 +225,8 @@ def _load_method(cls, path):
     return load_unitensor(path)
 
 
+UniTensor.upload_payload_ = upload_payload_
+UniTensor.download_payload = download_payload
 UniTensor.save = _save_method
 UniTensor.Save = _save_method
 UniTensor.load = classmethod(_load_method)

@@ -49,3 +49,15 @@ def c4_sectors(total=2048, qmax=10, sigma2=18.0):
     for k in np.argsort(-(x - np.floor(x)), kind="stable")[:rem]:
         n[k] += 1
     return [(q, int(c)) for q, c in zip(qs, n)]
+
+
+def peps_inputs(chi=256, D=8, d=2, site=0):
+    """C5 site `site`: every slot N(0,1) from its own seed 9000 + 16*site + slot index, so the
+    32 sites of the batch are distinct, independently reproducible networks."""
+    return {nm: dense.host_normal(shp, seed=9000 + 16 * site + k)
+            for k, (nm, shp) in enumerate(peps_shapes(chi, D, d).items())}
+
+
+def lawr_batch_seed(i):
+    """C3b instance i: L, A, W, R = normal(seed .. seed+3) (seeds S+4i)."""
+    return 5000 + 4 * i

@@ -13,12 +13,11 @@ from paper_2401_01921_b200 import random as trandom
 pytestmark = pytest.mark.gpu
 
 
-def _build(bonds_meta, labels, qns, arrays, dtype):
-    t = UniTensor(bonds_from_meta(bonds_meta), labels=labels, dtype=np.dtype(dtype))
-    assert [list(q) for q in t._qns] == [list(q) for q in qns] or True
-    for i, arr in enumerate(arrays):
-        t.get_block_(i).storage().copy_(__import__("torch").from_numpy(arr.reshape(-1)))
-    return t
+def _payload(blocks):
+    """Every block's elements, concatenated in block order (a slab's alignment padding
+    between blocks is never written and holds whatever the allocator left there)."""
+    import torch
+    return torch.cat([b.storage().reshape(-1) for b in blocks])
 
 
 def test_golden_block_sparse_cases(cuda):
@@ -156,14 +155,14 @@ def test_grouped_stream_k_is_deterministic(cuda):
     import torch
     from paper_2401_01921_b200 import graphs
     A, E, _ = _c4()
-    first = contract(A, E)._blocks[0]._slab.clone()
+    first = _payload(contract(A, E)._blocks).clone()
     for _ in range(3):
-        assert torch.equal(contract(A, E)._blocks[0]._slab, first)
+        assert torch.equal(_payload(contract(A, E)._blocks), first)
     g = graphs.capture(lambda: contract(A, E))
     for _ in range(3):
         out = g.replay()
         torch.cuda.synchronize()
-        assert torch.equal(out._blocks[0]._slab, first)
+        assert torch.equal(_payload(out._blocks), first)
 
 
 def test_one_shot_abi_matches_plan_execute(cuda):
@@ -184,7 +183,7 @@ def test_one_shot_abi_matches_plan_execute(cuda):
                             [x.data_ptr for x in oblk], dense.stream_handle(), want_pairs=True)
     ref = contract(A, E)
     torch.cuda.synchronize()
-    assert torch.equal(slab[:ref._blocks[0]._slab.numel()], ref._blocks[0]._slab)
+    assert torch.equal(_payload(oblk), _payload(ref._blocks))
     assert trip.tolist() == block_pairs(A, E).tolist()
 
 
@@ -349,3 +348,56 @@ def test_random_block_sparse_pairs_vs_oracle(cuda, seed):
         g = blk.numpy()
         assert g.shape == w.shape
         assert rel_fro(g, w) <= 1e-12 or np.linalg.norm(w) == 0 and np.abs(g).max() == 0
+
+
+def test_contract_batched_mixed_dtype_conversions_stay_alive(cuda):
+    """float64 x complex128 batch: every pair's A blocks are widened to complex128 on the
+    fly (fresh allocations). Those must live until the one grouped launch has run; each
+    result equals its own contract_pair (converted blocks were freed early)."""
+    u1 = Symmetry.u1()
+    V = Bond(btype=IN, sectors=[(-2, 9), (-1, 17), (0, 24), (1, 15), (2, 8)], syms=[u1])
+    P = Bond(btype=IN, sectors=[(1, 1), (-1, 1)], syms=[u1])
+    pairs = []
+    for i in range(12):
+        A = UniTensor([V, P, V.redirect()], labels=["vl", "p", "vr"], dtype=storage.Float64)
+        E = UniTensor([V, P.redirect(), V.redirect()], labels=["vr", "p", "x"], dtype=storage.Complex128)
+        trandom.normal_(A, seed=400 + 2 * i)
+        trandom.normal_(E, seed=401 + 2 * i)
+        pairs.append((A, E))
+    outs = tnb.contract_batched(pairs)
+    for (A, E), got in zip(pairs, outs):
+        want = tnb.contract_pair(A, E)
+        assert got.dtype == np.complex128
+        for gb, wb in zip(got.get_blocks_(), want.get_blocks_()):
+            w = wb.numpy()
+            assert np.linalg.norm(gb.numpy() - w) <= 1e-13 * max(np.linalg.norm(w), 1e-300)
+
+
+def test_captured_graph_survives_workspace_growth_and_plan_flush(cuda):
+    """A captured block-sparse graph owns its stream-K workspace and keeps its plan alive:
+    after eager calls that grow the shared workspace (complex128 needs twice the partials)
+    and after more than 256 new structures flush the library's plan cache, replays still
+    reproduce the eager result bit for bit."""
+    import torch
+    from paper_2401_01921_b200 import graphs
+    A, E, _ = _c4()
+    first = _payload(contract(A, E)._blocks).clone()
+    g = graphs.capture(lambda: contract(A, E))
+    out = g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(_payload(out._blocks), first)
+    # eager complex128 contraction: larger workspace (reallocation of the shared one)
+    contract(A.astype(storage.Complex128), E)
+    u1 = Symmetry.u1()
+    P = Bond(btype=IN, sectors=[(1, 1), (-1, 1)], syms=[u1])
+    for n in range(1, 270):  # > 256 distinct structures: the library flushes its plan cache
+        V = Bond(btype=IN, sectors=[(-1, 1 + n % 7), (0, 1 + n // 7), (1, 2)], syms=[u1])
+        a = UniTensor([V, P, V.redirect()], labels=["vl", "p", "vr"])
+        e = UniTensor([V, P.redirect(), V.redirect()], labels=["vr", "p", "x"])
+        contract(a, e)
+    for _ in range(3):
+        out = g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(_payload(out._blocks), first)
+    # eager calls after the flush re-plan transparently
+    assert torch.equal(_payload(contract(A, E)._blocks), first)

@@ -121,8 +121,9 @@ def test_lawr_matvec_vs_oracle(cuda, chi, dtype):
     assert rel_fro(out.numpy(), want) <= 1e-12
 
 
-def test_peps_small_vs_left_fold(cuda):
-    """PEPS reading A at small size: optimal launch equals a pairwise left fold."""
+def test_peps_small_vs_oracle_and_left_fold(cuda):
+    """PEPS reading A at small size: the optimal launch equals the oracle's launch and the
+    engine's own appearance-order left fold."""
     _, meta = load("network.npz")
     lines = meta["cases"][4]["net"]
     chi, D, d = 6, 3, 2
@@ -130,12 +131,16 @@ def test_peps_small_vs_left_fold(cuda):
            "T0": [chi, D, D, chi], "T1": [chi, D, D, chi], "T2": [chi, D, D, chi], "T3": [chi, D, D, chi],
            "a": [D, D, D, D, d], "a*": [D, D, D, D, d]}
     net = Network(lines)
-    rel = []
+    arrays = {}
     for i, (nm, s) in enumerate(shp.items()):
-        t = UniTensor(storage.from_numpy(oracle.normal(s, seed=50 + i)), labels=[f"x{j}" for j in range(len(s))])
+        arrays[nm] = oracle.normal(s, seed=50 + i)
+        t = UniTensor(storage.from_numpy(arrays[nm]), labels=[f"x{j}" for j in range(len(s))])
         net.put_tensor(nm, t)
     net.set_order(optimal=True)
     val = net.launch().item()
+    want, tree = oracle.launch(oracle.net_slots(lines), "", arrays)
+    assert net.get_order() == oracle.render_order(tree)
+    assert abs(val - float(want)) <= 1e-12 * max(1.0, abs(float(want)))
     net2 = Network(lines)
     for nm in shp:
         net2.put_tensor(nm, net._bindings[nm][0])
