@@ -33,16 +33,19 @@ def up_to_date():
     return all(os.path.getmtime(s) <= t for s in sources() + headers())
 
 
-def build(force=False, verbose=False):
-    if not force and up_to_date():
+def build(force=False, verbose=False, defines=(), out=None):
+    """Compile every csrc/ source for sm_100a and link libtnb.so. `defines` / `out` build
+    a variant (e.g. ``-DTNB_X=1`` into build/variant.so) for A/B measurements."""
+    lib = out or LIB
+    if not force and not defines and out is None and up_to_date():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build", os.path.splitext(os.path.basename(lib))[0]) if out else os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", *defines, "-Xcompiler", "-fPIC,-O3",
                "-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj]
         if src.endswith(".cpp"):
             cmd = [NVCC, "-x", "cu", *cmd[1:]]
@@ -58,12 +61,13 @@ def build(force=False, verbose=False):
             sys.stderr.write(f"[tnb build] FAILED: {src}\n")
     if failed:
         raise RuntimeError("libtnb build failed")
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    defs = [a for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[len("--out="):] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs, out=outs[0] if outs else None))

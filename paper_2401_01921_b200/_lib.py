@@ -10,7 +10,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtnb.so")
+LIB_PATH = os.environ.get("TNB_LIB_PATH") or os.path.join(_HERE, "libtnb.so")  # override: dev A/B builds
 
 TNB_OK, TNB_EINVAL, TNB_ECUDA, TNB_ENODEV, TNB_ENOMEM, TNB_EUNSUP = 0, 1, 2, 3, 4, 5
 TNB_F64, TNB_C128, TNB_I64, TNB_BOOL = 0, 1, 2, 3

@@ -207,6 +207,8 @@ class Bond:
         return Bond(btype=self.btype, sectors=list(degs.items()), syms=self.syms)
 
     def combine_(self, other):
+        from .dense import bump_epoch
+        bump_epoch()
         m = self.combine(other)
         self.btype, self.dim, self.sectors, self.syms, self._offsets = m.btype, m.dim, m.sectors, m.syms, None
         return self
@@ -221,6 +223,8 @@ class Bond:
         return b
 
     def redirect_(self):
+        from .dense import bump_epoch
+        bump_epoch()
         if self.btype != REGULAR:
             self.btype = OUT if self.btype == IN else IN
         return self

@@ -140,6 +140,10 @@ def contract_pair(a, b):
         raise TypeError("contract expects UniTensors")
     if a.is_sym != b.is_sym:
         raise ValueError("cannot contract a block-sparse tensor with a dense one; use convert_from first")
+    if a.is_sym:
+        out = _contract_blocks_fast(a, b)  # a structure pair seen (and checked) before
+        if out is not None:
+            return out
     a_pos, b_pos, a_free, b_free, out_labels, out_bonds = _pair_layout(a, b)
     if not a.is_sym:
         return _contract_dense(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds)
@@ -237,6 +241,126 @@ def _widen(blocks, dt):
     return [b if b.dtype == dt else b.astype(dt) for b in blocks]
 
 
+# -- cached block-sparse structure (host fast path) ---------------------------------------------------
+_SIG_IDS = {}          # structure signature -> id (ids are never reused, so stale ids cannot collide)
+_SIG_NEXT = [1]
+
+
+def _bond_key(b):
+    return (b.btype, b.dim, tuple(b.sectors), tuple(b.syms))
+
+
+def _bs_info(t):
+    """(structure id, slab, element offsets, dtype) of a block-sparse tensor whose blocks are
+    all views of ONE slab with ONE common perm -- every tensor the engine itself builds --
+    else None. The structure id stands for (dtype, labels, bonds by
+    value, qn tuples, block storage shapes, perm): equal ids mean the reference's pair checks
+    and the device plan of pair 0 hold for this tensor too. Cached on the tensor until the next
+    in-place metadata mutation anywhere (dense._EPOCH)."""
+    ep = dense._EPOCH[0]
+    c = getattr(t, "_bsc", None)
+    if c is not None and c[0] == ep:
+        return c[1]
+    info = None
+    if t._qns is not None:
+        if t._blk is None:  # lazily held output blocks: contiguous views of one slab
+            slab, base, offs, shapes, isz = t._lazy
+            perm = tuple(range(len(shapes[0]))) if shapes else ()
+            offs = np.asarray(offs, dtype=np.int64) + base
+            sshapes = tuple(shapes)
+        else:
+            blks = t._blk
+            slab = blks[0]._slab if blks else None
+            perm = blks[0]._perm if blks else ()
+            ok = slab is not None and all(b._slab is slab and b._perm == perm for b in blks)
+            if ok:
+                offs = np.fromiter((b._off for b in blks), dtype=np.int64, count=len(blks))
+                sshapes = tuple(b._sshape for b in blks)
+            else:
+                slab = None
+        if slab is not None:
+            dt = dense._NP_OF_TORCH[slab.dtype]
+            sig = (dt.char, tuple(t._labels), tuple(_bond_key(b) for b in t._bonds), tuple(t._qns), sshapes, perm)
+            sid = _SIG_IDS.get(sig)
+            if sid is None:
+                if len(_SIG_IDS) >= 4096:
+                    _SIG_IDS.clear()
+                sid = _SIG_IDS[sig] = _SIG_NEXT[0]
+                _SIG_NEXT[0] += 1
+            info = (sid, slab, offs, dt)
+    t._bsc = (ep, info)
+    return info
+
+
+def _info_ptrs(info):
+    """Device addresses of the blocks of a tensor described by _bs_info (awaits a pending
+    upload into its slab, as block_ptrs does)."""
+    sid, slab, offs, dt = info
+    dense._await(slab)
+    return slab.data_ptr() + offs * dt.itemsize
+
+
+# (structure id of a, structure id of b) -> everything a contraction of that pair of
+# structures needs besides data pointers: the reference's pair checks passed for it once.
+_FAST = {}
+
+
+def _fast_entry(ia, ib):
+    return _FAST.get((ia[0], ib[0])) if ia is not None and ib is not None else None
+
+
+def _remember_fast(ia, ib, plan, lay, shapes, qns, dt):
+    if ia is None or ib is None or ia[3] != dt or ib[3] != dt:
+        return
+    offs, total = _slab_layout_of(shapes, dt)
+    if len(_FAST) >= 512:
+        _FAST.clear()
+    _FAST[(ia[0], ib[0])] = (plan, lay, tuple(shapes), list(qns), {q: i for i, q in enumerate(qns)},
+                             np.asarray(offs, dtype=np.int64), int(max(total, 1)), dt)
+
+
+def _slab_layout_of(shapes, dt):
+    from .labeled import _slab_layout
+    return _slab_layout(tuple(shapes), dt)
+
+
+def _fast_outputs(entry, pairs):
+    """Lazily held results of one structure for every (a, b) in `pairs`, in ONE allocation:
+    (results, pointer table [n][nout]). Each result's bonds are its own a's / b's Bond objects
+    (a_free then b_free), as the reference builds them (contract.py:124)."""
+    plan, lay, shapes, qns, lookup, offs, total, dt = entry
+    n = len(pairs)
+    slab = dense._alloc(total * n, dt)
+    isz = dt.itemsize
+    base = slab.data_ptr()
+    ptrs = base + (np.arange(n, dtype=np.int64)[:, None] * total + offs[None, :]) * isz
+    a_free, b_free, out_labels = lay[2], lay[3], lay[4]
+    offl = offs.tolist()
+    outs = []
+    for i, (a, b) in enumerate(pairs):
+        bonds = [a._bonds[x] for x in a_free] + [b._bonds[x] for x in b_free]
+        outs.append(UniTensor._assemble_lazy(bonds, out_labels, len(a_free), "", (slab, i * total, offl, shapes, isz),
+                                             qns, lookup))
+    return outs, ptrs
+
+
+def _contract_blocks_fast(a, b):
+    """contract_pair of two block-sparse tensors whose structure pair was contracted before:
+    pointer arrays from the cached slab descriptors, cached plan, lazily held output. Returns
+    None when the fast path does not apply (the caller takes the full path)."""
+    ia, ib = _bs_info(a), _bs_info(b)
+    entry = _fast_entry(ia, ib)
+    if entry is None:
+        return None
+    outs, optrs = _fast_outputs(entry, ((a, b),))
+    if not entry[0].execute(_info_ptrs(ia).tolist(), _info_ptrs(ib).tolist(), optrs[0].tolist(),
+                            dense.stream_handle()):
+        _FAST.clear()
+        _BS_PLANS.clear()
+        return None
+    return outs[0]
+
+
 def _contract_blocks(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds, panel_mask=None):
     dt = _result_dtype(a.dtype, b.dtype)
     ablk, aperm = _common_perm(a)
@@ -260,6 +384,9 @@ def _contract_blocks(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds, 
         plan, _ = _bs_plan(dt, a, ablk, aperm, b, bblk, bperm, a_pos, b_pos, out_bonds, qns, panel_mask)
         if not plan.execute(aptrs, bptrs, optrs, dense.stream_handle()):
             raise _lib.EngineError("block-sparse plan went stale twice")
+    if panel_mask is None:
+        _remember_fast(_bs_info(a), _bs_info(b), plan, (a_pos, b_pos, a_free, b_free, out_labels, out_bonds), shapes,
+                       qns, dt)
     return UniTensor._assemble(out_bonds, out_labels, len(a_free), "", oblk, qns)
 
 
@@ -303,6 +430,20 @@ def contract_batched(pairs):
     a0, b0 = pairs[0]
     if not (a0.is_sym and b0.is_sym) or len(pairs) == 1:
         return [contract_pair(a, b) for a, b in pairs]
+    # fast path: every pair has the structure ids of a pair of structures contracted (and
+    # checked) before -> pointer tables straight from the cached slab descriptors
+    ia0, ib0 = _bs_info(a0), _bs_info(b0)
+    entry = _fast_entry(ia0, ib0)
+    if entry is not None:
+        infos = [(_bs_info(a), _bs_info(b)) for a, b in pairs]
+        if all(x is not None and y is not None and x[0] == ia0[0] and y[0] == ib0[0] for x, y in infos):
+            outs, optrs = _fast_outputs(entry, pairs)
+            aps = np.stack([_info_ptrs(x) for x, _ in infos])
+            bps = np.stack([_info_ptrs(y) for _, y in infos])
+            if entry[0].execute_batched(aps, bps, optrs, dense.stream_handle()):
+                return outs
+            _FAST.clear()  # the library flushed its plans: re-plan on the full path
+            _BS_PLANS.clear()
     a_pos, b_pos, a_free, b_free, out_labels, out_bonds = _pair_layout(a0, b0)
     if not out_bonds:
         return [contract_pair(a, b) for a, b in pairs]
@@ -351,6 +492,7 @@ def contract_batched(pairs):
         if not plan.execute_batched(aps, bps, ops, dense.stream_handle()):
             raise _lib.EngineError("block-sparse plan went stale twice")
     del keep  # the launch is queued on the stream: the allocator reuses these only after it
+    _remember_fast(ia0, ib0, plan, (a_pos, b_pos, a_free, b_free, out_labels, out_bonds), shapes, qns, dt)
     return outs
 
 

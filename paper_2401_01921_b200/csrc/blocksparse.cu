@@ -311,6 +311,9 @@ struct BsSK {
   int* flags;  // [G], zero between launches (consumers reset them)
   // dev instrumentation (TNB_BS_TRACE=file): per CTA [kTraceW] int64 of %globaltimer stamps
   long long* trace;
+  // dev experiments (TNB_BS_EXP): bit 0 = producers issue no copies, bit 1 = math warps
+  // issue no DMMA (the skeleton's cost without memory traffic / tensor work)
+  int exp;
 };
 constexpr int kTraceW = 64;
 
@@ -519,7 +522,8 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
             const int krem = Kp - k0;
             if (gi >= STAGES) detail::mbar_wait(&empty[s], ((gi / STAGES) & 1) ^ 1);
             const uint32_t sa = sAbase + s * stA, sbb = sBbase + s * stB;
-            if (krem >= BK) {  // whole k-tile: validity = padding row/col only
+            if (sk.exp & 1) {
+            } else if (krem >= BK) {  // whole k-tile: validity = padding row/col only
 #pragma unroll
               for (int x = 0; x < EA; ++x) {
                 const bool v = oA[x] >= 0;
@@ -644,9 +648,11 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
       // fragments of this warp's 16x16 tile that lie inside the output block
       const TileRef tr = tiles[t];
       const int warp = tid >> 5;
-      const int r0 = tr.m0 + (warp / Cfg::WN) * Core::WTM, c0 = tr.n0 + (warp % Cfg::WN) * Core::WTN;
+      int wm, wn;
+      Base::warp_mn(warp, wm, wn);
+      const int r0 = tr.m0 + wm * Core::WTM, c0 = tr.n0 + wn * Core::WTN;
       const int mfa = (oM[tr.o] - r0 + 7) >> 3, nfa = (oN[tr.o] - c0 + 7) >> 3;
-      Core::consume(As, Bs, full, empty, gi, (int)(e - sb), acc, mfa, nfa);
+      Core::consume(As, Bs, full, empty, gi, (int)(e - sb), acc, (sk.exp & 2) ? 0 : mfa, (sk.exp & 2) ? 0 : nfa);
     }
     if (tr_ && nseg < 14) tr_[4 + 4 * nseg] = gtimer();
     if (e < tend) {
@@ -784,11 +790,13 @@ int launch_bs_one(const BsMeta& meta, const void* const* hp, int nptr, BsSK sk, 
     // the graph owns its workspace (stream-ordered allocation node + flag memset node):
     // a replay never shares flags/partials with eager launches or other graphs, and a
     // later eager call that grows the shared workspace cannot free memory a graph reads
-    TNB_CUDA_CHECK(cudaMallocAsync(&graph_ws, need, st));
+    int rc = capture_device_ws(st, need, &graph_ws);
+    if (rc) return rc;
     TNB_CUDA_CHECK(cudaMemsetAsync(graph_ws, 0, kBsPartialOff, st));
     sk.flags = static_cast<int*>(graph_ws);
     sk.ws = reinterpret_cast<double*>(static_cast<char*>(graph_ws) + kBsPartialOff);
   } else {
+    release_deferred_host();  // memory of destroyed graphs
     PlanCache& C = cur_cache();
     if (C.ws_bytes < need) {
       if (C.ws) {
@@ -805,6 +813,8 @@ int launch_bs_one(const BsMeta& meta, const void* const* hp, int nptr, BsSK sk, 
     sk.ws = reinterpret_cast<double*>(static_cast<char*>(C.ws) + kBsPartialOff);
   }
   sk.trace = nullptr;
+  static const int exp_mode = getenv("TNB_BS_EXP") ? atoi(getenv("TNB_BS_EXP")) : 0;
+  sk.exp = exp_mode;
   static const char* trace_path = getenv("TNB_BS_TRACE");
   if (trace_path && !capturing) {
     TNB_CUDA_CHECK(cudaMallocAsync((void**)&sk.trace, (size_t)G * kTraceW * 8, st));
@@ -817,7 +827,6 @@ int launch_bs_one(const BsMeta& meta, const void* const* hp, int nptr, BsSK sk, 
   count_launch();
   {
     cudaError_t e = cudaGetLastError();
-    if (graph_ws) cudaFreeAsync(graph_ws, st);
     if (e != cudaSuccess) return cuda_fail(e, "bs_contract: grouped GEMM launch");
   }
   if (sk.trace) {

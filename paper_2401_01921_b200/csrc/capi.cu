@@ -119,39 +119,94 @@ bool capturing(cudaStream_t st) {
 }
 
 namespace {
+// memory owned by captured graphs, queued for release by their user objects' destructors
+// (which may not call CUDA): pinned host buffers and device buffers (with their device)
+struct Deferred {
+  void* p;
+  int device;  // -1: pinned host memory
+};
 std::mutex g_deferred_mu;
-std::vector<void*> g_deferred;
-void CUDART_CB queue_host_free(void* p) {
+std::vector<Deferred> g_deferred;
+void CUDART_CB queue_free(void* rec) {
+  Deferred* d = static_cast<Deferred*>(rec);
   std::lock_guard<std::mutex> lk(g_deferred_mu);
-  g_deferred.push_back(p);
+  g_deferred.push_back(*d);
+  delete d;
+}
+
+// Ties `p` to the graph being captured on `st` (a user object the graph retains).
+int tie_to_graph(cudaStream_t st, void* p, int device) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaGraph_t graph = nullptr;
+  TNB_CUDA_CHECK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, nullptr, nullptr));
+  if (cs != cudaStreamCaptureStatusActive || !graph) return fail(TNB_EINVAL, "tie_to_graph: stream is not capturing");
+  Deferred* rec = new Deferred{p, device};
+  cudaUserObject_t obj = nullptr;
+  cudaError_t e = cudaUserObjectCreate(&obj, rec, queue_free, 1, cudaUserObjectNoDestructorSync);
+  if (e != cudaSuccess) {
+    delete rec;
+    return cuda_fail(e, "tie_to_graph: cudaUserObjectCreate");
+  }
+  // the graph takes over our reference: p lives until the graph and every exec made from it die
+  TNB_CUDA_CHECK(cudaGraphRetainUserObject(graph, obj, 1, cudaGraphUserObjectMove));
+  return TNB_OK;
 }
 }  // namespace
 
 void release_deferred_host() {
-  std::vector<void*> q;
+  std::vector<Deferred> q;
   {
     std::lock_guard<std::mutex> lk(g_deferred_mu);
     q.swap(g_deferred);
   }
-  for (void* p : q) cudaFreeHost(p);
+  int cur = -1;
+  for (const Deferred& d : q) {
+    if (d.device < 0) {
+      cudaFreeHost(d.p);
+    } else {
+      if (cur < 0) cudaGetDevice(&cur);
+      cudaSetDevice(d.device);
+      cudaFree(d.p);
+    }
+  }
+  if (cur >= 0) cudaSetDevice(cur);
+  cudaGetLastError();
 }
 
 int capture_pinned(cudaStream_t st, size_t bytes, void** out) {
   *out = nullptr;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  cudaGraph_t graph = nullptr;
-  TNB_CUDA_CHECK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, nullptr, nullptr));
-  if (cs != cudaStreamCaptureStatusActive || !graph) return fail(TNB_EINVAL, "capture_pinned: stream is not capturing");
   void* p = nullptr;
-  TNB_CUDA_CHECK(cudaMallocHost(&p, bytes));
-  cudaUserObject_t obj = nullptr;
-  cudaError_t e = cudaUserObjectCreate(&obj, p, queue_host_free, 1, cudaUserObjectNoDestructorSync);
-  if (e != cudaSuccess) {
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  TNB_CUDA_CHECK(cudaThreadExchangeStreamCaptureMode(&mode));
+  cudaError_t e = cudaMallocHost(&p, bytes);
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  if (e != cudaSuccess) return cuda_fail(e, "capture_pinned: cudaMallocHost");
+  int rc = tie_to_graph(st, p, -1);
+  if (rc) {
     cudaFreeHost(p);
-    return cuda_fail(e, "capture_pinned: cudaUserObjectCreate");
+    return rc;
   }
-  // the graph takes over our reference: p lives until the graph and every exec made from it die
-  TNB_CUDA_CHECK(cudaGraphRetainUserObject(graph, obj, 1, cudaGraphUserObjectMove));
+  *out = p;
+  return TNB_OK;
+}
+
+int capture_device_ws(cudaStream_t st, size_t bytes, void** out) {
+  *out = nullptr;
+  int dev = 0;
+  TNB_CUDA_CHECK(cudaGetDevice(&dev));
+  void* p = nullptr;
+  // cudaMalloc is a "potentially unsafe" call under global-mode capture: relax this
+  // thread's capture mode for the allocation only (it does not touch the stream)
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  TNB_CUDA_CHECK(cudaThreadExchangeStreamCaptureMode(&mode));
+  cudaError_t e = cudaMalloc(&p, bytes);
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  if (e != cudaSuccess) return cuda_fail(e, "capture_device_ws: cudaMalloc");
+  int rc = tie_to_graph(st, p, dev);
+  if (rc) {
+    cudaFree(p);
+    return rc;
+  }
   *out = p;
   return TNB_OK;
 }

@@ -35,7 +35,11 @@ bool capturing(cudaStream_t st);
 // by the next release_deferred_host() call (CUDA API calls are not allowed inside a
 // user-object destructor).
 int capture_pinned(cudaStream_t st, size_t bytes, void** out);
-// Frees queued graph-owned host buffers. Call only outside stream capture.
+// Device memory owned by the graph being captured on `st`, allocated once at capture time
+// (not a per-replay allocation node) and released after the graph is destroyed. Used for
+// stream-K workspaces of captured GEMMs: a replay never shares them with eager launches.
+int capture_device_ws(cudaStream_t st, size_t bytes, void** out);
+// Frees queued graph-owned host / device buffers. Call only outside stream capture.
 void release_deferred_host();
 
 // Counts every kernel this library launches (tnb_launch_count); bench.py reports it.

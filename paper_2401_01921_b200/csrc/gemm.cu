@@ -639,18 +639,18 @@ struct StreamK {
       // graph capture: the graph owns its workspace (a graph replays independently of
       // eager launches on other streams); flags zeroed by a memset node
       void* mem = nullptr;
-      TNB_CUDA_CHECK(cudaMallocAsync(&mem, ws_bytes + (size_t)sk.G * 4 + 64, st));
+      int rc = capture_device_ws(st, ws_bytes + (size_t)sk.G * 4 + 64, &mem);
+      if (rc) return rc;
       sk.ws = static_cast<double*>(mem);
       sk.flags = reinterpret_cast<int*>(static_cast<char*>(mem) + ws_bytes);
-      sk.clear = 0;
+      sk.clear = 1;  // owners reset the flags they consume: clean for the next replay
       cudaError_t e = cudaMemsetAsync(sk.flags, 0, (size_t)sk.G * 4, st);
-      int rc = e != cudaSuccess ? cuda_fail(e, "contract: workspace memset") : dispatch(A, B, C, d, sk, st);
-      cudaFreeAsync(mem, st);
-      return rc;
+      return e != cudaSuccess ? cuda_fail(e, "contract: workspace memset") : dispatch(A, B, C, d, sk, st);
     }
     // eager: one persistent workspace per process whose flags the owners reset, so a
     // launch needs no allocation and no memset; launches from different streams are
     // serialised on it through an event
+    release_deferred_host();  // memory of destroyed graphs
     SkWorkspace& w = sk_workspace();
     std::lock_guard<std::mutex> lk(w.mu);
     int rc = w.acquire(ws_bytes, sk.G, st);

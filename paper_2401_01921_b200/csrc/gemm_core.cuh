@@ -88,6 +88,21 @@ struct TileCore {
 
   using Acc = double[NACC][MF][NF][2];
 
+  // Warp -> (row group, column group) of the CTA tile. With a 4 x 4 warp grid the assignment
+  // is a Latin square over the four SM sub-partitions (warp w issues on SMSP w % 4): every
+  // SMSP holds one warp of each row group and one of each column group, so a tile whose
+  // valid region covers only some row or column groups (block-sparse edge tiles, whose
+  // all-padding fragments skip their DMMAs) still spreads its DMMAs over all four pipes.
+  __device__ __forceinline__ static void warp_mn(int warp, int& wm, int& wn) {
+    if constexpr (WARPS_M == 4 && WARPS_N == 4) {
+      wn = warp >> 2;
+      wm = (warp + wn) & 3;
+    } else {
+      wm = warp / WARPS_N;
+      wn = warp % WARPS_N;
+    }
+  }
+
   __device__ static void zero(Acc& acc) {
 #pragma unroll
     for (int q = 0; q < NACC; ++q)
@@ -110,7 +125,8 @@ struct TileCore {
     int64_t* kOffB = kOffA + KSLOTS * BK;  // [KSLOTS][BK]
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
-    const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+    int wm, wn;
+    warp_mn(warp, wm, wn);
     const int KT = (kend - kbeg + BK - 1) / BK;
 
     for (int i = tid; i < BM; i += NT) rowOffA[i] = (m0 + i < M) ? group_offset(rowA, m0 + i) : -1;
@@ -245,7 +261,8 @@ struct TileCore {
   // C[m, n] (row-major, leading dim ld) = acc for the tile at (m0, n0), clipped to M x N.
   __device__ static void store(T* __restrict__ C, int64_t ld, int m0, int n0, int M, int N, const Acc& acc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+    int wm, wn;
+    warp_mn(warp, wm, wn);
     const int kq = lane & 3;
 #pragma unroll
     for (int i = 0; i < MF; ++i) {
@@ -303,9 +320,13 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
 }
 // A waiting warp may be suspended (up to this hint) instead of re-polling: spinning
 // consumers would otherwise take issue slots from the producer warps on their SMSP.
+#ifndef TNB_MBAR_WAIT
+#define TNB_MBAR_WAIT 0
+#endif
 constexpr uint32_t kSuspendHintNs = 0x989680;
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
+#if TNB_MBAR_WAIT == 0
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
@@ -314,6 +335,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(addr),
       "r"(parity), "r"(kSuspendHintNs));
+#elif TNB_MBAR_WAIT == 1
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity));
+#else
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity));
+#endif
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)));
@@ -374,6 +414,21 @@ struct TileCoreWS {
   static_assert(NMATH % 128 == 0, "math warps must form whole warpgroups");
   static_assert((BM * BK) % NPROD == 0 && (BN * BK) % NPROD == 0, "tile/producer mismatch");
   using Acc = double[NACC][MF][NF][2];
+
+  // Warp -> (row group, column group) of the CTA tile. With a 4 x 4 warp grid the assignment
+  // is a Latin square over the four SM sub-partitions (warp w issues on SMSP w % 4): every
+  // SMSP holds one warp of each row group and one of each column group, so a tile whose
+  // valid region covers only some row or column groups (block-sparse edge tiles, whose
+  // all-padding fragments skip their DMMAs) still spreads its DMMAs over all four pipes.
+  __device__ __forceinline__ static void warp_mn(int warp, int& wm, int& wn) {
+    if constexpr (WARPS_M == 4 && WARPS_N == 4) {
+      wn = warp >> 2;
+      wm = (warp + wn) & 3;
+    } else {
+      wm = warp / WARPS_N;
+      wn = warp % WARPS_N;
+    }
+  }
 
   __device__ static void zero(Acc& acc) { TileCore<CPLX, MODE, BM, BN, BK, WARPS_M, WARPS_N, STAGES>::zero(acc); }
 
@@ -527,7 +582,8 @@ struct TileCoreWS {
     // -------------------------------------------------------------- math warps
     if constexpr (REG_MATH > 0) detail::reg_alloc<REG_MATH>();
     const int lane = tid & 31, warp = tid >> 5;
-    const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+    int wm, wn;
+    warp_mn(warp, wm, wn);
     const int arow = wm * WTM + (lane >> 2);
     const int bcol = wn * WTN + (lane >> 2);
     const int kq = lane & 3;

@@ -108,7 +108,8 @@ struct SKCore {
                                                       int nk, Acc& acc, int mfa, int nfa) {
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
-    const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+    int wm, wn;
+    Base::warp_mn(warp, wm, wn);
     const int arow = wm * WTM + (lane >> 2);
     const int bcol = wn * WTN + (lane >> 2);
     const int kq = lane & 3;

@@ -401,3 +401,96 @@ def test_captured_graph_survives_workspace_growth_and_plan_flush(cuda):
         assert torch.equal(_payload(out._blocks), first)
     # eager calls after the flush re-plan transparently
     assert torch.equal(_payload(contract(A, E)._blocks), first)
+
+
+def test_cached_structure_fast_path_follows_mutations(cuda):
+    """Repeated contractions of an already-seen structure pair take the host fast path
+    (cached slab descriptors / plan, lazily held outputs). In-place metadata mutations
+    (put_block_, relabel_, redirect_) must invalidate it; lazily held outputs feed later
+    contractions correctly; output bonds are the operands' own Bond objects."""
+    import torch
+    u1 = Symmetry.u1()
+    V = Bond(btype=IN, sectors=[(-1, 5), (0, 9), (1, 6)], syms=[u1])
+    P = Bond(btype=IN, sectors=[(1, 1), (-1, 1)], syms=[u1])
+
+    def mk(seed):
+        A = UniTensor([V, P, V.redirect()], labels=["vl", "p", "vr"])
+        E = UniTensor([V, P.redirect(), V.redirect()], labels=["vr", "p", "x"])
+        trandom.normal_(A, seed=seed)
+        trandom.normal_(E, seed=seed + 1)
+        return A, E
+
+    def dense_of(t):
+        return np.concatenate([b.numpy().reshape(-1) for b in t.get_blocks_()])
+
+    A, E = mk(11)
+    r1 = contract(A, E)             # full path; remembers the structure pair
+    r2 = contract(A, E)             # fast path
+    assert np.array_equal(dense_of(r1), dense_of(r2))
+    assert r2.bonds[0] is A.bonds[0] and r2.bonds[1] is E.bonds[2]
+    # put_block_: a new buffer for block 3 -> the slab descriptor is stale
+    blk = A.get_block(3)
+    blk.storage().mul_(-2.0)
+    A.put_block_(blk, 3)
+    ref = contract(A.clone(), E)
+    assert np.allclose(dense_of(contract(A, E)), dense_of(ref), rtol=1e-13, atol=1e-13)
+    assert not np.allclose(dense_of(ref), dense_of(r1))
+    # relabel_: the contracted label set changes -> a different structure
+    A2, E2 = mk(21)
+    contract(A2, E2)
+    contract(A2, E2)
+    E2.relabel_(["vr", "q", "x"])  # p no longer shared: only vr is contracted now
+    got = contract(A2, E2)
+    want = contract(A2.clone(), E2.clone())
+    assert got.labels == want.labels == ["vl", "p", "q", "x"]
+    assert np.array_equal(dense_of(got), dense_of(want))
+    # lazily held outputs as inputs of the next contraction (and of a batch)
+    A3, E3 = mk(31)
+    out = contract(A3, E3)
+    out2 = contract(A3, E3)
+    X = UniTensor([V, V.redirect()], labels=["x", "y"])
+    trandom.normal_(X, seed=5)
+    want = contract(out.clone(), X)
+    got = contract(out2, X)
+    assert np.allclose(dense_of(got), dense_of(want), rtol=1e-13, atol=1e-13)
+    outs = tnb.contract_batched([(out2, X), (out, X)])
+    for o in outs:
+        assert np.allclose(dense_of(o), dense_of(want), rtol=1e-13, atol=1e-13)
+    # redirect_ of a shared bond object flips the directions -> checks fail, no stale reuse
+    A4, E4 = mk(41)
+    contract(A4, E4)
+    contract(A4, E4)
+    A4.bonds[1].redirect_()
+    with pytest.raises(ValueError):
+        contract(A4, E4)
+    A4.bonds[1].redirect_()
+    torch.cuda.synchronize()
+
+
+def test_graph_owned_workspaces_are_released(cuda):
+    """Each captured grouped GEMM owns its stream-K workspace (allocated at capture, tied to
+    the graph); destroying the graphs releases it on the next eager launch, so repeated
+    capture / destroy does not grow device memory."""
+    import gc
+    import torch
+    from paper_2401_01921_b200 import graphs
+    A, E, _ = _c4()
+    contract(A, E)
+    torch.cuda.synchronize()
+
+    def cycle():
+        g = graphs.capture(lambda: contract(A, E), warmup=1)
+        g.replay()
+        torch.cuda.synchronize()
+        del g
+        gc.collect()
+        contract(A, E)  # eager launch: frees workspaces of destroyed graphs
+        torch.cuda.synchronize()
+    cycle()
+    torch.cuda.empty_cache()
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(12):
+        cycle()
+    torch.cuda.empty_cache()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < (24 << 20), (free0, free1)  # 12 x 4.9 MB would leak ~59 MB
