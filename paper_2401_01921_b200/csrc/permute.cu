@@ -529,12 +529,96 @@ __global__ void __launch_bounds__(256) permute_t2d_kernel(const typename Word<ES
   }
 }
 
+// Fast path 2b -- the same 2-D transpose with CTA-wide tiles of 512-byte runs on BOTH
+// sides (64 x 64 float64, 32 x 32 complex128): every input row segment and every output
+// row segment a CTA touches is 512 contiguous bytes moved by 16-byte vector accesses, so a
+// DRAM page opened for a tile serves 4x more bytes than with the 128-byte runs of the
+// warp tiles above (the transposes whose two inner axes lie far apart in memory were
+// row-activation bound there). Needs Di, Do >= the tile and 16-byte aligned rows.
+template <int ES>
+struct WideCfg {
+  static constexpr int T = ES == 8 ? 64 : 32;  // 512-byte runs
+  static constexpr int V = 16 / ES;            // elements per 16-byte vector
+  static constexpr int LD = T + 1;             // padded smem row (elements)
+};
+
+template <int ES>
+__global__ void __launch_bounds__(256) permute_t2w_kernel(const typename Word<ES>::T* __restrict__ src,
+                                                          typename Word<ES>::T* __restrict__ dst,
+                                                          const __grid_constant__ T2Desc d) {
+  using W = typename Word<ES>::T;
+  constexpr int T = WideCfg<ES>::T, V = WideCfg<ES>::V, LD = WideCfg<ES>::LD;
+  constexpr int LANES_PER_ROW = T / V;          // 32: one row = one warp instruction
+  constexpr int ROWS_PER_WARP = T / 8;          // 8 warps share the tile's rows
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  W* tile = reinterpret_cast<W*>(smem_raw);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  static_assert(LANES_PER_ROW == 32, "one 512-byte row per warp instruction");
+  for (int64_t t = blockIdx.x; t < d.ntiles; t += gridDim.x) {
+    uint32_t q = (uint32_t)t;
+    uint32_t qi = d.ti_div.div(q);
+    const int64_t it = q - qi * (uint32_t)d.ti;
+    uint32_t qj = d.tj_div.div(qi);
+    const int64_t jt = qi - qj * (uint32_t)d.tj;
+    int64_t bin = 0, bout = 0;
+    uint32_t rem = qj;
+    for (int k = d.nb - 1; k >= 0; --k) {
+      uint32_t quo = d.bdiv[k].div(rem);
+      int64_t dig = rem - quo * (uint32_t)d.bdim[k];
+      rem = quo;
+      bin += dig * d.bistr[k];
+      bout += dig * d.bostr[k];
+    }
+    const int64_t i0 = it * T, j0 = jt * T;
+    const W* s = src + bin + i0 + j0 * d.sj;
+    W* o = dst + bout + j0 + i0 * d.si;
+    if ((i0 + T <= d.Di) && (j0 + T <= d.Do)) {
+      // read: rows j (input-contiguous along i), 16-byte vectors, all loads in flight
+      uint4 v[ROWS_PER_WARP];
+#pragma unroll
+      for (int k = 0; k < ROWS_PER_WARP; ++k) {
+        const int j = warp * ROWS_PER_WARP + k;
+        v[k] = __ldcs(reinterpret_cast<const uint4*>(s + (int64_t)j * d.sj) + lane);
+      }
+#pragma unroll
+      for (int k = 0; k < ROWS_PER_WARP; ++k) {
+        const int j = warp * ROWS_PER_WARP + k;
+        const W* e = reinterpret_cast<const W*>(&v[k]);
+#pragma unroll
+        for (int u = 0; u < V; ++u) tile[j * LD + lane * V + u] = e[u];
+      }
+      __syncthreads();
+      // write: rows i (output-contiguous along j)
+#pragma unroll
+      for (int k = 0; k < ROWS_PER_WARP; ++k) {
+        const int i = warp * ROWS_PER_WARP + k;
+        uint4 w;
+        W* e = reinterpret_cast<W*>(&w);
+#pragma unroll
+        for (int u = 0; u < V; ++u) e[u] = tile[(lane * V + u) * LD + i];
+        __stcs(reinterpret_cast<uint4*>(o + (int64_t)i * d.si) + lane, w);
+      }
+      __syncthreads();
+    } else {
+      for (int x = threadIdx.x; x < T * T; x += blockDim.x) {
+        const int j = x / T, i = x % T;
+        if (i0 + i < d.Di && j0 + j < d.Do) tile[j * LD + i] = s[i + (int64_t)j * d.sj];
+      }
+      __syncthreads();
+      for (int x = threadIdx.x; x < T * T; x += blockDim.x) {
+        const int i = x / T, j = x % T;
+        if (j0 + j < d.Do && i0 + i < d.Di) o[j + (int64_t)i * d.si] = tile[j * LD + i];
+      }
+      __syncthreads();
+    }
+  }
+}
 
 struct Plan {
   bool identity = false;
   int64_t nelem = 0;
   int kind = 0;  // 0 generic tiled, 1 rows, 2 transpose2d
-  int t2d_T = 0;
+  int t2d_T = 0;  // 16 / 8: warp tiles; 0 with kind 2 never; -1: CTA-wide tiles (t2w)
   PermDesc d;
   RowDesc rd;
   T2Desc td;
@@ -634,7 +718,8 @@ int make_plan(int es, int rank, const int64_t* shape, const int32_t* perm, Plan&
       p.kind = 1;
       return TNB_OK;
     }
-    if (a_si != a_so && mdim[a_si] * es >= 64 && mdim[a_so] * es >= 64 && (es == 8 || es == 16)) {
+    static const bool force_tiled = getenv("TNB_PERM_TILED") != nullptr;  // dev A/B
+    if (!force_tiled && a_si != a_so && mdim[a_si] * es >= 64 && mdim[a_so] * es >= 64 && (es == 8 || es == 16)) {
       T2Desc& td = p.td;
       memset(&td, 0, sizeof(td));
       // 16 x 16 tiles (128-byte runs for f64, 256-byte for c128): measured 0.87-0.95 of
@@ -642,6 +727,20 @@ int make_plan(int es, int rank, const int64_t* shape, const int32_t* perm, Plan&
       // no tail wave, more tiles in flight per SM)
       int T = 16;
       if (es == 16 && (mdim[a_si] < 16 || mdim[a_so] < 16)) T = 8;
+      // CTA-wide 512-byte-run tiles when both inner axes span a tile and every row start
+      // stays 16-byte aligned (all input/output strides even in float64 elements)
+      const int TW = es == 8 ? 64 : 32;
+      bool wide = mdim[a_si] >= TW && mdim[a_so] >= TW;
+      if (wide && es == 8) {
+        wide = mis[a_so] % 2 == 0 && mos[a_si] % 2 == 0;
+        for (int k = 0; k < r; ++k) {
+          int a = o2s[k];
+          if (a != a_si && a != a_so && (mis[a] % 2 || mos[a] % 2)) wide = false;
+        }
+      }
+      static const int t_env = getenv("TNB_T2D_T") ? atoi(getenv("TNB_T2D_T")) : 0;  // dev A/B
+      if (t_env == 16) wide = false;
+      if (wide) T = TW;
       td.Di = mdim[a_si];
       td.Do = mdim[a_so];
       td.sj = mis[a_so];
@@ -663,7 +762,7 @@ int make_plan(int es, int rank, const int64_t* shape, const int32_t* perm, Plan&
           td.nb++;
         }
         p.kind = 2;
-        p.t2d_T = T;
+        p.t2d_T = wide ? -1 : T;
         return TNB_OK;
       }
     }
@@ -838,6 +937,27 @@ int launch_t2d(const void* src, void* dst, const Plan& p, cudaStream_t st) {
 }
 
 template <int ES>
+int launch_t2w(const void* src, void* dst, const Plan& p, cudaStream_t st) {
+  using W = typename Word<ES>::T;
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) != 0)
+    return -1;  // caller falls back to the warp-tile kernel
+  auto kern = permute_t2w_kernel<ES>;
+  constexpr int T = WideCfg<ES>::T, LD = WideCfg<ES>::LD;
+  const size_t smem = (size_t)T * LD * ES;
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    TNB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TNB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int64_t grid = std::min<int64_t>(p.td.ntiles, (int64_t)sm_count() * per_sm);
+  kern<<<(unsigned)grid, 256, smem, st>>>(static_cast<const W*>(src), static_cast<W*>(dst), p.td);
+  count_launch();
+  TNB_CUDA_CHECK(cudaGetLastError());
+  return TNB_OK;
+}
+
+template <int ES>
 int launch_rows_bulk(const void* src, void* dst, const Plan& p, cudaStream_t st) {
   auto kern = permute_rows_bulk_kernel<ES>;
   const size_t smem = (size_t)kBulkWarps * kBulkStages * kBulkStage;
@@ -888,6 +1008,22 @@ template <int ES>
 int launch(const void* src, void* dst, const Plan& p, cudaStream_t st) {
   if (p.kind == 1) return launch_rows<ES>(src, dst, p, st);
   if (p.kind == 2) {
+    if constexpr (ES == 8 || ES == 16) {
+      if (p.t2d_T == -1) {
+        int rc = launch_t2w<ES>(src, dst, p, st);
+        if (rc != -1) return rc;
+        // unaligned base pointers: warp tiles over the same descriptor (tile sides 16 / 8)
+        Plan q = p;
+        const int Tn = 16;
+        q.td.ti = (q.td.Di + Tn - 1) / Tn;
+        q.td.tj = (q.td.Do + Tn - 1) / Tn;
+        q.td.ntiles = q.td.ntiles / ((p.td.Di + WideCfg<ES>::T - 1) / WideCfg<ES>::T) /
+                      ((p.td.Do + WideCfg<ES>::T - 1) / WideCfg<ES>::T) * q.td.ti * q.td.tj;
+        q.td.ti_div = FastDiv((uint32_t)q.td.ti);
+        q.td.tj_div = FastDiv((uint32_t)q.td.tj);
+        return launch_t2d<ES, 16>(src, dst, q, st);
+      }
+    }
     if constexpr (ES == 8) return launch_t2d<8, 16>(src, dst, p, st);
     if constexpr (ES == 16) {
       if (p.t2d_T == 16) return launch_t2d<16, 16>(src, dst, p, st);
