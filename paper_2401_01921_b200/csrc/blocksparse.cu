@@ -822,7 +822,7 @@ int launch_bs_one(const BsMeta& meta, const void* const* hp, int nptr, BsSK sk, 
   }
   {
     KTimer kt(TNB_KF_BS_GEMM, st, 0.0);
-    kern<<<G, Core::NT, smem, st>>>(meta, pt, sk);
+    TNB_CUDA_CHECK(launch_cooperative(kern, (unsigned)G, (unsigned)Core::NT, smem, st, meta, pt, sk));
   }
   count_launch();
   {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "../../include/tnb.h"
@@ -59,6 +60,28 @@ struct KTimer {
   double work;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
+
+// Launches a persistent kernel whose CTAs wait on one another (stream-K partial
+// hand-offs: an owner spins on the flags of its predecessor CTAs) with the COOPERATIVE
+// attribute: the driver co-schedules every CTA of the grid (or rejects the launch), so an
+// owner never waits on a CTA that cannot be dispatched because other kernels -- NCCL
+// collectives, work on other streams -- hold SMs. The attribute survives graph capture.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_cooperative(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                               cudaStream_t st, Args&&... args) {
+  static const bool off = getenv("TNB_NO_COOP") != nullptr;  // dev A/B switch
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
+}
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 

@@ -590,8 +590,8 @@ struct StreamK {
     }
     {
       KTimer kt(TNB_KF_GEMM, st, 2.0 * d.M * (double)d.N * d.K * (CPLX ? 4 : 1));
-      kern<<<sk.G, Core::NT, Core::kSmem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B),
-                                                static_cast<T*>(C), d, sk);
+      TNB_CUDA_CHECK(launch_cooperative(kern, (unsigned)sk.G, (unsigned)Core::NT, Core::kSmem, st,
+                                        static_cast<const T*>(A), static_cast<const T*>(B), static_cast<T*>(C), d, sk));
     }
     count_launch();
     TNB_CUDA_CHECK(cudaGetLastError());

@@ -247,3 +247,29 @@ def test_streamk_workspace_across_streams_and_graphs(cuda):
     for st, o in outs:
         got = o.numpy()
         assert np.array_equal(got, ref), "stream-K result differs across streams / graph replays"
+
+
+@pytest.mark.timeout(300)
+def test_stream_k_gemms_run_beside_a_long_kernel_stream(cuda):
+    """The persistent stream-K GEMMs (dense and grouped block-sparse) hand partials between
+    CTAs; they are launched cooperatively, so they are co-scheduled as a whole even while
+    another stream keeps SMs busy with long kernels. Results stay exact and nothing hangs."""
+    import torch
+    import bench
+    inp = oracle.lawr_inputs(96, seed=8)
+    want, _ = oracle.launch(oracle.lawr_slots(), "b, q, b2", inp)
+    net, _ = bench.make_network(tnb, oracle.LAWR_NET, inp)
+    A, E = bench.c4_tensors(tnb, seed=5)
+    ref_bs = [b.numpy() for b in tnb.contract(A, E).get_blocks_()]
+    side = torch.cuda.Stream()
+    x = torch.randn(4096, 4096, dtype=torch.float64, device=cuda)
+    with torch.cuda.stream(side):
+        for _ in range(12):  # ~0.1 s of DGEMMs occupying every SM, queued ahead
+            y = x @ x
+    for _ in range(5):
+        out = net.launch().numpy()
+        got_bs = [b.numpy() for b in tnb.contract(A, E).get_blocks_()]
+    torch.cuda.synchronize()
+    assert rel_fro(out, want) <= 1e-12
+    assert all(np.array_equal(g, w) for g, w in zip(got_bs, ref_bs))
+    del y

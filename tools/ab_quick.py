@@ -48,3 +48,9 @@ if "lawr" in what:
         macs, _ = bench.lawr_macs(tnb, 1024)
         fl = macs * (8 if dt == np.complex128 else 2)
         print(f"[{tag}] lawr1024 {np.dtype(dt).name} gemm {g:.3f} ms launch {w:.3f} ms ({fl / w / 1e9:.0f} GF/s)")
+if "c1" in what:
+    net, _ = bench.make_network(tnb, WL.LAWR_NET, WL.lawr_inputs(128))
+    g, w = ktime(net.launch, tnb._lib.KF_GEMM, 50)
+    cn = net.compile()
+    _, wg = ktime(cn.launch, tnb._lib.KF_GEMM, 50)
+    print(f"[{tag}] C1 chi128: gemm {g * 1e3:.1f} us/launch, eager launch {w * 1e3:.1f} us, graph {wg * 1e3:.1f} us")
