@@ -135,9 +135,10 @@ int tnb_copy2d_batched(const void* src, void* dst, int64_t nseg, const TnbCopy2D
  * with ldb = n, ldq = m for complex128 and both rounded up to even for float64
  * (16-byte rows); outputs the thin factors in torch/LAPACK layout
  * u (m x m row-major), s (m, descending), vh (m x n row-major) and *status:
- * sweeps used (> 0), -1 not converged within max_sweeps, -2 rank deficient
- * (a singular value <= rank_tol * max: its v row cannot be normalised; the
- * caller recomputes that sector). A row pair is rotated while
+ * sweeps used (> 0) or -1 (not converged within max_sweeps). Rank-deficient
+ * sectors (singular values <= rank_tol * max) are handled in the kernel: their
+ * vh rows are completed to an orthonormal basis of the complement of the kept
+ * rows (two-pass Gram-Schmidt), as LAPACK completes V. A row pair is rotated while
  * |b_p.b_q| > tol * sqrt(n) * eps * |b_p||b_q| (eps = 2^-52).
  * One thread-block cluster per sector, all sectors in one launch. */
 typedef struct {

@@ -19,8 +19,11 @@
 // run concurrently, one cluster each. The finalize pass (same kernel) ranks the
 // singular values (descending, ties by row) and writes the torch-compatible thin
 // factors U (m x m), S (m), Vh (m x n). Rows with sigma below rank_tol * sigma_max
-// cannot be normalised into an orthonormal V: such sectors are flagged (status -2)
-// and the host recomputes them with the library factorisation.
+// (rank-deficient sectors: product states, degenerate wavefunctions) cannot be normalised
+// into V rows; their Vh rows are completed in the same kernel to an orthonormal basis of
+// the complement of the kept rows (deterministic pseudo-random starts, two-pass Gram-Schmidt
+// against every earlier row, cluster-wide), as LAPACK's gesdd completes V. U = Q^H is
+// unitary whatever the rank, so U S Vh = A and both factors stay orthonormal.
 #include <cmath>
 #include <vector>
 
@@ -43,6 +46,7 @@ struct SvdTask {
   int* status;     // [1] out: sweeps used (>0), -1 not converged, -2 rank deficient
   int* counter;    // [2] rotation counters (zero on entry)
   double* norm;    // [m] scratch: |b_i|
+  double* coef;    // [2m + 2] scratch: Gram-Schmidt coefficients (re, im) + the candidate's norm
   int m, n;
 };
 
@@ -138,6 +142,92 @@ __device__ __forceinline__ bool rotation(double al, double be, double gre, doubl
   c = 1.0 / sqrt(1.0 + tt * tt);
   s = c * tt;
   return true;
+}
+
+// deterministic pseudo-random value in [-1, 1) (splitmix64 of the key)
+__device__ __forceinline__ double rnd_unit(uint64_t key) {
+  uint64_t z = key + 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+}
+
+// Orthonormal completion of Vh rows [r0, m): row r starts from a pseudo-random vector,
+// is orthogonalised (twice) against rows 0 .. r-1 and normalised; all warps of the
+// cluster cooperate on every step (rows are sequentially dependent).
+template <bool CPLX>
+__device__ void complete_rows(typename Sc<CPLX>::T* __restrict__ VH, int r0, int m, int n, double* coef, int gw,
+                              int lane) {
+  using S = Sc<CPLX>;
+  using T = typename S::T;
+  constexpr int NW = kCluster * kWarps;
+  const int gt = gw * 32 + lane;
+  for (int r = r0; r < m; ++r) {
+    T* v = VH + (int64_t)r * n;
+    for (int attempt = 0; attempt < 8; ++attempt) {
+      for (int j = gt; j < n; j += NW * 32) {
+        const uint64_t key = ((uint64_t)r << 40) ^ ((uint64_t)attempt << 32) ^ (uint64_t)j;
+        if constexpr (CPLX) stcg(v + j, make_double2(rnd_unit(key), rnd_unit(key ^ 0x5555555555555555ull)));
+        else stcg(v + j, rnd_unit(key));
+      }
+      cluster_sync_all();
+      double before = 0.0;
+      for (int pass = 0; pass < 2; ++pass) {
+        // coefficients <v_k, v> of the earlier rows (a warp per row)
+        for (int k = gw; k < r; k += NW) {
+          double re = 0.0, im = 0.0;
+          for (int j = lane; j < n; j += 32) S::dot(re, im, ldcg(VH + (int64_t)k * n + j), ldcg(v + j));
+          re = warp_sum(re);
+          if constexpr (CPLX) im = warp_sum(im);
+          if (lane == 0) {
+            __stcg(coef + 2 * k, re);
+            __stcg(coef + 2 * k + 1, im);
+          }
+        }
+        if (pass == 0 && gw == 0) {  // the candidate's norm before projection
+          double x2 = 0.0;
+          for (int j = lane; j < n; j += 32) x2 += S::abs2(ldcg(v + j));
+          x2 = warp_sum(x2);
+          if (lane == 0) __stcg(coef + 2 * m, x2);
+        }
+        cluster_sync_all();
+        if (pass == 0) before = __ldcg(coef + 2 * m);
+        // v -= sum_k <v_k, v> v_k   (a thread per element)
+        for (int j = gt; j < n; j += NW * 32) {
+          T x = ldcg(v + j);
+          for (int k = 0; k < r; ++k) {
+            const double cr = __ldcg(coef + 2 * k), ci = __ldcg(coef + 2 * k + 1);
+            const T y = ldcg(VH + (int64_t)k * n + j);
+            if constexpr (CPLX) {
+              x.x -= cr * y.x - ci * y.y;
+              x.y -= cr * y.y + ci * y.x;
+            } else {
+              x -= cr * y;
+            }
+          }
+          stcg(v + j, x);
+        }
+        cluster_sync_all();
+      }
+      if (gw == 0) {
+        double x2 = 0.0;
+        for (int j = lane; j < n; j += 32) x2 += S::abs2(ldcg(v + j));
+        x2 = warp_sum(x2);
+        if (lane == 0) __stcg(coef + 2 * m + 1, x2);
+      }
+      cluster_sync_all();
+      const double after = __ldcg(coef + 2 * m + 1);
+      // accept unless the start lay (numerically) inside the span of the earlier rows
+      const bool ok = after > 1e-6 * before && after > 0.0;
+      if (ok) {
+        const double inv = 1.0 / sqrt(after);
+        for (int j = gt; j < n; j += NW * 32) stcg(v + j, S::scale(inv, ldcg(v + j)));
+      }
+      cluster_sync_all();
+      if (ok) break;
+    }
+  }
 }
 
 template <bool CPLX>
@@ -351,7 +441,12 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32)
   for (int k = lane; k < m; k += 32) smax = fmax(smax, __ldcg(t.norm + k));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
-  bool deficient = false;
+  // rows whose sigma is below rank_tol * sigma_max (they rank last): their Vh rows are
+  // completed below instead of normalised
+  int nd = 0;
+  for (int k = lane; k < m; k += 32) nd += __ldcg(t.norm + k) <= rank_tol * smax ? 1 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nd += __shfl_xor_sync(0xffffffffu, nd, o);
   for (int i = gw; i < m; i += NW) {
     const double si = __ldcg(t.norm + i);
     int rank = 0;
@@ -361,17 +456,16 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32)
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
-    if (si <= rank_tol * smax) deficient = true;
     if (lane == 0) t.s[rank] = si;
-    const double inv = si > 0.0 ? 1.0 / si : 0.0;
-    for (int j = lane; j < n; j += 32) VH[(int64_t)rank * n + j] = S::scale(inv, ldcg(B + (int64_t)i * ldb + j));
+    if (rank < m - nd) {
+      const double inv = 1.0 / si;
+      for (int j = lane; j < n; j += 32) stcg(VH + (int64_t)rank * n + j, S::scale(inv, ldcg(B + (int64_t)i * ldb + j)));
+    }
     for (int j = lane; j < m; j += 32) U[(int64_t)j * m + rank] = S::conj(ldcg(Q + (int64_t)i * ldq + j));
   }
-  if (deficient && lane == 0) atomicExch(t.status, -2);
   cluster_sync_all();
-  if (crank == 0 && threadIdx.x == 0) {
-    if (atomicAdd(t.status, 0) != -2) *t.status = status;
-  }
+  if (nd > 0) complete_rows<CPLX>(VH, m - nd, m, n, t.coef, gw, lane);
+  if (crank == 0 && threadIdx.x == 0) *t.status = status;
 }
 
 template <bool CPLX>
@@ -411,20 +505,22 @@ extern "C" int tnb_svd_jacobi_batched(int dtype, int nsec, const TnbSvdSector* s
     const TnbSvdSector& x = secs[i];
     if (x.m < 1 || x.n < x.m || !x.a || !x.b || !x.q || !x.u || !x.s || !x.vh || !x.status)
       return fail(TNB_EINVAL, "svd_jacobi: sector needs 1 <= m <= n and all buffers");
-    h[i] = {x.a, x.b, x.q, x.u, static_cast<double*>(x.s), x.vh, x.status, nullptr, nullptr, (int)x.m, (int)x.n};
+    h[i] = {x.a, x.b, x.q, x.u, static_cast<double*>(x.s), x.vh, x.status, nullptr, nullptr, nullptr, (int)x.m,
+            (int)x.n};
     msum += x.m;
     work += 2.0 * x.m * (double)x.m * x.n;
   }
   // device task table + rotation counters + norm scratch in one allocation
   const size_t tb = sizeof(SvdTask) * (size_t)nsec, cb = sizeof(int) * 2 * (size_t)nsec;
-  const size_t nb = sizeof(double) * (size_t)msum;
+  const size_t nb = sizeof(double) * (size_t)(3 * msum + 2 * nsec);  // norms [m] + coefficients [2m + 2]
   void* mem = nullptr;
   TNB_CUDA_CHECK(cudaMallocAsync(&mem, tb + nb + cb, st));
   double* norms = reinterpret_cast<double*>(static_cast<char*>(mem) + tb);
   int* counters = reinterpret_cast<int*>(static_cast<char*>(mem) + tb + nb);
-  for (int i = 0, off = 0; i < nsec; off += (int)secs[i].m, ++i) {
+  for (int i = 0, off = 0; i < nsec; off += 3 * (int)secs[i].m + 2, ++i) {
     h[i].counter = counters + 2 * i;
     h[i].norm = norms + off;
+    h[i].coef = norms + off + secs[i].m;
   }
   cudaError_t e = cudaMemcpyAsync(mem, h.data(), tb, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(counters, 0, cb, st);

@@ -153,9 +153,10 @@ def _row_charge(row_bonds, row_qn, syms):
 
 
 # sector matrices go through the engine's batched Jacobi kernel (tnb_svd_jacobi_batched: one
-# thread-block cluster per sector, all sectors in one launch); any sector the kernel flags
-# (not converged / rank deficient) through the library factorisation. "library" forces the
-# latter for everything.
+# thread-block cluster per sector, all sectors in one launch; rank-deficient sectors are
+# completed in the kernel). A sector the kernel reports as not converged within its sweep
+# budget (never observed) is refactorised by the library; "library" forces the latter for
+# everything (A/B measurements only).
 SVD_BACKEND = "jacobi"
 
 

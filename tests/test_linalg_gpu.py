@@ -154,8 +154,8 @@ def test_reference_truncation_rules(cuda):
 def test_jacobi_kernel_vs_library(cuda):
     """The engine's batched Jacobi kernel (float64 default) and the library path agree:
     singular values to 1e-12 relative, factors reconstruct and are isometries; tall and wide
-    sectors (tnb_permute transposes), odd row counts, a rank-deficient sector (flagged ->
-    library recompute)."""
+    sectors (tnb_permute transposes), odd row counts, a rank-deficient sector (completed in
+    the kernel)."""
     import torch
     from paper_2401_01921_b200 import linalg as L
     rng = np.random.default_rng(3)
@@ -221,3 +221,50 @@ def test_jacobi_kernel_converges_without_fallback(cuda, dt):
         rec = U @ np.diag(s.cpu().numpy()) @ V
         assert np.linalg.norm(rec - a) <= 1e-12 * np.linalg.norm(a)
         assert np.linalg.norm(U.conj().T @ U - np.eye(U.shape[1])) <= 1e-12
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.complex128])
+def test_rank_deficient_sectors_complete_in_kernel(cuda, dt, monkeypatch):
+    """Rank-deficient sectors (a product-state two-site wavefunction: every sector matrix is
+    rank <= 1; plus a rank-3 dense matrix and an all-zero sector) are factorised by the
+    engine kernel alone -- the library path must never be called: singular values match
+    LAPACK, U S Vh reconstructs, U and Vh are orthonormal (Vh's null rows completed)."""
+    import torch
+    from paper_2401_01921_b200 import linalg as L
+
+    def boom(view):
+        raise AssertionError("library SVD fallback called")
+    monkeypatch.setattr(L, "_library_svd", boom)
+    rng = np.random.default_rng(12)
+
+    def rnd(*shape):
+        x = rng.standard_normal(shape)
+        return x if dt == np.float64 else x + 1j * rng.standard_normal(shape)
+    # dense rank-3 and all-zero matrices
+    for a in (rnd(20, 3) @ rnd(3, 24), np.zeros((6, 9), dtype=dt)):
+        t = UniTensor(storage.from_numpy(np.ascontiguousarray(a.astype(dt))), labels=["r", "c"], rowrank=1)
+        s, u, v = L.svd(t)
+        want = np.linalg.svd(a, compute_uv=False)
+        got = np.diag(s.get_block_().numpy())
+        assert np.max(np.abs(got - want)) <= 1e-12 * max(want[0], 1.0)
+        _check_factors(t, s, u, v)
+    # a U(1) product state: block (kl, k1, k2, kr) = l[kl, k1] (x) r[k2, kr], so every charge
+    # sector matrix (rows (vl, p1), columns (p2, vr)) is an outer product: rank <= 1
+    u1 = Symmetry.u1()
+    V = Bond(btype=IN, sectors=[(-1, 6), (0, 9), (1, 5)], syms=[u1])
+    P = Bond(btype=IN, sectors=[(1, 1), (-1, 1)], syms=[u1])
+    psi = UniTensor([V, P, P, V.redirect()], labels=["vl", "p1", "p2", "vr"], rowrank=2,
+                    dtype=storage.Complex128 if dt == np.complex128 else storage.Float64)
+    ls, rs = {}, {}
+    for i in range(psi.nblocks):
+        kl, k1, k2, kr = psi.block_qn_indices(i)
+        shp = psi.get_block_(i).shape
+        l = ls.setdefault((kl, k1), rnd(shp[0]))
+        r = rs.setdefault((k2, kr), rnd(shp[3]))
+        blk = np.multiply.outer(l, r).reshape(shp).astype(dt)
+        psi.get_block_(i).storage().copy_(torch.from_numpy(np.ascontiguousarray(blk).reshape(-1)))
+    s, u, v = L.svd(psi)
+    for i in range(s.nblocks):
+        d = np.diag(s.get_block_(i).numpy())
+        assert np.all(d[1:] <= 1e-12 * max(d[0], 1e-300))  # rank <= 1 per sector
+    _check_factors(psi, s, u, v)
