@@ -129,6 +129,16 @@ typedef struct {
 } TnbCopy2D;
 int tnb_copy2d_batched(const void* src, void* dst, int64_t nseg, const TnbCopy2D* segs, void* stream);
 
+/* ---- one Lanczos orthogonalisation step (linalg.py:474-562 vector work) ----
+ * q: r basis vectors as ROWS (row pitch ldq elements), w: the matvec result (n elements,
+ * overwritten by w - sum_k <q_k, w> q_k), q_next: receives w / |w| (may be NULL);
+ * *alpha = Re <q_{r-1}, w> and *beta = |w| are written to DEVICE memory (no host sync).
+ * r = 0: only normalises w into q_next. work: tnb_lanczos_work_bytes(r_max, n) bytes,
+ * zeroed before first use (the step leaves its counters zeroed). float64 / complex128. */
+int64_t tnb_lanczos_work_bytes(int r_max, int64_t n);
+int tnb_lanczos_step(int dtype, const void* q, int64_t ldq, int r, void* w, int64_t n, void* q_next,
+                     double* alpha, double* beta, void* work, void* stream);
+
 /* ---- batched one-sided Jacobi SVD of sector matrices (linalg.py:246-341) ---
  * Each sector: A (m x n, 1 <= m <= n, row-major, dtype TNB_F64 or TNB_C128; s is
  * float64 either way) in `a` (read only), workspaces b (m x ldb) and q (m x ldq)

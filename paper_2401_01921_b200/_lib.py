@@ -23,6 +23,7 @@ EXPORTS = (
     "tnb_zero_flux_blocks", "tnb_bs_contract", "tnb_bs_contract_masked", "tnb_optimal_order",
     "tnb_ktimer_enable", "tnb_ktimer_reset", "tnb_ktimer_read",
     "tnb_bs_plan", "tnb_bs_execute", "tnb_bs_execute_batched", "tnb_bs_plan_pairs", "tnb_copy2d_batched", "tnb_svd_jacobi_batched",
+    "tnb_lanczos_work_bytes", "tnb_lanczos_step",
 )
 
 # kernel families of the kernel timer (TNB_KF_* in include/tnb.h)
@@ -86,6 +87,8 @@ def _declare(lib):
         "tnb_bs_execute_batched": ([_i64, _i64, _p, _p, _p, _p], ctypes.c_int),
         "tnb_bs_plan_pairs": ([_i64, _i64, _pi32, _pi64, _p], ctypes.c_int),
         "tnb_copy2d_batched": ([_p, _p, _i64, _p, _p], ctypes.c_int),
+        "tnb_lanczos_work_bytes": ([ctypes.c_int, _i64], _i64),
+        "tnb_lanczos_step": ([ctypes.c_int, _p, _i64, ctypes.c_int, _p, _i64, _p, _p, _p, _p, _p], ctypes.c_int),
         "tnb_svd_jacobi_batched": ([ctypes.c_int, ctypes.c_int, _p, ctypes.c_int, ctypes.c_double,
                                     ctypes.c_double, _p], ctypes.c_int),
         "tnb_optimal_order": ([ctypes.c_int, ctypes.c_char_p, _pi32, _pi32, _pi64,
@@ -352,6 +355,16 @@ def bs_plan(dtype, a_qn, a_shapes, a_perm, b_qn, b_shapes, b_perm, a_axes, b_axe
 
 COPY2D_DTYPE = np.dtype([("src_off", "<i8"), ("dst_off", "<i8"), ("rows", "<i8"), ("row_bytes", "<i8"),
                          ("src_pitch", "<i8"), ("dst_pitch", "<i8")])  # TnbCopy2D
+
+
+def lanczos_work_bytes(r_max, n):
+    return int(lib().tnb_lanczos_work_bytes(int(r_max), int(n)))
+
+
+def lanczos_step(dtype, q_ptr, ldq, r, w_ptr, n, q_next_ptr, alpha_ptr, beta_ptr, work_ptr, stream):
+    """tnb_lanczos_step: reorthogonalise w against r basis rows, alpha / beta to device memory."""
+    check(lib().tnb_lanczos_step(dtype, q_ptr, ldq, r, w_ptr, n, q_next_ptr, alpha_ptr, beta_ptr, work_ptr, stream),
+          "lanczos_step")
 
 
 def copy2d_batched(src_ptr, dst_ptr, segs, stream):

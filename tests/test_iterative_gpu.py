@@ -129,3 +129,26 @@ def test_device_lanczos_complex_hermitian(cuda):
         for i in range(k):
             r = torch.linalg.vector_norm(ad @ vecs[:, i] - vals[i] * vecs[:, i])
             assert float(r) <= 1e-8
+
+
+def test_device_lanczos_breakdown_restart_and_no_torch_vector_ops(cuda, monkeypatch):
+    """A start vector inside a 2-dimensional invariant subspace breaks the recurrence down
+    after two steps; the device Lanczos restarts with a random orthogonal vector (as the
+    reference does) and still finds the 3 lowest eigenvalues. The vector work runs in
+    libtnb (tnb_lanczos_step): torch's vdot / vector_norm are never called."""
+    import torch
+    d = np.array([-3.0, -1.0, 0.5, 1.5, 2.0, 4.0, 5.0, 7.0])
+    ad = torch.diag(torch.from_numpy(d)).cuda()
+    v0 = np.zeros(8)
+    v0[[1, 4]] = 1.0
+
+    def boom(*a, **k):
+        raise AssertionError("torch vector op called inside lanczos")
+    monkeypatch.setattr(torch, "vdot", boom)
+    monkeypatch.setattr(torch.linalg, "vector_norm", boom)
+    vals, vecs = lanczos(LinOp(8, matvec=lambda v: ad @ v), k=3, v0=v0, tol=1e-12, seed=2)
+    assert np.allclose(vals, np.sort(d)[:3], atol=1e-12)
+    for i in range(3):
+        v = vecs[:, i]
+        r = (ad @ v - vals[i] * v).norm().item() if False else float(np.linalg.norm((ad @ v - vals[i] * v).cpu().numpy()))
+        assert r <= 1e-10
