@@ -292,6 +292,7 @@ struct BsCfg {
   // rate, is the limit, so two producer warpgroups feed the 16 math warps (measured: 4 math
   // warps of 32x32 tiles at 1 or 2 CTAs per SM 15% slower; 8 math warps of 32x16 tiles + one
   // producer warpgroup at 2 CTAs per SM 10% slower)
+  // (r02, 64 x C4 batch: NPROD 64 / 128 and BK 32 with 4-5 stages measured no better)
   static constexpr int BM = 64, BN = 64, BK = CPLX ? 8 : 16, WM = 4, WN = 4, STAGES = 8, NPROD = 256;
   using Core = SKCore<CPLX, MODE, BM, BN, BK, WM, WN, STAGES, NPROD>;
 };

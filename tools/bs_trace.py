@@ -40,3 +40,8 @@ else:
         segs = [(int(r[6 + 4 * k]), int(r[7 + 4 * k]), round((r[4 + 4 * k] - t0) / 1e3, 1), round((r[5 + 4 * k] - t0) / 1e3, 1))
                 for k in range(min(int(r[2]), 14))]
         print(f"cta {c}: start {(r[0]-t0)/1e3:.1f} end {(r[1]-t0)/1e3:.1f} iters {r[3]} segs(tile,n,consumed,done) {segs}")
+    if "stages" in sys.argv:
+        for c in list(order[-3:]):
+            r = d[c]
+            st = [(r[30 + g] - t0) / 1e3 for g in range(24) if r[30 + g] > 0]
+            print(f"cta {c} producer stage issue times (us):", " ".join(f"{x:.2f}" for x in st))
