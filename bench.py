@@ -98,28 +98,44 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.backend = "nccl"
 
     def init(self, backend):
+        # dev: TNB_BENCH_BACKEND=gloo runs the multi-rank code paths with host-side
+        # collectives (e.g. two ranks sharing one GPU) -- a functional check, not a measurement
+        self.backend = os.environ.get("TNB_BENCH_BACKEND", backend)
         if self.world > 1:
             import torch.distributed as dist
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group(backend=backend)
+            dist.init_process_group(backend=self.backend)
             self.pg = dist
+
+    @property
+    def coll_device(self):
+        import torch
+        return "cuda" if torch.cuda.is_available() and self.backend == "nccl" else "cpu"
 
     def barrier(self):
         if self.pg:
-            import torch
-            if torch.cuda.is_available():
+            if self.coll_device == "cuda":
                 self.pg.barrier(device_ids=[self.local])
             else:
                 self.pg.barrier()
+
+    def all_gather(self, out, inp):
+        """all_gather_into_tensor, staged through host memory for a host backend."""
+        if self.coll_device == "cuda" or not inp.is_cuda:
+            self.pg.all_gather_into_tensor(out, inp)
+            return
+        o = out.cpu()
+        self.pg.all_gather_into_tensor(o, inp.cpu())
+        out.copy_(o)
 
     def _reduce(self, x, op):
         if not self.pg:
             return x
         import torch
-        t = torch.tensor([float(x)], dtype=torch.float64,
-                         device="cuda" if torch.cuda.is_available() else "cpu")
+        t = torch.tensor([float(x)], dtype=torch.float64, device=self.coll_device)
         self.pg.all_reduce(t, op=op)
         return float(t.item())
 
@@ -581,7 +597,7 @@ def gpu_peps(tnb, n_sites, chi, D, d, steps, warmup, flush, dist):
             mine_buf[k:k + 1].copy_(net.launch().get_block_().storage().reshape(-1))
         if dist.pg:
             gathered = torch.empty(per * dist.world, dtype=torch.float64, device="cuda")
-            dist.pg.all_gather_into_tensor(gathered, mine_buf)
+            dist.all_gather(gathered, mine_buf)
             # rank r holds sites r, r + world, ...: scatter back to site order
             vals.copy_(gathered.view(dist.world, per).t().reshape(-1)[:n_sites])
         else:
@@ -901,7 +917,7 @@ def main():
         return run_reference(args, dist)
 
     import torch
-    torch.cuda.set_device(dist.local)
+    torch.cuda.set_device(dist.local % max(torch.cuda.device_count(), 1))
     dist.init("nccl")
     import paper_2401_01921_b200 as tnb
     flush = L2Flush()
