@@ -57,6 +57,22 @@ __device__ __forceinline__ double warp_sum(double x) {
   return x;
 }
 
+// Deterministic CTA-wide sum: thread t adds elements t, t + kThreads, ... of its own
+// subset in order, then a fixed-shape tree over the threads (smem `red`, kThreads doubles).
+__device__ double cta_sum_fixed(const double* v, int64_t count, int64_t stride, double* red) {
+  double s = 0.0;
+  for (int64_t c = threadIdx.x; c < count; c += kThreads) s += __ldcg(v + c * stride);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int h = kThreads / 2; h > 0; h >>= 1) {
+    if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+    __syncthreads();
+  }
+  const double out = red[0];
+  __syncthreads();
+  return out;
+}
+
 struct LzWork {
   double* part;    // [nchunks][r][2] partial dots
   double* coef;    // [r][2] reduced coefficients c_k
@@ -81,13 +97,22 @@ __global__ void __launch_bounds__(kThreads) lz_project(const typename Lv<CPLX>::
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kThreads / 32;
   for (int k = warp; k < r; k += nw) {
     const T* q = Q + (int64_t)k * ldq + j0;
-    double re = 0.0, im = 0.0;
-    for (int x = lane; x < len; x += 32) L::dot(re, im, __ldcs(q + x), ws[x]);
-    re = warp_sum(re);
-    if (CPLX) im = warp_sum(im);
+    // 4 independent partial sums per lane keep 4 loads in flight; combined in a fixed order
+    double re[4] = {0.0, 0.0, 0.0, 0.0}, im[4] = {0.0, 0.0, 0.0, 0.0};
+    int x = lane;
+    for (; x + 96 < len; x += 128) {
+      const T a0 = __ldcs(q + x), a1 = __ldcs(q + x + 32), a2 = __ldcs(q + x + 64), a3 = __ldcs(q + x + 96);
+      L::dot(re[0], im[0], a0, ws[x]);
+      L::dot(re[1], im[1], a1, ws[x + 32]);
+      L::dot(re[2], im[2], a2, ws[x + 64]);
+      L::dot(re[3], im[3], a3, ws[x + 96]);
+    }
+    for (; x < len; x += 32) L::dot(re[0], im[0], __ldcs(q + x), ws[x]);
+    double sre = warp_sum((re[0] + re[1]) + (re[2] + re[3]));
+    double sim = CPLX ? warp_sum((im[0] + im[1]) + (im[2] + im[3])) : 0.0;
     if (lane == 0) {
-      wk.part[((int64_t)blockIdx.x * r + k) * 2] = re;
-      wk.part[((int64_t)blockIdx.x * r + k) * 2 + 1] = im;
+      wk.part[((int64_t)blockIdx.x * r + k) * 2] = sre;
+      wk.part[((int64_t)blockIdx.x * r + k) * 2 + 1] = sim;
     }
   }
   // the last CTA to finish reduces the partials in chunk order (deterministic)
@@ -97,14 +122,14 @@ __global__ void __launch_bounds__(kThreads) lz_project(const typename Lv<CPLX>::
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int k = threadIdx.x; k < r; k += kThreads) {
-    double re = 0.0, im = 0.0;
-    for (int c = 0; c < (int)gridDim.x; ++c) {
-      re += __ldcg(wk.part + ((int64_t)c * r + k) * 2);
-      im += __ldcg(wk.part + ((int64_t)c * r + k) * 2 + 1);
+  __shared__ double red[kThreads];
+  for (int k = 0; k < r; ++k) {
+    const double re = cta_sum_fixed(wk.part + 2 * (int64_t)k, gridDim.x, 2 * (int64_t)r, red);
+    const double im = CPLX ? cta_sum_fixed(wk.part + 2 * (int64_t)k + 1, gridDim.x, 2 * (int64_t)r, red) : 0.0;
+    if (threadIdx.x == 0) {
+      wk.coef[2 * k] = re;
+      wk.coef[2 * k + 1] = im;
     }
-    wk.coef[2 * k] = re;
-    wk.coef[2 * k + 1] = im;
   }
   if (threadIdx.x == 0) *wk.counter = 0;
 }
@@ -115,18 +140,37 @@ __global__ void __launch_bounds__(kThreads) lz_update(const typename Lv<CPLX>::T
   using L = Lv<CPLX>;
   using T = typename L::T;
   extern __shared__ double cs[];  // [r][2]
-  __shared__ double red[kThreads / 32];
+  __shared__ double red[kThreads];
   __shared__ bool last;
   for (int x = threadIdx.x; x < 2 * r; x += kThreads) cs[x] = __ldcg(wk.coef + x);
   __syncthreads();
   const int64_t j0 = (int64_t)blockIdx.x * kChunk;
   const int len = (int)min64(kChunk, n - j0);
+  // each thread owns kEl elements; every basis row is one round of kEl independent loads
+  constexpr int kEl = kChunk / kThreads;
+  T v[kEl];
+#pragma unroll
+  for (int e = 0; e < kEl; ++e) {
+    const int x = threadIdx.x + e * kThreads;
+    if (x < len) v[e] = w[j0 + x];
+  }
+  for (int k = 0; k < r; ++k) {
+    const T* q = Q + (int64_t)k * ldq + j0;
+    const double cr = cs[2 * k], ci = cs[2 * k + 1];
+#pragma unroll
+    for (int e = 0; e < kEl; ++e) {
+      const int x = threadIdx.x + e * kThreads;
+      if (x < len) v[e] = L::axpy(v[e], cr, ci, __ldcs(q + x));
+    }
+  }
   double nrm = 0.0;
-  for (int x = threadIdx.x; x < len; x += kThreads) {
-    T v = w[j0 + x];
-    for (int k = 0; k < r; ++k) v = L::axpy(v, cs[2 * k], cs[2 * k + 1], __ldcs(Q + (int64_t)k * ldq + j0 + x));
-    w[j0 + x] = v;
-    nrm += L::abs2(v);
+#pragma unroll
+  for (int e = 0; e < kEl; ++e) {
+    const int x = threadIdx.x + e * kThreads;
+    if (x < len) {
+      w[j0 + x] = v[e];
+      nrm += L::abs2(v[e]);
+    }
   }
   nrm = warp_sum(nrm);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
@@ -142,10 +186,9 @@ __global__ void __launch_bounds__(kThreads) lz_update(const typename Lv<CPLX>::T
   __syncthreads();
   if (!last) return;
   __threadfence();
+  const double s2 = cta_sum_fixed(wk.npart, gridDim.x, 1, red);
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int c = 0; c < (int)gridDim.x; ++c) s += __ldcg(wk.npart + c);
-    *wk.beta = sqrt(s);
+    *wk.beta = sqrt(s2);
     *wk.alpha = r > 0 ? cs[2 * (r - 1)] : 0.0;
     wk.counter[1] = 0;
   }

@@ -80,3 +80,21 @@ def c4_batch(n, iters):
 
 if __name__ == "__main__" and sys.argv[1] == "c4_batch":
     c4_batch(int(sys.argv[2]), int(sys.argv[3]))
+
+
+def lanczos_probe(chi, iters):
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2401_01921_b200 import eig
+    inp = oracle.hermitian_lawr_inputs(chi, seed=7)
+    net, _ = bench.make_network(tnb, oracle.LAWR_NET, inp)
+    op = eig.NetworkMatvec(net.compile(), "A")
+    try:
+        eig.lanczos(op, k=1, tol=1e-14, max_iter=iters, seed=3)
+    except eig.ConvergenceError:
+        pass
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__" and sys.argv[1] == "lanczos":
+    lanczos_probe(int(sys.argv[2]), int(sys.argv[3]))
