@@ -631,6 +631,8 @@ struct StreamK {
     sk.total = (int64_t)d.tiles_m * d.tiles_n * sk.KT;
     if ((int64_t)d.tiles_m * d.tiles_n >= (1ll << 31)) return fail(TNB_EUNSUP, "contract: too many tiles");
     // >= 4 k-tiles per CTA: tiny problems do not pay for many partial hand-offs
+    // (r02: 8 / 12 / 16 / 24 k-tiles per CTA measured slower at chi = 128 -- fewer CTAs each
+    // walking more k-tiles, while the partial hand-off chain was not the limiter)
     sk.G = (int)std::max<int64_t>(1, std::min<int64_t>(sk.total / 4, sms()));
     const size_t ws_bytes = (size_t)sk.G * Core::ACCN * Core::NMATH * 8;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
