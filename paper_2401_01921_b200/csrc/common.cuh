@@ -89,8 +89,8 @@ __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return
 // (Granlund-Montgomery). Valid for 0 <= n < 2^31 and 1 <= d < 2^31.
 struct FastDiv {
   uint32_t d, m, s;
-  FastDiv() : d(1), m(0), s(0) {}
-  explicit FastDiv(uint32_t div) {
+  __host__ __device__ FastDiv() : d(1), m(0), s(0) {}
+  __host__ __device__ explicit FastDiv(uint32_t div) {
     d = div;
     if (d == 1) { m = 0; s = 0; return; }
     s = 0;
