@@ -24,7 +24,7 @@ namespace tnb {
 namespace {
 
 constexpr int kMaxR = TNB_MAX_RANK;
-constexpr int kThreads = 512;
+constexpr int kThreads = 256;  // generic tiled kernel: 4+ CTAs (tiles) in flight per SM
 
 template <int ES>
 struct Word;
@@ -61,12 +61,13 @@ struct PermDesc {
   int32_t tsi[kMaxR];        // unpadded input-order tile stride (boundary path)
   int32_t tso[kMaxR];        // output-order tile stride (boundary path)
   FastDiv div_in, div_out;   // by N_in, N_out
+  FastDiv cin_div, cout_div; // by ceil(N_in / 32), ceil(N_out / 32): 32-element items per run
   FastDiv tsi_div[kMaxR], tso_div[kMaxR], ext_div[kMaxR];
 };
 
 // Shared-memory layout per CTA: [tile data (N_t padded) | inhi | outhi | shi | slo]
 template <int ES>
-__global__ void __launch_bounds__(kThreads, 2) permute_tiled_kernel(
+__global__ void __launch_bounds__(kThreads, 4) permute_tiled_kernel(
     const typename Word<ES>::T* __restrict__ src, typename Word<ES>::T* __restrict__ dst,
     const __grid_constant__ PermDesc d) {
   using T = typename Word<ES>::T;
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(kThreads, 2) permute_tiled_kernel(
   }
   __syncthreads();
 
-  constexpr int kMaxItems = 8;  // N_t <= kThreads * kMaxItems
+  constexpr int kMaxItems = 8;  // items in flight per lane
   for (int64_t tileid = blockIdx.x; tileid < d.ntiles; tileid += gridDim.x) {
     // tile coordinates -> base offsets, boundary limits
     int64_t base_in = 0, base_out = 0;
@@ -149,42 +150,50 @@ __global__ void __launch_bounds__(kThreads, 2) permute_tiled_kernel(
     const T* s = src + base_in;
     T* o = dst + base_out;
     if (!boundary) {
-      T v[kMaxItems];
+      // warp-per-run: an item is 32 consecutive elements of one contiguous run (input runs of
+      // N_in elements on the load side, output runs of N_out on the store side); the only
+      // per-item index math is one warp-uniform division, per element one add. Eight items
+      // per lane are in flight before any of them is stored.
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kThreads / 32;
+      const int cin = (d.N_in + 31) >> 5, cout = (d.N_out + 31) >> 5;
+      const int items_in = d.n_hi_in * cin, items_out = d.n_hi_out * cout;
+      for (int i0 = warp; i0 < items_in; i0 += nw * kMaxItems) {
+        T v[kMaxItems];
 #pragma unroll
-      for (int it = 0; it < kMaxItems; ++it) {
-        int t = threadIdx.x + it * kThreads;
-        if (t < d.N_t) {
-          uint32_t hi = d.div_in.div((uint32_t)t);
-          uint32_t lo = (uint32_t)t - hi * (uint32_t)d.N_in;
-          v[it] = __ldg(s + inhi[hi] + lo);
+        for (int u = 0; u < kMaxItems; ++u) {
+          const int i = i0 + u * nw;
+          if (i < items_in) {
+            const int hi = d.cin_div.div((uint32_t)i), lo = (i - hi * cin) * 32 + lane;
+            if (lo < d.N_in) v[u] = __ldg(s + inhi[hi] + lo);
+          }
         }
-      }
 #pragma unroll
-      for (int it = 0; it < kMaxItems; ++it) {
-        int t = threadIdx.x + it * kThreads;
-        if (t < d.N_t) {
-          uint32_t hi = d.div_in.div((uint32_t)t);
-          uint32_t lo = (uint32_t)t - hi * (uint32_t)d.N_in;
-          tile[hi * d.rowp + lo] = v[it];
+        for (int u = 0; u < kMaxItems; ++u) {
+          const int i = i0 + u * nw;
+          if (i < items_in) {
+            const int hi = d.cin_div.div((uint32_t)i), lo = (i - hi * cin) * 32 + lane;
+            if (lo < d.N_in) tile[hi * d.rowp + lo] = v[u];
+          }
         }
       }
       __syncthreads();
+      for (int i0 = warp; i0 < items_out; i0 += nw * kMaxItems) {
+        T v[kMaxItems];
 #pragma unroll
-      for (int it = 0; it < kMaxItems; ++it) {
-        int u = threadIdx.x + it * kThreads;
-        if (u < d.N_t) {
-          uint32_t hi = d.div_out.div((uint32_t)u);
-          uint32_t lo = (uint32_t)u - hi * (uint32_t)d.N_out;
-          v[it] = tile[shi[hi] + slo[lo]];
+        for (int u = 0; u < kMaxItems; ++u) {
+          const int i = i0 + u * nw;
+          if (i < items_out) {
+            const int hi = d.cout_div.div((uint32_t)i), lo = (i - hi * cout) * 32 + lane;
+            if (lo < d.N_out) v[u] = tile[shi[hi] + slo[lo]];
+          }
         }
-      }
 #pragma unroll
-      for (int it = 0; it < kMaxItems; ++it) {
-        int u = threadIdx.x + it * kThreads;
-        if (u < d.N_t) {
-          uint32_t hi = d.div_out.div((uint32_t)u);
-          uint32_t lo = (uint32_t)u - hi * (uint32_t)d.N_out;
-          o[outhi[hi] + lo] = v[it];
+        for (int u = 0; u < kMaxItems; ++u) {
+          const int i = i0 + u * nw;
+          if (i < items_out) {
+            const int hi = d.cout_div.div((uint32_t)i), lo = (i - hi * cout) * 32 + lane;
+            if (lo < d.N_out) o[outhi[hi] + lo] = v[u];
+          }
         }
       }
       __syncthreads();
@@ -800,7 +809,7 @@ int make_plan(int es, int rank, const int64_t* shape, const int32_t* perm, Plan&
     inU[a] = 1;
     ++gin;
   }
-  int N_in = (int)prod;
+  const int gin_lo = r - gin;  // G_in = storage axes [gin_lo, r)
   // G_out: output suffix
   int64_t tprod = prod;  // tile size so far
   int64_t oprod = 1;
@@ -811,8 +820,19 @@ int make_plan(int es, int rank, const int64_t* shape, const int32_t* perm, Plan&
     bool need_more = (oprod < run_lo) || (tprod < 1024 && oprod * 2 <= tmax);
     if (!need_more) break;
     if (inU[a]) {
-      if (a == d.a_in && d.ext[a] != d.dim[a]) {  // partial axis: must be G_out's top
-        oprod *= d.ext[a];
+      if (a == d.a_in && d.ext[a] != d.dim[a]) {
+        // the partial input axis is also inner on the output side: take it whole if the tile
+        // stays within bounds (else the output runs would be only ext elements long)
+        const int64_t grown = tprod / d.ext[a] * d.dim[a];
+        if (grown <= tmax) {
+          tprod = grown;
+          oprod *= d.dim[a];
+          d.ext[a] = (int32_t)d.dim[a];
+          d.a_in = -1;
+          ++gout;
+          continue;
+        }
+        oprod *= d.ext[a];  // partial axis: must be G_out's top
         ++gout;
         break;
       }
@@ -847,6 +867,9 @@ int make_plan(int es, int rank, const int64_t* shape, const int32_t* perm, Plan&
   // that sits inside it (can only be full G_in axes) -- already counted above.
   int N_t = (int)tprod;
   int N_out = (int)oprod;
+  int64_t nin = 1;  // G_in extents (the partial input axis may have grown to full above)
+  for (int a = gin_lo; a < r; ++a) nin *= d.ext[a];
+  const int N_in = (int)nin;
   // U in storage order and output order
   d.nuin = 0;
   for (int a = 0; a < r; ++a)
@@ -892,6 +915,8 @@ int make_plan(int es, int rank, const int64_t* shape, const int32_t* perm, Plan&
   }
   d.div_in = FastDiv((uint32_t)N_in);
   d.div_out = FastDiv((uint32_t)N_out);
+  d.cin_div = FastDiv((uint32_t)((N_in + 31) / 32));
+  d.cout_div = FastDiv((uint32_t)((N_out + 31) / 32));
   // batch axes in output order (outer -> inner), tiles along each
   d.nb = 0;
   int64_t ntiles = 1;
@@ -910,7 +935,7 @@ int make_plan(int es, int rank, const int64_t* shape, const int32_t* perm, Plan&
   d.ntiles = ntiles;
   size_t data_bytes = ((size_t)d.n_hi_in * d.rowp * es + 15) & ~(size_t)15;
   p.smem = data_bytes + (size_t)(d.n_hi_in + d.n_hi_out) * 8 + (size_t)(d.n_hi_out + d.N_out) * 4;
-  if (N_t > kThreads * 8) return fail(TNB_EINVAL, "permute: internal tile too large");
+  if (N_t > 4096) return fail(TNB_EINVAL, "permute: internal tile too large");
   return TNB_OK;
 }
 

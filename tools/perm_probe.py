@@ -42,3 +42,14 @@ buf = src.storage()
 dst = torch.empty_like(buf)
 ms = bench.time_steps(lambda: [dst.copy_(buf) for _ in range(8)], 1, flush, dist)
 print(f"  torch copy_ back-to-back: {nbytes * 8 / ms / 1e6 / hbm:.3f} of HBM peak")
+
+# 1-byte elements (bool) take the generic tiled path
+if os.environ.get("BOOL"):
+    b = tnb.storage.DenseTensor(np.random.default_rng(1).integers(0, 2, size=shape).astype(np.bool_))
+    rates = []
+    for p in perms:
+        g = tnb.graphs.capture(lambda: b.permute(*p).contiguous(), warmup=1)
+        ms = bench.time_steps(lambda: [g.replay() for _ in range(8)], 1, flush, dist)
+        rates.append(2 * b.size * 8 / ms / 1e6 / hbm)  # 8 replays x 2 x bytes
+        del g
+    print(f"  bool: median {np.median(rates):.3f} min {min(rates):.3f} of HBM")
