@@ -6,7 +6,9 @@
 //
 // One launch moves every segment: the (segment, row) space is flattened and
 // walked by warps; each warp copies one row with the widest aligned vector
-// (16/8/4/1 bytes) the row's addresses allow. HBM-bound: 2 x bytes moved.
+// (16/8/4/1 bytes) the row's addresses allow; rows longer than 4 KB are split into 4 KB
+// pieces so that a few long rows (packed block payloads) still spread over the whole GPU.
+// HBM-bound: 2 x bytes moved.
 #include <algorithm>
 #include <vector>
 
@@ -18,10 +20,11 @@ namespace tnb {
 namespace {
 
 constexpr int kInlineSegs = 256;
+constexpr int64_t kChunkBytes = 4096;  // work unit: one 4 KB piece of one row (long rows spread over warps)
 
 struct SegTable {
   TnbCopy2D s[kInlineSegs];
-  int64_t row0[kInlineSegs + 1];  // prefix sums of rows
+  int64_t row0[kInlineSegs + 1];  // prefix sums of work units (rows x 4 KB pieces)
 };
 
 template <typename V>
@@ -30,6 +33,7 @@ __device__ __forceinline__ void copy_row(const unsigned char* __restrict__ src, 
   const int64_t n = bytes / (int64_t)sizeof(V);
   const V* s = reinterpret_cast<const V*>(src);
   V* d = reinterpret_cast<V*>(dst);
+#pragma unroll 4
   for (int64_t i = lane; i < n; i += 32) d[i] = s[i];
 }
 
@@ -57,14 +61,18 @@ __global__ void __launch_bounds__(256) copy2d_kernel(const unsigned char* __rest
       seg = lo;
     }
     const TnbCopy2D g = segs[seg];
-    const int64_t k = r - row0[seg];
-    const unsigned char* s = src + g.src_off + k * g.src_pitch;
-    unsigned char* d = dst + g.dst_off + k * g.dst_pitch;
-    const uintptr_t al = reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d) | (uintptr_t)g.row_bytes;
-    if ((al & 15) == 0) copy_row<uint4>(s, d, g.row_bytes, lane);
-    else if ((al & 7) == 0) copy_row<uint2>(s, d, g.row_bytes, lane);
-    else if ((al & 3) == 0) copy_row<uint32_t>(s, d, g.row_bytes, lane);
-    else copy_row<unsigned char>(s, d, g.row_bytes, lane);
+    const int64_t cpr = (g.row_bytes + kChunkBytes - 1) / kChunkBytes;  // pieces per row
+    const int64_t u = r - row0[seg];
+    const int64_t k = u / cpr, piece = u - k * cpr;
+    const int64_t b0 = piece * kChunkBytes;
+    const int64_t bytes = (g.row_bytes - b0) < kChunkBytes ? (g.row_bytes - b0) : kChunkBytes;
+    const unsigned char* s = src + g.src_off + k * g.src_pitch + b0;
+    unsigned char* d = dst + g.dst_off + k * g.dst_pitch + b0;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d) | (uintptr_t)bytes;
+    if ((al & 15) == 0) copy_row<uint4>(s, d, bytes, lane);
+    else if ((al & 7) == 0) copy_row<uint2>(s, d, bytes, lane);
+    else if ((al & 3) == 0) copy_row<uint32_t>(s, d, bytes, lane);
+    else copy_row<unsigned char>(s, d, bytes, lane);
   }
 }
 
@@ -85,7 +93,7 @@ extern "C" int tnb_copy2d_batched(const void* src, void* dst, int64_t nseg, cons
     const TnbCopy2D& g = segs[i];
     if (g.rows < 0 || g.row_bytes < 0 || g.src_off < 0 || g.dst_off < 0)
       return fail(TNB_EINVAL, "copy2d: negative extent or offset");
-    row0[i + 1] = row0[i] + (g.row_bytes > 0 ? g.rows : 0);
+    row0[i + 1] = row0[i] + (g.row_bytes > 0 ? g.rows * ((g.row_bytes + kChunkBytes - 1) / kChunkBytes) : 0);
     bytes += 2.0 * (double)g.rows * (double)g.row_bytes;
   }
   const int64_t total = row0[nseg];

@@ -171,6 +171,43 @@ def _read_to_device(f, staging, nbytes, path):
             evs[b].synchronize()  # buffers are reused by the next load
 
 
+_PAYLOAD_SEGS = {}  # (structure id, direction) -> (segments, packed bytes, slab byte offset of block 0)
+
+
+def _cached_segments(ut, packed_to_slab):
+    """Payload <-> slab segments of a block-sparse tensor held in one slab (contraction._bs_info):
+    computed once per block structure; returns (segments, slab base pointer, bytes) or None."""
+    from .contraction import _bs_info
+    info = _bs_info(ut) if ut.is_sym else None
+    if info is None:
+        return None
+    sid, slab, offs, dt = info
+    key = (sid, bool(packed_to_slab))
+    hit = _PAYLOAD_SEGS.get(key)
+    if hit is None:
+        isz = dt.itemsize
+        sizes = np.array([int(np.prod(b, dtype=np.int64)) for b in _shapes_of(ut)], dtype=np.int64) * isz
+        packed = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+        slab_off = (offs - offs[0]) * isz
+        segs = np.zeros(len(sizes), dtype=_lib.COPY2D_DTYPE)
+        src, dst = (packed, slab_off) if packed_to_slab else (slab_off, packed)
+        segs["src_off"], segs["dst_off"], segs["rows"] = src, dst, 1
+        segs["row_bytes"], segs["src_pitch"], segs["dst_pitch"] = sizes, sizes, sizes
+        if len(_PAYLOAD_SEGS) >= 256:
+            _PAYLOAD_SEGS.clear()
+        hit = _PAYLOAD_SEGS[key] = (segs, int(sizes.sum()), int(offs[0]) * isz)
+    segs, nbytes, off0 = hit
+    from . import dense as _dense
+    _dense._await(slab)
+    return segs, slab.data_ptr() + off0, nbytes
+
+
+def _shapes_of(ut):
+    if ut._blk is None:
+        return ut._lazy[3]
+    return [b.storage_shape for b in ut._blk]
+
+
 def payload_nbytes(ut):
     """Bytes of the packed payload of ``ut``: every block's C-order elements concatenated in
     block order (the ``.utn`` payload layout, io.py:56-80)."""
@@ -183,16 +220,23 @@ def upload_payload_(ut, host):
     one ``tnb_copy2d_batched`` scatter to the blocks' places in the slab, both queued on the
     current stream (asynchronous for pinned input). Blocks must be stored contiguously
     (a freshly built or loaded tensor)."""
-    blocks = ut.get_blocks_()
-    if any(not b.is_contiguous for b in blocks):
-        raise ValueError("upload_payload_: blocks must be contiguous (materialise with contiguous_() first)")
     h = torch.as_tensor(host) if not isinstance(host, torch.Tensor) else host
-    nbytes = payload_nbytes(ut)
+    fast = _cached_segments(ut, True)
+    if fast is not None and ut._blk is not None and ut._blk and ut._blk[0]._perm != tuple(range(ut.rank)):
+        fast = None  # lazily permuted blocks: the payload is in logical order
+    if fast is not None:
+        segs, base, nbytes = fast
+    else:
+        blocks = ut.get_blocks_()
+        if any(not b.is_contiguous for b in blocks):
+            raise ValueError("upload_payload_: blocks must be contiguous (materialise with contiguous_() first)")
+        nbytes = payload_nbytes(ut)
     if h.numel() * h.element_size() != nbytes:
         raise ValueError(f"upload_payload_: host payload has {h.numel() * h.element_size()} bytes, expected {nbytes}")
     if not nbytes:
         return ut
-    segs, base, _ = _segments(blocks, ut.dtype.itemsize, packed_to_slab=True)
+    if fast is None:
+        segs, base, _ = _segments(blocks, ut.dtype.itemsize, packed_to_slab=True)
     staging = torch.empty(nbytes, dtype=torch.uint8, device=dense.device())
     staging.copy_(h.reshape(-1).view(torch.uint8), non_blocking=True)
     _lib.copy2d_batched(staging.data_ptr(), base, segs, dense.stream_handle())
@@ -203,14 +247,21 @@ def download_payload(ut, host):
     """Copy every block of ``ut`` into a host payload (pinned CPU tensor in the packed
     ``.utn`` layout): one gather launch and one device->host copy queued on the current
     stream; synchronise (or wait on an event) before reading ``host``."""
-    blocks = [b.contiguous() for b in ut.get_blocks_()]
-    nbytes = payload_nbytes(ut)
+    fast = _cached_segments(ut, False)
+    if fast is not None and ut._blk is not None and ut._blk and ut._blk[0]._perm != tuple(range(ut.rank)):
+        fast = None
+    if fast is not None:
+        segs, base, nbytes = fast
+    else:
+        blocks = [b.contiguous() for b in ut.get_blocks_()]
+        nbytes = payload_nbytes(ut)
     if host.numel() * host.element_size() != nbytes:
         raise ValueError(f"download_payload: host buffer has {host.numel() * host.element_size()} bytes, "
                          f"expected {nbytes}")
     if not nbytes:
         return host
-    segs, base, _ = _segments(blocks, ut.dtype.itemsize, packed_to_slab=False)
+    if fast is None:
+        segs, base, _ = _segments(blocks, ut.dtype.itemsize, packed_to_slab=False)
     packed = torch.empty(nbytes, dtype=torch.uint8, device=dense.device())
     _lib.copy2d_batched(base, packed.data_ptr(), segs, dense.stream_handle())
     host.reshape(-1).view(torch.uint8).copy_(packed, non_blocking=True)

@@ -118,3 +118,32 @@ def test_large_payload_multi_chunk(cuda, tmp_path, monkeypatch):
     back = tio.load_unitensor(p)
     tio._PINNED[:] = saved
     assert back.name == "big" and np.array_equal(back.get_block_().numpy(), arr)
+
+
+def test_payload_upload_download_roundtrip(cuda):
+    """upload_payload_ / download_payload (packed .utn payload <-> HBM slab): round trip on a
+    fresh tensor, on a lazily held contraction result (cached-structure fast path) and on a
+    lazily permuted tensor (logical order, general path)."""
+    import numpy as np
+    import torch
+    import bench
+    import paper_2401_01921_b200 as tnb
+    from paper_2401_01921_b200 import io as tio
+    A, E = bench.c4_tensors(tnb, seed=3)
+    for t in (A, tnb.contract(A, E), tnb.contract(A, E)):  # the second result: fast path, lazy blocks
+        n = tio.payload_nbytes(t)
+        want = np.concatenate([b.numpy().reshape(-1) for b in t.get_blocks_()])
+        host = torch.empty(n, dtype=torch.uint8).pin_memory()
+        t.download_payload(host)
+        torch.cuda.synchronize()
+        assert np.array_equal(host.numpy().view(np.float64), want)
+        t2 = tnb.UniTensor(t.bonds, labels=t.labels, rowrank=t.rowrank)
+        t2.upload_payload_(host)
+        assert all(np.array_equal(x.numpy(), y.numpy()) for x, y in zip(t2.get_blocks_(), t.get_blocks_()))
+    P = A.permute(["vr", "vl", "p"])
+    n = tio.payload_nbytes(P)
+    host = torch.empty(n, dtype=torch.uint8).pin_memory()
+    P.download_payload(host)
+    torch.cuda.synchronize()
+    want = np.concatenate([b.numpy().reshape(-1) for b in P.get_blocks_()])
+    assert np.array_equal(host.numpy().view(np.float64), want)
