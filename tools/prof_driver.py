@@ -98,3 +98,17 @@ def lanczos_probe(chi, iters):
 
 if __name__ == "__main__" and sys.argv[1] == "lanczos":
     lanczos_probe(int(sys.argv[2]), int(sys.argv[3]))
+
+
+def peps_site(iters):
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2401_01921_b200 import workloads as WL
+    net, _ = bench.make_network(tnb, WL.PEPS_NET, WL.peps_inputs(256, 8, 2, site=0))
+    for _ in range(iters):
+        net.launch()
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__" and sys.argv[1] == "peps_site":
+    peps_site(int(sys.argv[2]))
