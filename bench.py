@@ -39,7 +39,7 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 import numpy as np
 
 FP64_PEAK_TFLOPS = 37.06   # measured DMMA peak on this pool's B200 (profiles/r01_fp64_peak.txt)
-PEAK_SOURCE = "measured DMMA.8x8x4 microbenchmark, profiles/r01_fp64_peak.txt (MEASURED_PEAKS.json has no fp64)"
+PEAK_SOURCE = "DMMA.8x8x4 microbenchmark, profiles/r01_fp64_peak.txt (no fp64 in MEASURED_PEAKS.json)"
 METRIC = "fp64 GFLOP/s (L.A.W.R Network matvec, chi=1024)"
 CONFIG = {"workload": "lawr_f64_chi1024", "chi": 1024, "d": 2, "D": 5, "order": "(((A,L),W),R)"}
 DATA = "synthetic (seeded N(0,1), reference recipe)"
@@ -933,8 +933,8 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
             "config": dict(CONFIG), "e2e": head["e2e"], "roofline": head["roofline"],
             "gpu_launches": int(head["launches_per_step"] * args.steps), "clocks": clocks,
-            "timing": f"L2 flushed before every timed step; CUDA events; max over ranks; replicas x{dist.world}; "
-                      f"e2e: pinned host in/out, double-buffered", "peak_source": PEAK_SOURCE}
+            "timing": f"L2 flushed per step; CUDA events; max over ranks; replicas x{dist.world}",
+            "peak_source": PEAK_SOURCE}
     detail["headline"] = {k: v for k, v in head.items() if k not in ("out", "inp")}
     if dist.rank == 0:
         line["parity"] = {"rel_fro": _r(parity_lawr(head["out"], 1024, np.float64, 1234), 3), "tol": TOL}
@@ -1061,8 +1061,7 @@ def main():
                 wl[name] = {"error": f"{type(e).__name__}: {e}"[:200]}
             torch.cuda.empty_cache()
         line["workloads"] = wl
-        line["workloads_keys"] = ("v value, frac roofline fraction, cpu oracle-port CPU value, e2e host-buffer value, "
-                                  "par rel.Frobenius vs oracle (0=bit-exact), ms per step")
+        line["workloads_keys"] = "v, frac=roofline, cpu=oracle port, e2e=host buffers, par=rel.err vs oracle, ms/step"
     if cpu_on:
         cb = cpu_lawr(1024, np.float64)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
