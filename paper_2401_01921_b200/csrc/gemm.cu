@@ -504,9 +504,13 @@ struct Tiled {
     if (d.splitk < 1) d.splitk = 1;
     int64_t grid = (int64_t)d.tiles_m * d.tiles_n * d.splitk;
     if (grid >= (1ll << 31)) return fail(TNB_EUNSUP, "contract: problem too large for the tile grid");
+    const double work = 2.0 * d.M * (double)d.N * d.K * (CPLX ? 4 : 1);
     if (d.splitk == 1) {
-      kern<<<(unsigned)grid, threads, smem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B),
-                                                  static_cast<T*>(C), d);
+      {
+        KTimer kt(TNB_KF_GEMM, st, work);
+        kern<<<(unsigned)grid, threads, smem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B),
+                                                    static_cast<T*>(C), d);
+      }
       count_launch();
       TNB_CUDA_CHECK(cudaGetLastError());
       return TNB_OK;
@@ -514,8 +518,11 @@ struct Tiled {
     size_t n = (size_t)d.M * d.N;
     void* ws = nullptr;
     TNB_CUDA_CHECK(cudaMallocAsync(&ws, n * d.splitk * ES, st));
-    kern<<<(unsigned)grid, threads, smem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B),
-                                                static_cast<T*>(ws), d);
+    {
+      KTimer kt(TNB_KF_GEMM, st, work);
+      kern<<<(unsigned)grid, threads, smem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B),
+                                                  static_cast<T*>(ws), d);
+    }
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) {
@@ -740,7 +747,19 @@ int dispatch(const void* A, const void* B, void* C, GemmDesc& d, cudaStream_t st
     // small problems (fewer than ~8 k-iterations of 128 x 128 tiles per SM, e.g. L.A.W.R at
     // chi = 128): 64 x 64 tiles give 4x more stream-K work units, so more SMs take part
     const int64_t it128 = (pad(d.M, 128) / 128) * (pad(d.N, 128) / 128) * ((d.K + 15) / 16);
-    if (it128 < (int64_t)sms() * 8) return StreamK<false, 0, 64, 64, 16, 4, 4, 4>::run(A, B, C, d, st);
+    if (it128 < (int64_t)sms() * 8) {
+      // tiny problems (L.A.W.R at chi = 128: ~2.4 us of DMMA work per launch) are latency
+      // bound: a plain one-tile-per-CTA kernel (64 x 64 tiles, 4 warps of 32 x 32, split-K
+      // planned by an occupancy model, fixed-order reduce) beats the persistent stream-K
+      // kernel's per-stage hand-offs -- C1 graph replay 41.7 -> 30.9 us. The split-K
+      // workspace is packed, so strided (column panel) outputs keep stream-K.
+      if (d.out_ld == d.N) {
+        int split = 1;
+        Tiled<false, 0, 64, 64, 16, 2, 2, 3, 2>::plan(d, split, 1.0);
+        return Tiled<false, 0, 64, 64, 16, 2, 2, 3, 2>::run(A, B, C, d, split, st);
+      }
+      return StreamK<false, 0, 64, 64, 16, 4, 4, 4>::run(A, B, C, d, st);
+    }
     if (aN64 < a128 && aN64 <= aM64) return StreamK<false, 0, 128, 64, 16, 4, 4, 4>::run(A, B, C, d, st);
     if (aM64 < a128) return StreamK<false, 0, 64, 128, 16, 4, 4, 4>::run(A, B, C, d, st);
     // (measured: BK = 32 / 3 stages 15% slower; 3, 5 and 6 stages of BK = 16 no faster than 4)

@@ -120,6 +120,7 @@ def test_large_payload_multi_chunk(cuda, tmp_path, monkeypatch):
     assert back.name == "big" and np.array_equal(back.get_block_().numpy(), arr)
 
 
+@pytest.mark.gpu
 def test_payload_upload_download_roundtrip(cuda):
     """upload_payload_ / download_payload (packed .utn payload <-> HBM slab): round trip on a
     fresh tensor, on a lazily held contraction result (cached-structure fast path) and on a

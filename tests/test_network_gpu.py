@@ -329,3 +329,36 @@ def test_random_networks_vs_oracle(cuda, seed):
     assert net.get_order() == oracle.render_order(tree)
     got = out.numpy() if opens else np.asarray(out.item())
     assert rel_fro(got, want) <= 1e-12
+
+
+def test_repeated_small_launch_graph_replay_returns_fresh_results(cuda):
+    """A latency-bound launch repeated on unchanged bindings is replayed from a captured CUDA
+    graph after two eager replays. Every launch must still return a FRESH result (earlier
+    results are not overwritten), follow in-place updates of the bound data, and stop using
+    the graph when the bindings change."""
+    import torch
+    inp = oracle.lawr_inputs(24, seed=41)
+    net = Network(oracle.LAWR_NET)
+    ts = {}
+    for nm, arr in inp.items():
+        t = UniTensor(storage.from_numpy(arr), labels=[f"{nm}{i}" for i in range(arr.ndim)])
+        net.put_tensor(nm, t, t.labels)
+        ts[nm] = t
+    net.set_order(optimal=True)
+    want, _ = oracle.launch(oracle.lawr_slots(), "b, q, b2", inp)
+    outs = [net.launch() for _ in range(6)]
+    assert net._program is not None and net._program.graph is not None
+    for o in outs:
+        assert rel_fro(o.numpy(), want) <= 1e-12
+    assert len({o.get_block_().data_ptr for o in outs}) == len(outs)  # no aliasing between results
+    # in-place update of a bound tensor's data: the graph reads the same buffer
+    a2 = oracle.normal(inp["A"].shape, seed=99)
+    ts["A"].get_block_().storage().copy_(torch.from_numpy(a2.reshape(-1)))
+    inp2 = dict(inp, A=a2)
+    want2, _ = oracle.launch(oracle.lawr_slots(), "b, q, b2", inp2)
+    assert rel_fro(net.launch().numpy(), want2) <= 1e-12
+    assert rel_fro(outs[0].numpy(), want) <= 1e-12  # earlier results untouched
+    # rebinding: a new program (eager first)
+    t = UniTensor(storage.from_numpy(inp["A"]), labels=["A0", "A1", "A2"])
+    net.put_tensor("A", t, t.labels)
+    assert rel_fro(net.launch().numpy(), want) <= 1e-12
