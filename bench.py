@@ -949,8 +949,10 @@ def main():
             cpu = cpu_lawr(128, np.float64, budget_s=2, max_iter=50) if cpu_on else None
             detail["C1"]["cpu_baseline"] = cpu
             par = parity_lawr(r["out"], 128, np.float64, 1234) if dist.rank == 0 else None
-            return compact(r["gflops"], "GFLOP/s", r["roofline"]["frac"], cpu and cpu["value"], r["e2e"]["value"],
-                           par, r["ms_per_step"])
+            d = compact(r["gflops_graph"], "GFLOP/s", r["roofline"]["frac"], cpu and cpu["value"], r["e2e"]["value"],
+                        par, r["graph_ms_per_step"])
+            d["v_eager"] = _r(r["gflops"], 5)  # plain Network.launch (host-bound at this size)
+            return d
 
         def w_perm():
             perm, samples = gpu_permute(tnb, max(4, args.steps), args.warmup, flush, dist)
