@@ -529,6 +529,7 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
               for (int x = 0; x < EA; ++x) {
                 const bool v = oA[x] >= 0;
                 const T* src = A + (v ? oA[x] + koA : 0);
+                TNB_DCHECK(!v || (oA[x] + koA >= 0 && (int64_t)oA[x] + koA < (int64_t)da.F * da.K), "bs A gather");
                 if constexpr (CPLX)
                   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa + dA[x]), "l"(src), "r"(v ? 16 : 0));
                 else
@@ -538,6 +539,7 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
               for (int x = 0; x < EB; ++x) {
                 const bool v = oB[x] >= 0;
                 const T* src = B + (v ? oB[x] + koB : 0);
+                TNB_DCHECK(!v || (oB[x] + koB >= 0 && (int64_t)oB[x] + koB < (int64_t)db.F * db.K), "bs B gather");
                 if constexpr (CPLX)
                   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sbb + dB[x]), "l"(src), "r"(v ? 16 : 0));
                 else
@@ -550,6 +552,7 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
                 mapA(x, mm, kk);
                 const bool v = oA[x] >= 0 && kk < krem;
                 const T* src = A + (v ? oA[x] + koA : 0);
+                TNB_DCHECK(!v || (oA[x] + koA >= 0 && (int64_t)oA[x] + koA < (int64_t)da.F * da.K), "bs A gather");
                 if constexpr (CPLX)
                   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa + dA[x]), "l"(src), "r"(v ? 16 : 0));
                 else
@@ -561,6 +564,7 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
                 mapB(x, nn, kk);
                 const bool v = oB[x] >= 0 && kk < krem;
                 const T* src = B + (v ? oB[x] + koB : 0);
+                TNB_DCHECK(!v || (oB[x] + koB >= 0 && (int64_t)oB[x] + koB < (int64_t)db.F * db.K), "bs B gather");
                 if constexpr (CPLX)
                   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sbb + dB[x]), "l"(src), "r"(v ? 16 : 0));
                 else
@@ -588,6 +592,7 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
             const int64_t ro = rA[x % RA], ko = ka[kk];
             const bool v = (ro >= 0) && (ko >= 0);
             const T* src = v ? A + ro + ko : A;
+            TNB_DCHECK(!v || (ro + ko >= 0 && ro + ko < (int64_t)da.F * da.K), "bs A gather (table)");
             const uint32_t dst = sAbase + s * stA + (uint32_t)(kk * LDA + mm) * ES;
             if constexpr (CPLX)
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
@@ -601,6 +606,7 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
             const int64_t co = rB[x % RB], ko = kb[kk];
             const bool v = (co >= 0) && (ko >= 0);
             const T* src = v ? B + co + ko : B;
+            TNB_DCHECK(!v || (co + ko >= 0 && co + ko < (int64_t)db.F * db.K), "bs B gather (table)");
             const uint32_t dst = sBbase + s * stB + (uint32_t)(kk * LDB + nn) * ES;
             if constexpr (CPLX)
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));

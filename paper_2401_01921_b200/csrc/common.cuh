@@ -9,6 +9,29 @@
 
 #include "../../include/tnb.h"
 
+// Device-side bounds checks for a CHECKED build (-DTNB_CHECKED=1, tools/build_checked.sh):
+// the stand-in for compute-sanitizer, which this GPU pool does not allow. Every gathered
+// operand offset is checked against its block / operand extent and every stream-K spin
+// wait is bounded; a violation prints the site and traps. Compiled out by default.
+#ifndef TNB_CHECKED
+#define TNB_CHECKED 0
+#endif
+#if TNB_CHECKED
+#include <cstdio>
+#define TNB_DCHECK(cond, what)                                                                            \
+  do {                                                                                                    \
+    if (!(cond)) {                                                                                        \
+      printf("TNB_DCHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x);                                                                           \
+      __trap();                                                                                           \
+    }                                                                                                     \
+  } while (0)
+#else
+#define TNB_DCHECK(cond, what) \
+  do {                         \
+  } while (0)
+#endif
+
 namespace tnb {
 
 // Thread-local last-error message (tnb_last_error).

@@ -908,6 +908,8 @@ int contract_dense_device(const void* a, int dta, int ra, const int64_t* sa, con
   d.M = (int)M;
   d.N = (int)N;
   d.K = (int)K;
+  d.a_elems = (int64_t)prod_dims(A);
+  d.b_elems = (int64_t)prod_dims(B);
   d.kaff.ok = 0;
   if (d.kA.n == 0) {
     d.kaff.ok = 0;  // K == 1: the single (partial) k-tile takes the table path

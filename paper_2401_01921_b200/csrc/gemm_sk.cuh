@@ -20,6 +20,7 @@ namespace tnb {
 
 struct GemmDesc {
   int M, N, K;
+  int64_t a_elems, b_elems;  // operand extents (elements from the base pointers; checked builds)
   int tiles_m, tiles_n, splitk;
   int k_per_split;
   int a_mfast, b_nfast;
@@ -199,9 +200,16 @@ struct SKCore {
     const int tid = threadIdx.x;
     double* flat = &acc[0][0][0][0];
     for (int cc = first; cc < c; ++cc) {
-      if (tid == 0)
+      if (tid == 0) {
+#if TNB_CHECKED
+        long long spins = 0;
+#endif
         while (detail::ld_acquire(flags + cc) < NMATH / 32) {  // every math warp of CTA cc published
+#if TNB_CHECKED
+          TNB_DCHECK(++spins < (1ll << 32), "stream-K partial never published");
+#endif
         }
+      }
       detail::named_sync(2, NMATH);
       const double* w = ws + (size_t)cc * ACCN * NMATH;
 #pragma unroll
@@ -335,6 +343,7 @@ struct SKCore {
               const int64_t ro = rA[i % RA];
               const bool v = ro >= 0;
               const T* src = v ? pa + ro + pra[kk] : A;
+              TNB_DCHECK(!v || (src >= A && src - A < d.a_elems), "dense A gather (periodic K)");
               const uint32_t dst = sAbase + s * stA + (uint32_t)(kk * LDA + m) * ES;
               if constexpr (CPLX)
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
@@ -349,6 +358,7 @@ if (!d.bulkB)
               const int64_t co = rB[i % RB];
               const bool v = co >= 0;
               const T* src = v ? pb + co + prb[kk] : B;
+              TNB_DCHECK(!v || (src >= B && src - B < d.b_elems), "dense B gather (periodic K)");
               const uint32_t dst = sBbase + s * stB + (uint32_t)(kk * LDB + n) * ES;
               if constexpr (CPLX)
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
@@ -369,6 +379,7 @@ if (!d.bulkB)
               const int64_t ro = rA[i % RA];
               const bool v = ro >= 0;
               const T* src = v ? pa + ro + (int64_t)kk * d.kaff.ksA : A;
+              TNB_DCHECK(!v || (src >= A && src - A < d.a_elems), "dense A gather (affine K)");
               const uint32_t dst = sAbase + s * stA + (uint32_t)(kk * LDA + m) * ES;
               if constexpr (CPLX)
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
@@ -383,6 +394,7 @@ if (!d.bulkB)
               const int64_t co = rB[i % RB];
               const bool v = co >= 0;
               const T* src = v ? pb + co + (int64_t)kk * d.kaff.ksB : B;
+              TNB_DCHECK(!v || (src >= B && src - B < d.b_elems), "dense B gather (affine K)");
               const uint32_t dst = sBbase + s * stB + (uint32_t)(kk * LDB + n) * ES;
               if constexpr (CPLX)
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
@@ -409,6 +421,7 @@ if (!d.bulkB)
               const int64_t ro = rA[i % RA], ko = ka[kk];
               const bool v = (ro >= 0) && (ko >= 0);
               const T* src = v ? A + ro + ko : A;
+              TNB_DCHECK(!v || (src >= A && src - A < d.a_elems), "dense A gather (table)");
               const uint32_t dst = sAbase + s * stA + (uint32_t)(kk * LDA + m) * ES;
               if constexpr (CPLX)
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));
@@ -422,6 +435,7 @@ if (!d.bulkB)
               const int64_t co = rB[i % RB], ko = kb[kk];
               const bool v = (co >= 0) && (ko >= 0);
               const T* src = v ? B + co + ko : B;
+              TNB_DCHECK(!v || (src >= B && src - B < d.b_elems), "dense B gather (table)");
               const uint32_t dst = sBbase + s * stB + (uint32_t)(kk * LDB + n) * ES;
               if constexpr (CPLX)
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 16 : 0));

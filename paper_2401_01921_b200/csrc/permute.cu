@@ -471,6 +471,7 @@ struct T2Desc {
   int64_t si;          // output stride of i
   int64_t ti, tj;      // tiles along i / j
   int64_t ntiles;      // batch * ti * tj
+  int64_t n;           // elements (checked builds)
   int nb;              // batch axes, output order (outer -> inner)
   int64_t bdim[kMaxR];
   int64_t bistr[kMaxR];
@@ -510,6 +511,9 @@ __global__ void __launch_bounds__(256) permute_t2d_kernel(const typename Word<ES
     const bool full = (i0 + T <= d.Di) && (j0 + T <= d.Do);
     const W* s = src + bin + i0 + j0 * d.sj;
     W* o = dst + bout + j0 + i0 * d.si;
+    TNB_DCHECK(bin + min64(T, d.Di - i0) - 1 + (min64(T, d.Do - j0) - 1) * d.sj + i0 + j0 * d.sj < d.n &&
+                   bout + min64(T, d.Do - j0) - 1 + (min64(T, d.Di - i0) - 1) * d.si + j0 + i0 * d.si < d.n,
+               "t2d tile out of range");
     W v[NI];
     if (full) {
 #pragma unroll
@@ -581,6 +585,9 @@ __global__ void __launch_bounds__(256) permute_t2w_kernel(const typename Word<ES
     const int64_t i0 = it * T, j0 = jt * T;
     const W* s = src + bin + i0 + j0 * d.sj;
     W* o = dst + bout + j0 + i0 * d.si;
+    TNB_DCHECK(bin + min64(T, d.Di - i0) - 1 + (min64(T, d.Do - j0) - 1) * d.sj + i0 + j0 * d.sj < d.n &&
+                   bout + min64(T, d.Do - j0) - 1 + (min64(T, d.Di - i0) - 1) * d.si + j0 + i0 * d.si < d.n,
+               "t2w tile out of range");
     if ((i0 + T <= d.Di) && (j0 + T <= d.Do)) {
       // read: rows j (input-contiguous along i), 16-byte vectors, all loads in flight
       uint4 v[ROWS_PER_WARP];
@@ -758,6 +765,7 @@ int make_plan(int es, int rank, const int64_t* shape, const int32_t* perm, Plan&
       td.tj = (td.Do + T - 1) / T;
       int64_t nbatch = n / (td.Di * td.Do);
       td.ntiles = nbatch * td.ti * td.tj;
+      td.n = n;
       if (td.ntiles < (int64_t(1) << 31)) {
         td.ti_div = FastDiv((uint32_t)td.ti);
         td.tj_div = FastDiv((uint32_t)td.tj);
