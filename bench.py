@@ -332,6 +332,7 @@ def lawr_macs(tnb, chi, d=2, D=5):
 
 
 E2E_CHUNKS = int(os.environ.get("TNB_E2E_CHUNKS", "2"))  # 1-8 swept with double buffering: 2 best
+E2E_SETS = int(os.environ.get("TNB_E2E_SETS", "3"))      # buffer sets rotated by the serving loop (3: 1.907 vs 1.931 ms)
 
 
 def lawr_e2e(tnb, inp, order, steps, warmup, dist, flop):
@@ -341,7 +342,7 @@ def lawr_e2e(tnb, inp, order, steps, warmup, dist, flop):
     ordered only after the launch that last read that set, so step i+1's uploads overlap step
     i's kernels."""
     import torch
-    sets = [make_network(tnb, WL.LAWR_NET, inp) for _ in range(2)]
+    sets = [make_network(tnb, WL.LAWR_NET, inp) for _ in range(E2E_SETS)]
     pinned = [{nm: torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for nm, a in inp.items()} for _ in sets]
     h2d = sum(p.numel() * p.element_size() for p in pinned[0].values())
     probe = sets[0][0].launch().get_block_().contiguous().storage()
@@ -349,11 +350,12 @@ def lawr_e2e(tnb, inp, order, steps, warmup, dist, flop):
     first_use = tnb.tree_leaves(tnb.parse_order(order))
 
     def step(i):
-        n, ts = sets[i % 2]
+        n, ts = sets[i % E2E_SETS]
         for nm in first_use:
             big = pinned[0][nm].numel() * pinned[0][nm].element_size() >= (8 << 20)
-            ts[nm].get_block_().upload_(pinned[i % 2][nm], chunks=E2E_CHUNKS if big else 1, after=n.done_event)
-        n.launch(host_out=outs[i % 2])
+            ts[nm].get_block_().upload_(pinned[i % E2E_SETS][nm], chunks=E2E_CHUNKS if big else 1,
+                                        after=n.done_event)
+        n.launch(host_out=outs[i % E2E_SETS])
 
     def loop(k):
         return lambda: [step(i) for i in range(k)]
