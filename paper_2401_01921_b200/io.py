@@ -197,9 +197,7 @@ def _cached_segments(ut, packed_to_slab):
             _PAYLOAD_SEGS.clear()
         hit = _PAYLOAD_SEGS[key] = (segs, int(sizes.sum()), int(offs[0]) * isz)
     segs, nbytes, off0 = hit
-    from . import dense as _dense
-    _dense._await(slab)
-    return segs, slab.data_ptr() + off0, nbytes
+    return segs, slab.data_ptr() + off0, nbytes, slab
 
 
 def _shapes_of(ut):
@@ -214,18 +212,22 @@ def payload_nbytes(ut):
     return sum(b.size for b in ut.get_blocks_()) * ut.dtype.itemsize
 
 
-def upload_payload_(ut, host):
+def upload_payload_(ut, host, after=None):
     """Fill every block of ``ut`` from a host payload (pinned CPU tensor or numpy array in
     the packed ``.utn`` layout, same dtype): one host->device copy into a staging buffer and
     one ``tnb_copy2d_batched`` scatter to the blocks' places in the slab, both queued on the
-    current stream (asynchronous for pinned input). Blocks must be stored contiguously
-    (a freshly built or loaded tensor)."""
+    engine's upload stream (asynchronous for pinned input); the next engine call reading the
+    tensor waits for them on its own stream (as ``DenseTensor.upload_``). ``after`` (a CUDA
+    event): order the upload after this event only instead of after everything queued on the
+    current stream (serving loops: the event that follows the last read of the old
+    contents). Blocks must be stored contiguously (a freshly built or loaded tensor)."""
     h = torch.as_tensor(host) if not isinstance(host, torch.Tensor) else host
     fast = _cached_segments(ut, True)
     if fast is not None and ut._blk is not None and ut._blk and ut._blk[0]._perm != tuple(range(ut.rank)):
         fast = None  # lazily permuted blocks: the payload is in logical order
     if fast is not None:
-        segs, base, nbytes = fast
+        segs, base, nbytes, slab = fast
+        owners = [slab]
     else:
         blocks = ut.get_blocks_()
         if any(not b.is_contiguous for b in blocks):
@@ -237,21 +239,39 @@ def upload_payload_(ut, host):
         return ut
     if fast is None:
         segs, base, _ = _segments(blocks, ut.dtype.itemsize, packed_to_slab=True)
-    staging = torch.empty(nbytes, dtype=torch.uint8, device=dense.device())
-    staging.copy_(h.reshape(-1).view(torch.uint8), non_blocking=True)
-    _lib.copy2d_batched(staging.data_ptr(), base, segs, dense.stream_handle())
+    if fast is None:
+        owners = list({id(o): o for o in (dense._owner(b) for b in blocks)}.values())
+    up = dense.upload_stream()
+    if after is None:
+        up.wait_stream(torch.cuda.current_stream())  # WAR: earlier readers of the blocks
+    else:
+        up.wait_event(after)
+    for o in owners:
+        o.record_stream(up)
+    with torch.cuda.stream(up):
+        staging = torch.empty(nbytes, dtype=torch.uint8, device=dense.device())
+        staging.copy_(h.reshape(-1).view(torch.uint8), non_blocking=True)
+        _lib.copy2d_batched(staging.data_ptr(), base, segs, up.cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(up)
+    for o in owners:  # a still-pending earlier upload into o precedes ev on the same stream
+        o._tnb_ready = ev
     return ut
 
 
-def download_payload(ut, host):
+def download_payload(ut, host, done=None):
     """Copy every block of ``ut`` into a host payload (pinned CPU tensor in the packed
     ``.utn`` layout): one gather launch and one device->host copy queued on the current
-    stream; synchronise (or wait on an event) before reading ``host``."""
+    stream; synchronise (or wait on an event) before reading ``host``. With ``done`` (a CUDA
+    event) both run on the engine's download stream instead, after everything queued on the
+    current stream, and ``done`` is recorded once ``host`` holds the payload -- the current
+    stream moves on to the next step's work meanwhile."""
     fast = _cached_segments(ut, False)
     if fast is not None and ut._blk is not None and ut._blk and ut._blk[0]._perm != tuple(range(ut.rank)):
         fast = None
     if fast is not None:
-        segs, base, nbytes = fast
+        segs, base, nbytes, slab = fast
+        dense._await(slab)
     else:
         blocks = [b.contiguous() for b in ut.get_blocks_()]
         nbytes = payload_nbytes(ut)
@@ -262,9 +282,20 @@ def download_payload(ut, host):
         return host
     if fast is None:
         segs, base, _ = _segments(blocks, ut.dtype.itemsize, packed_to_slab=False)
-    packed = torch.empty(nbytes, dtype=torch.uint8, device=dense.device())
-    _lib.copy2d_batched(base, packed.data_ptr(), segs, dense.stream_handle())
-    host.reshape(-1).view(torch.uint8).copy_(packed, non_blocking=True)
+    if done is None:
+        packed = torch.empty(nbytes, dtype=torch.uint8, device=dense.device())
+        _lib.copy2d_batched(base, packed.data_ptr(), segs, dense.stream_handle())
+        host.reshape(-1).view(torch.uint8).copy_(packed, non_blocking=True)
+        return host
+    d2h = dense.download_stream()
+    d2h.wait_stream(torch.cuda.current_stream())
+    for o in ([slab] if fast is not None else {id(dense._owner(b)): dense._owner(b) for b in blocks}.values()):
+        o.record_stream(d2h)  # the blocks may be freed (to the current stream's pool) before d2h reads them
+    with torch.cuda.stream(d2h):
+        packed = torch.empty(nbytes, dtype=torch.uint8, device=dense.device())
+        _lib.copy2d_batched(base, packed.data_ptr(), segs, d2h.cuda_stream)
+        host.reshape(-1).view(torch.uint8).copy_(packed, non_blocking=True)
+        done.record(d2h)
     return host
 
 

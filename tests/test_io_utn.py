@@ -148,3 +148,42 @@ def test_payload_upload_download_roundtrip(cuda):
     torch.cuda.synchronize()
     want = np.concatenate([b.numpy().reshape(-1) for b in P.get_blocks_()])
     assert np.array_equal(host.numpy().view(np.float64), want)
+
+
+@pytest.mark.gpu
+def test_payload_serving_loop_async_ordering(cuda):
+    """upload_payload_ runs on the upload stream and download_payload(done=ev) on the download
+    stream: a two-set serving loop whose inputs change every step (refills ordered only after
+    the contraction that last read the set) returns every step's exact result."""
+    import torch
+    import bench
+    import paper_2401_01921_b200 as tnb
+    from paper_2401_01921_b200 import io as tio
+    pairs = [bench.c4_tensors(tnb, seed=11 + 2 * j) for j in range(3)]
+    payloads, expect = [], []
+    for A, E in pairs:
+        hA = torch.empty(tio.payload_nbytes(A), dtype=torch.uint8, pin_memory=True)
+        hE = torch.empty(tio.payload_nbytes(E), dtype=torch.uint8, pin_memory=True)
+        A.download_payload(hA)
+        E.download_payload(hE)
+        o = tnb.contract(A, E)
+        ho = torch.empty(tio.payload_nbytes(o), dtype=torch.uint8, pin_memory=True)
+        o.download_payload(ho)
+        payloads.append((hA, hE))
+        expect.append(ho)
+    torch.cuda.synchronize()
+    sets = [bench.c4_tensors(tnb, seed=99 + k) for k in range(2)]
+    read = [None, None]
+    outs = [torch.empty_like(expect[0]) for _ in range(9)]
+    for i in range(9):
+        k = i % 2
+        hA, hE = payloads[i % 3]
+        sets[k][0].upload_payload_(hA, after=read[k])
+        sets[k][1].upload_payload_(hE, after=read[k])
+        o = tnb.contract(*sets[k])
+        read[k] = torch.cuda.Event()
+        read[k].record()
+        o.download_payload(outs[i], done=torch.cuda.Event())
+    torch.cuda.synchronize()
+    for i in range(9):
+        assert torch.equal(outs[i], expect[i % 3]), i
