@@ -287,6 +287,217 @@ __global__ void __launch_bounds__(WARPS * 32) narrow_kernel(const typename Elem<
   }
 }
 
+// Row-panel variant for the layout the T1.W step of L.A.W.R really has (T1[p][vr][b][w],
+// rows (vr, b), contracted (w, p)): the contracted index splits into an INNER digit of
+// stride 1 (w, extent Kin) and outer digits (p), and consecutive rows step by exactly Kin.
+// Then, for a panel of ROWS consecutive rows inside one run of the innermost row digit,
+// each outer k value j covers ONE contiguous span of ROWS * Kin elements, and the panel's
+// ROWS x N outputs are one contiguous run of C. Every warp runs its own pipeline over its
+// panels: the TMA engine moves the spans into a 3-deep ring of shared-memory panels
+// (cp.async.bulk, completion counted in bytes on one mbarrier per slot) and the finished
+// panel back out (cp.async.bulk shared -> global), so the LSU only serves the FMA operands
+// -- the per-lane 8-byte gathers of narrow_kernel touch a sector per lane and its stores
+// go through the L1 a sector at a time.
+struct SlabDesc {
+  int kin, kout;
+  int64_t so[32];         // element offset of outer k value j (added to the panel's row offset)
+  int16_t soff[32];       // k -> offset in the staged panel: j * ROWS * Kin + kin
+};
+
+template <bool CPLX, int NMAX, int KMAX, int WARPS, int ROWS, bool EXACT>
+__global__ void __launch_bounds__(WARPS * 32) narrow_slab_kernel(const typename Elem<CPLX>::T* __restrict__ A,
+                                                          const typename Elem<CPLX>::T* __restrict__ B,
+                                                          typename Elem<CPLX>::T* __restrict__ C,
+                                                          const __grid_constant__ GemmDesc d,
+                                                          const __grid_constant__ SlabDesc s) {
+  using T = typename Elem<CPLX>::T;
+  constexpr int ES = CPLX ? 16 : 8;
+#ifndef TNB_SLAB_NB
+#define TNB_SLAB_NB 2
+#endif
+  constexpr int NB = TNB_SLAB_NB;  // panels in the ring (2 / 4 warps: 34.8 us at chi = 1024 f64, 3 / 2: 36.6)
+  constexpr int RPL = ROWS / 32;  // rows per lane, multiplied together (one B read feeds all)
+  static_assert(NMAX % 2 == 0, "B rows are read as pairs");
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(16) T Bs[KMAX * NMAX];
+  __shared__ __align__(8) uint64_t bars[WARPS][NB];
+  const int K = EXACT ? KMAX : d.K, N = EXACT ? NMAX : d.N;  // EXACT: sizes known at compile time
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int panel = ROWS * K, outsz = ROWS * N;  // elements
+  T* wbase = reinterpret_cast<T*>(smem) + (size_t)warp * (NB * panel + outsz);
+  T* out = wbase + NB * panel;
+  uint64_t* bar = bars[warp];
+  for (int i = threadIdx.x; i < KMAX * NMAX; i += blockDim.x) {
+    const int k = i / NMAX, n = i - k * NMAX;
+    T v;
+    if constexpr (CPLX) v = make_double2(0.0, 0.0);
+    else v = 0.0;
+    if (k < K && n < N) v = B[group_offset(d.kB, k) + group_offset(d.colB, n)];
+    Bs[i] = v;
+  }
+  if (lane == 0) {
+    for (int b = 0; b < NB; ++b) detail::mbar_init(&bar[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t npan = (int64_t)d.M / ROWS;
+  const int64_t step = (int64_t)gridDim.x * WARPS;
+  const uint32_t span_bytes = (uint32_t)(ROWS * s.kin * ES);
+  auto issue = [&](int64_t pn, int b) {  // lane 0 only
+    const T* src = A + group_offset(d.rowA, (uint32_t)(pn * ROWS));
+    const uint32_t dst = smem_u32(wbase + b * panel);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&bar[b])),
+                 "r"(span_bytes * (uint32_t)s.kout)
+                 : "memory");
+    for (int j = 0; j < s.kout; ++j) detail::bulk_load(dst + j * span_bytes, src + s.so[j], span_bytes, &bar[b]);
+  };
+  const int64_t first = (int64_t)blockIdx.x * WARPS + warp;
+  if (lane == 0)
+    for (int b = 0; b < NB; ++b)
+      if (first + b * step < npan) issue(first + b * step, b);
+  int it = 0;
+  for (int64_t pn = first; pn < npan; pn += step, ++it) {
+    const int b = it % NB;
+    detail::mbar_wait(&bar[b], (uint32_t)(it / NB) & 1);
+    const T* buf = wbase + b * panel;
+    // the previous panel's bulk store must have finished READING the out buffer
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    __syncwarp();
+    if constexpr (!CPLX) {
+      double acc[RPL][NMAX];
+#pragma unroll
+      for (int h = 0; h < RPL; ++h)
+#pragma unroll
+        for (int n = 0; n < NMAX; ++n) acc[h][n] = 0.0;
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k < K) {
+          double a[RPL];
+#pragma unroll
+          for (int h = 0; h < RPL; ++h) a[h] = buf[(h * 32 + lane) * s.kin + s.soff[k]];
+#pragma unroll
+          for (int n = 0; n < NMAX; n += 2) {
+            const double2 bb = *reinterpret_cast<const double2*>(&Bs[k * NMAX + n]);
+#pragma unroll
+            for (int h = 0; h < RPL; ++h) {
+              acc[h][n] = fma(a[h], bb.x, acc[h][n]);
+              acc[h][n + 1] = fma(a[h], bb.y, acc[h][n + 1]);
+            }
+          }
+        }
+#pragma unroll
+      for (int h = 0; h < RPL; ++h) {
+        double* o = out + (h * 32 + lane) * N;
+        if ((N & 1) == 0) {
+#pragma unroll
+          for (int n = 0; n < NMAX; n += 2)
+            if (n < N) *reinterpret_cast<double2*>(o + n) = make_double2(acc[h][n], acc[h][n + 1]);
+        } else {
+#pragma unroll
+          for (int n = 0; n < NMAX; ++n)
+            if (n < N) o[n] = acc[h][n];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < RPL; ++h) {
+        double ar[NMAX], ai[NMAX];
+#pragma unroll
+        for (int n = 0; n < NMAX; ++n) ar[n] = ai[n] = 0.0;
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+          if (k < K) {
+            const double2 a = buf[(h * 32 + lane) * s.kin + s.soff[k]];
+#pragma unroll
+            for (int n = 0; n < NMAX; ++n) {
+              const double2 bb = Bs[k * NMAX + n];
+              ar[n] = fma(a.x, bb.x, ar[n]);
+              ar[n] = fma(-a.y, bb.y, ar[n]);
+              ai[n] = fma(a.x, bb.y, ai[n]);
+              ai[n] = fma(a.y, bb.x, ai[n]);
+            }
+          }
+        double2* o = out + (h * 32 + lane) * N;
+#pragma unroll
+        for (int n = 0; n < NMAX; ++n)
+          if (n < N) o[n] = make_double2(ar[n], ai[n]);
+      }
+    }
+    // generic-proxy writes of the out buffer -> visible to the bulk store (async proxy)
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(C + pn * ROWS * N),
+                   "r"(smem_u32(out)), "r"((uint32_t)(outsz * ES))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      // every lane's reads of slot b are complete (their values fed the outputs): refill it
+      if (pn + NB * step < npan) issue(pn + NB * step, b);
+    }
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
+// host mirror of group_offset
+int64_t host_group_offset(const Group& g, uint32_t idx) {
+  int64_t off = 0;
+  for (int q = g.n - 1; q >= 0; --q) {
+    const uint32_t dig = idx % (uint32_t)g.dim[q];
+    idx /= (uint32_t)g.dim[q];
+    off += (int64_t)dig * g.stride[q];
+  }
+  return off;
+}
+
+// The row-panel layout of narrow_slab_kernel, if the operand has it.
+bool slab_layout(const GemmDesc& d, int es, const void* A, const void* C, int kRows, SlabDesc& s) {
+  memset(&s, 0, sizeof(s));
+  if (d.rowA.n < 1 || d.kA.n < 1 || d.K > 32 || d.M % kRows) return false;
+  // the contracted digit of stride 1
+  int qi = -1;
+  for (int q = 0; q < d.kA.n; ++q)
+    if (d.kA.stride[q] == 1) qi = q;
+  if (qi < 0) return false;
+  const int kin = d.kA.dim[qi];
+  const int rq = d.rowA.n - 1;  // innermost row digit: consecutive rows step by kin
+  if (d.rowA.stride[rq] != kin || d.rowA.dim[rq] % kRows) return false;
+  s.kin = kin;
+  s.kout = d.K / kin;
+  if (s.kout * kin != d.K || s.kout > 32) return false;
+  // enumerate k: (outer offset -> j, kin digit)
+  std::vector<int64_t> outers;
+  for (int k = 0; k < d.K; ++k) {
+    uint32_t idx = (uint32_t)k;
+    int64_t outer = 0;
+    int kd = 0;
+    for (int q = d.kA.n - 1; q >= 0; --q) {
+      const int dig = (int)(idx % (uint32_t)d.kA.dim[q]);
+      idx /= (uint32_t)d.kA.dim[q];
+      if (q == qi) kd = dig;
+      else outer += (int64_t)dig * d.kA.stride[q];
+    }
+    int j = -1;
+    for (size_t x = 0; x < outers.size(); ++x)
+      if (outers[x] == outer) j = (int)x;
+    if (j < 0) {
+      j = (int)outers.size();
+      outers.push_back(outer);
+      if (j >= 32) return false;
+      s.so[j] = outer;
+    }
+    s.soff[k] = (int16_t)(j * kRows * kin + kd);
+  }
+  if ((int)outers.size() != s.kout) return false;
+  // bulk copies: every span starts 16-byte aligned (panel row offsets: outer row digits'
+  // strides and the panel step kRows * kin; outer k offsets; the base pointer) and every
+  // output run too
+  bool al = (reinterpret_cast<uintptr_t>(A) % 16) == 0;
+  for (int q = 0; q < rq; ++q) al = al && (d.rowA.stride[q] * es) % 16 == 0;
+  for (int j = 0; j < s.kout; ++j) al = al && (s.so[j] * es) % 16 == 0;
+  if (!al || (kRows * kin * es) % 16 || (kRows * d.N * es) % 16 || (reinterpret_cast<uintptr_t>(C) % 16)) return false;
+  return true;
+}
+
 template <bool CPLX, int NMAX, int KMAX>
 int run_narrow(const void* A, const void* B, void* C, const GemmDesc& d, cudaStream_t st) {
   using T = typename Elem<CPLX>::T;
@@ -296,6 +507,45 @@ int run_narrow(const void* A, const void* B, void* C, const GemmDesc& d, cudaStr
   if (per_sm == 0) {
     TNB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, 0));
     if (per_sm < 1) per_sm = 1;
+  }
+  SlabDesc sd;
+  static const bool no_slab = getenv("TNB_NO_SLAB") != nullptr;  // dev A/B switch
+#ifndef TNB_SLAB_SW
+#define TNB_SLAB_SW 4
+#endif
+#ifndef TNB_SLAB_ROWS
+#define TNB_SLAB_ROWS 64
+#endif
+  constexpr int SROWS = CPLX ? 32 : TNB_SLAB_ROWS, SW = TNB_SLAB_SW;
+  if (!no_slab && slab_layout(d, CPLX ? 16 : 8, A, C, SROWS, sd)) {
+    auto sk = (d.K == KMAX && d.N == NMAX) ? narrow_slab_kernel<CPLX, NMAX, KMAX, SW, SROWS, true>
+                                           : narrow_slab_kernel<CPLX, NMAX, KMAX, SW, SROWS, false>;
+    const size_t smem = (size_t)SW * (TNB_SLAB_NB * SROWS * d.K + SROWS * d.N) * (CPLX ? 16 : 8);
+    // occupancy per (kernel, shared-memory size), set up once each
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<const void*, size_t>, int>> occ_cache;
+    int slab_per_sm = 0;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      for (auto& e : occ_cache)
+        if (e.first.first == (const void*)sk && e.first.second == smem) slab_per_sm = e.second;
+      if (!slab_per_sm) {
+        TNB_CUDA_CHECK(cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TNB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&slab_per_sm, sk, SW * 32, smem));
+        if (slab_per_sm < 1) slab_per_sm = 1;
+        occ_cache.push_back({{(const void*)sk, smem}, slab_per_sm});
+      }
+    }
+    const int64_t panels = d.M / SROWS;
+    const int64_t grid = std::min<int64_t>((panels + SW - 1) / SW, (int64_t)sm_count() * slab_per_sm);
+    {
+      KTimer kt(TNB_KF_GEMM_SKINNY, st, 2.0 * d.M * (double)d.N * d.K * (CPLX ? 4 : 1));
+      sk<<<(unsigned)grid, SW * 32, smem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B), static_cast<T*>(C),
+                                                d, sd);
+    }
+    count_launch();
+    TNB_CUDA_CHECK(cudaGetLastError());
+    return TNB_OK;
   }
   const int64_t chunks = ((int64_t)d.M + 31) / 32;
   const int64_t grid = std::min<int64_t>((chunks + WARPS - 1) / WARPS, (int64_t)sm_count() * per_sm);
@@ -734,6 +984,8 @@ int dispatch(const void* A, const void* B, void* C, GemmDesc& d, cudaStream_t st
   // the memory-bound kernels write packed rows; a strided output (column panel) takes stream-K
   const bool packed = d.out_ld == d.N;
   if (packed && (int64_t)d.M * d.N <= 16) return run_dot<CPLX>(A, B, C, d, st);
+  // (N, K <= 10: the MPO step of L.A.W.R with D = 5, d = 2 -- registers sized to it)
+  if (packed && d.N <= 10 && d.K <= 10 && d.M >= 4096) return run_narrow<CPLX, 10, 10>(A, B, C, d, st);
   if (packed && d.N <= 16 && d.K <= 16 && d.M >= 4096) return run_narrow<CPLX, 16, 16>(A, B, C, d, st);
   if constexpr (!CPLX)
     if (packed && d.N <= 16 && d.K <= 32 && d.M >= 4096) return run_narrow<CPLX, 16, 32>(A, B, C, d, st);

@@ -273,3 +273,29 @@ def test_stream_k_gemms_run_beside_a_long_kernel_stream(cuda):
     assert rel_fro(out, want) <= 1e-12
     assert all(np.array_equal(g, w) for g, w in zip(got_bs, ref_bs))
     del y
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.complex128])
+def test_narrow_row_panel_path(cuda, dt):
+    """The T1.W layout (T1[p][vr][b][w], contracted (w, p) -- the stride-1 digit w, rows
+    stepping by its extent): narrow_slab_kernel's staged row panels vs numpy, for both
+    orders of the contracted labels, odd / even inner extents and several outer extents."""
+    rng = np.random.default_rng(77)
+
+    def arr(shape):
+        x = rng.standard_normal(shape)
+        if dt == np.complex128:
+            x = x + 1j * rng.standard_normal(shape)
+        return x.astype(dt)
+
+    for (p, vr, b, w, w2, q) in [(2, 64, 128, 5, 5, 2), (2, 64, 64, 4, 3, 2), (3, 8, 512, 3, 2, 5), (1, 4, 1024, 10, 16, 1),
+                                 (2, 64, 64, 3, 3, 1), (2, 32, 256, 5, 5, 2)]:
+        t1, W = arr((p, vr, b, w)), arr((w, w2, q, p))
+        T1 = UniTensor(storage.from_numpy(t1), labels=["p", "vr", "b", "w"])
+        for wl, wperm in ((["w", "w2", "q", "p"], W), (["p", "q", "w2", "w"], W.transpose(3, 2, 1, 0).copy())):
+            Wt = UniTensor(storage.from_numpy(wperm), labels=wl)
+            got = contract(T1, Wt)
+            want = np.einsum("pvbw,wxqp->vbxq", t1, W)
+            if wl[1] == "q":
+                want = want.transpose(0, 1, 3, 2)
+            assert rel_fro(got.numpy(), want) <= 1e-13, ((p, vr, b, w), wl)
