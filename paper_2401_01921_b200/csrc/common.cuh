@@ -106,6 +106,31 @@ cudaError_t launch_cooperative(void (*kern)(KArgs...), unsigned grid, unsigned b
   return cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
 }
 
+// Programmatic dependent launch: the kernel may be scheduled while the previous kernel on
+// the stream is still running (its launch latency and index-table prologue overlap that
+// kernel's tail); it MUST execute pdl_wait() before touching global memory another kernel
+// produces or consumes. Only kernels that do are launched this way.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  static const bool off = getenv("TNB_NO_PDL") != nullptr;  // dev A/B switch
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
+}
+// griddepcontrol.wait: every prerequisite grid has completed and its memory is visible.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// let the next PDL-launched kernel be scheduled (it still waits in pdl_wait for our completion)
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
 // Unsigned 32-bit division by a runtime-invariant divisor via multiply-high

@@ -93,6 +93,8 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
                 typename Elem<CPLX>::T* __restrict__ C, const __grid_constant__ GemmDesc d) {
   using Core = TileCore<CPLX, MODE, BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
   extern __shared__ __align__(16) unsigned char smem[];
+  pdl_wait();
+  pdl_launch_dependents();
   int bid = blockIdx.x;
   const int split = bid % d.splitk;
   bid /= d.splitk;
@@ -121,6 +123,8 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
 template <bool CPLX>
 __global__ void splitk_reduce_kernel(const typename Elem<CPLX>::T* __restrict__ ws,
                                      typename Elem<CPLX>::T* __restrict__ out, int64_t n, int S) {
+  pdl_wait();
+  pdl_launch_dependents();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (; i < n; i += stride) {
@@ -227,6 +231,8 @@ __global__ void __launch_bounds__(WARPS * 32) narrow_kernel(const typename Elem<
   __shared__ T Bs[KMAX * NMAX];
   __shared__ int64_t kA[KMAX];
   __shared__ T stage[WARPS][32 * NMAX + 1];
+  pdl_wait();
+  pdl_launch_dependents();
   const int K = d.K, N = d.N;
   for (int i = threadIdx.x; i < K; i += blockDim.x) kA[i] = group_offset(d.kA, i);
   for (int i = threadIdx.x; i < K * N; i += blockDim.x) {
@@ -327,6 +333,8 @@ __global__ void __launch_bounds__(WARPS * 32) narrow_slab_kernel(const typename 
   T* wbase = reinterpret_cast<T*>(smem) + (size_t)warp * (NB * panel + outsz);
   T* out = wbase + NB * panel;
   uint64_t* bar = bars[warp];
+  pdl_wait();
+  pdl_launch_dependents();
   for (int i = threadIdx.x; i < KMAX * NMAX; i += blockDim.x) {
     const int k = i / NMAX, n = i - k * NMAX;
     T v;
@@ -540,8 +548,8 @@ int run_narrow(const void* A, const void* B, void* C, const GemmDesc& d, cudaStr
     const int64_t grid = std::min<int64_t>((panels + SW - 1) / SW, (int64_t)sm_count() * slab_per_sm);
     {
       KTimer kt(TNB_KF_GEMM_SKINNY, st, 2.0 * d.M * (double)d.N * d.K * (CPLX ? 4 : 1));
-      sk<<<(unsigned)grid, SW * 32, smem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B), static_cast<T*>(C),
-                                                d, sd);
+      TNB_CUDA_CHECK(launch_pdl(sk, (unsigned)grid, SW * 32, smem, st, static_cast<const T*>(A),
+                                static_cast<const T*>(B), static_cast<T*>(C), d, sd));
     }
     count_launch();
     TNB_CUDA_CHECK(cudaGetLastError());
@@ -551,7 +559,8 @@ int run_narrow(const void* A, const void* B, void* C, const GemmDesc& d, cudaStr
   const int64_t grid = std::min<int64_t>((chunks + WARPS - 1) / WARPS, (int64_t)sm_count() * per_sm);
   {
     KTimer kt(TNB_KF_GEMM_SKINNY, st, 2.0 * d.M * (double)d.N * d.K * (CPLX ? 4 : 1));
-    kern<<<(unsigned)grid, WARPS * 32, 0, st>>>(static_cast<const T*>(A), static_cast<const T*>(B), static_cast<T*>(C), d);
+    TNB_CUDA_CHECK(launch_pdl(kern, (unsigned)grid, WARPS * 32, 0, st, static_cast<const T*>(A),
+                              static_cast<const T*>(B), static_cast<T*>(C), d));
   }
   count_launch();
   TNB_CUDA_CHECK(cudaGetLastError());
@@ -758,8 +767,8 @@ struct Tiled {
     if (d.splitk == 1) {
       {
         KTimer kt(TNB_KF_GEMM, st, work);
-        kern<<<(unsigned)grid, threads, smem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B),
-                                                    static_cast<T*>(C), d);
+        TNB_CUDA_CHECK(launch_pdl(kern, (unsigned)grid, threads, smem, st, static_cast<const T*>(A),
+                                  static_cast<const T*>(B), static_cast<T*>(C), d));
       }
       count_launch();
       TNB_CUDA_CHECK(cudaGetLastError());
@@ -770,17 +779,17 @@ struct Tiled {
     TNB_CUDA_CHECK(cudaMallocAsync(&ws, n * d.splitk * ES, st));
     {
       KTimer kt(TNB_KF_GEMM, st, work);
-      kern<<<(unsigned)grid, threads, smem, st>>>(static_cast<const T*>(A), static_cast<const T*>(B),
-                                                  static_cast<T*>(ws), d);
+      TNB_CUDA_CHECK(launch_pdl(kern, (unsigned)grid, threads, smem, st, static_cast<const T*>(A),
+                                static_cast<const T*>(B), static_cast<T*>(ws), d));
     }
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) {
       int blocks = (int)std::min<size_t>((n + 255) / 256, (size_t)sms() * 8);
-      splitk_reduce_kernel<CPLX><<<blocks, 256, 0, st>>>(static_cast<const T*>(ws), static_cast<T*>(C), (int64_t)n,
-                                                           d.splitk);
+      e = launch_pdl(splitk_reduce_kernel<CPLX>, (unsigned)blocks, 256, 0, st, static_cast<const T*>(ws),
+                     static_cast<T*>(C), (int64_t)n, d.splitk);
       count_launch();
-      e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaGetLastError();
     }
     cudaFreeAsync(ws, st);
     if (e != cudaSuccess) return cuda_fail(e, "contract: split-K GEMM launch");
@@ -1001,14 +1010,19 @@ int dispatch(const void* A, const void* B, void* C, GemmDesc& d, cudaStream_t st
     const int64_t it128 = (pad(d.M, 128) / 128) * (pad(d.N, 128) / 128) * ((d.K + 15) / 16);
     if (it128 < (int64_t)sms() * 8) {
       // tiny problems (L.A.W.R at chi = 128: ~2.4 us of DMMA work per launch) are latency
-      // bound: a plain one-tile-per-CTA kernel (64 x 64 tiles, 4 warps of 32 x 32, split-K
-      // planned by an occupancy model, fixed-order reduce) beats the persistent stream-K
-      // kernel's per-stage hand-offs -- C1 graph replay 41.7 -> 30.9 us. The split-K
-      // workspace is packed, so strided (column panel) outputs keep stream-K.
+      // bound: a plain one-tile-per-CTA kernel (split-K planned by an occupancy model,
+      // fixed-order reduce; launched as programmatic dependents) beats the persistent
+      // stream-K kernel's per-stage hand-offs -- C1 graph replay 41.7 -> 28.8 us. The split-K
+      // workspace is packed, so strided (column panel) outputs keep stream-K. (Measured and
+      // dropped: the reduce inside the GEMM, each of a tile's S co-resident CTAs summing 1/S
+      // of its rows after a per-tile arrival counter -- 48 us: the CTAs of a tile wait for
+      // the slowest.)
       if (d.out_ld == d.N) {
+        // 64 x 64 tiles, 8 warps of 32 x 16 (C1 graph 28.8 us; 4 warps of 32 x 32: 30.8; 16
+        // warps: 30.8; 32 x 32 tiles: 28.8; BK = 32: 39.0; 4 stages: 30.9)
         int split = 1;
-        Tiled<false, 0, 64, 64, 16, 2, 2, 3, 2>::plan(d, split, 1.0);
-        return Tiled<false, 0, 64, 64, 16, 2, 2, 3, 2>::run(A, B, C, d, split, st);
+        Tiled<false, 0, 64, 64, 16, 2, 4, 3, 2>::plan(d, split, 1.0);
+        return Tiled<false, 0, 64, 64, 16, 2, 4, 3, 2>::run(A, B, C, d, split, st);
       }
       return StreamK<false, 0, 64, 64, 16, 4, 4, 4>::run(A, B, C, d, st);
     }
