@@ -93,8 +93,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
                 typename Elem<CPLX>::T* __restrict__ C, const __grid_constant__ GemmDesc d) {
   using Core = TileCore<CPLX, MODE, BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
   extern __shared__ __align__(16) unsigned char smem[];
-  pdl_wait();
-  pdl_launch_dependents();
+  pdl_launch_dependents();  // (pdl_wait: in the mainloop, after the index tables)
   int bid = blockIdx.x;
   const int split = bid % d.splitk;
   bid /= d.splitk;
@@ -697,6 +696,50 @@ struct Cfg {
 
 int sms() { return sm_count(); }
 
+// Persistent stream-K workspace (eager launches): partials, then one flag per CTA.
+struct SkWorkspace {
+  std::mutex mu;
+  void* mem = nullptr;
+  size_t flags_off = 0;  // bytes of partials
+  int nflags = 0;
+  int device = -1;
+  cudaEvent_t ev = nullptr;
+  cudaStream_t last = nullptr;
+  int acquire(size_t partial_bytes, int G, cudaStream_t st) {
+    int dev = 0;
+    TNB_CUDA_CHECK(cudaGetDevice(&dev));
+    if (dev != device || partial_bytes > flags_off || G > nflags) {
+      if (mem) {
+        TNB_CUDA_CHECK(cudaDeviceSynchronize());
+        cudaFree(mem);
+        mem = nullptr;
+      }
+      if (ev && dev != device) {
+        cudaEventDestroy(ev);
+        ev = nullptr;
+      }
+      flags_off = std::max(partial_bytes, flags_off);
+      nflags = std::max(G, std::max(nflags, 1024));
+      TNB_CUDA_CHECK(cudaMalloc(&mem, flags_off + (size_t)nflags * 4));
+      TNB_CUDA_CHECK(cudaMemset(static_cast<char*>(mem) + flags_off, 0, (size_t)nflags * 4));
+      device = dev;
+      last = nullptr;
+    }
+    if (!ev) TNB_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    if (last && last != st) TNB_CUDA_CHECK(cudaStreamWaitEvent(st, ev, 0));
+    return TNB_OK;
+  }
+  int release(cudaStream_t st) {
+    TNB_CUDA_CHECK(cudaEventRecord(ev, st));
+    last = st;
+    return TNB_OK;
+  }
+};
+SkWorkspace& sk_workspace() {
+  static SkWorkspace* w = new SkWorkspace();  // never destroyed (process-lifetime device memory)
+  return *w;
+}
+
 // WS = 1: warp-specialised kernel (producer warpgroup + DMMA warps); 0: single-role kernel.
 template <bool CPLX, int MODE, int BM, int BN, int BK, int WM, int WN, int ST, int MINB, int WS = 0>
 struct Tiled {
@@ -774,9 +817,24 @@ struct Tiled {
       TNB_CUDA_CHECK(cudaGetLastError());
       return TNB_OK;
     }
+    // split-K partials: graph-owned memory under capture, else the process-wide persistent
+    // workspace -- no allocation / free nodes between the GEMM and its neighbours, so the
+    // programmatic-dependent launches chain (a cudaMallocAsync per call broke the chain)
     size_t n = (size_t)d.M * d.N;
     void* ws = nullptr;
-    TNB_CUDA_CHECK(cudaMallocAsync(&ws, n * d.splitk * ES, st));
+    SkWorkspace* w = nullptr;
+    std::unique_lock<std::mutex> lk;
+    if (capturing(st)) {
+      int rc = capture_device_ws(st, n * d.splitk * ES, &ws);
+      if (rc) return rc;
+    } else {
+      release_deferred_host();
+      w = &sk_workspace();
+      lk = std::unique_lock<std::mutex>(w->mu);
+      int rc = w->acquire(n * d.splitk * ES, 0, st);
+      if (rc) return rc;
+      ws = w->mem;
+    }
     {
       KTimer kt(TNB_KF_GEMM, st, work);
       TNB_CUDA_CHECK(launch_pdl(kern, (unsigned)grid, threads, smem, st, static_cast<const T*>(A),
@@ -791,55 +849,11 @@ struct Tiled {
       count_launch();
       if (e == cudaSuccess) e = cudaGetLastError();
     }
-    cudaFreeAsync(ws, st);
+    if (w) w->release(st);
     if (e != cudaSuccess) return cuda_fail(e, "contract: split-K GEMM launch");
     return TNB_OK;
   }
 };
-
-// Persistent stream-K workspace (eager launches): partials, then one flag per CTA.
-struct SkWorkspace {
-  std::mutex mu;
-  void* mem = nullptr;
-  size_t flags_off = 0;  // bytes of partials
-  int nflags = 0;
-  int device = -1;
-  cudaEvent_t ev = nullptr;
-  cudaStream_t last = nullptr;
-  int acquire(size_t partial_bytes, int G, cudaStream_t st) {
-    int dev = 0;
-    TNB_CUDA_CHECK(cudaGetDevice(&dev));
-    if (dev != device || partial_bytes > flags_off || G > nflags) {
-      if (mem) {
-        TNB_CUDA_CHECK(cudaDeviceSynchronize());
-        cudaFree(mem);
-        mem = nullptr;
-      }
-      if (ev && dev != device) {
-        cudaEventDestroy(ev);
-        ev = nullptr;
-      }
-      flags_off = std::max(partial_bytes, flags_off);
-      nflags = std::max(G, std::max(nflags, 1024));
-      TNB_CUDA_CHECK(cudaMalloc(&mem, flags_off + (size_t)nflags * 4));
-      TNB_CUDA_CHECK(cudaMemset(static_cast<char*>(mem) + flags_off, 0, (size_t)nflags * 4));
-      device = dev;
-      last = nullptr;
-    }
-    if (!ev) TNB_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    if (last && last != st) TNB_CUDA_CHECK(cudaStreamWaitEvent(st, ev, 0));
-    return TNB_OK;
-  }
-  int release(cudaStream_t st) {
-    TNB_CUDA_CHECK(cudaEventRecord(ev, st));
-    last = st;
-    return TNB_OK;
-  }
-};
-SkWorkspace& sk_workspace() {
-  static SkWorkspace* w = new SkWorkspace();  // never destroyed (process-lifetime device memory)
-  return *w;
-}
 
 // Host side of the stream-K kernel: one CTA per SM, workspace for split tiles.
 template <bool CPLX, int MODE, int BM, int BN, int BK, int WM, int WN, int ST>

@@ -143,6 +143,9 @@ struct TileCore {
     };
     for (int kt = 0; kt < STAGES && kt < KT; ++kt) fill_koff(kt);
     __syncthreads();
+    // programmatic dependent launch: everything above reads only kernel parameters, so it
+    // overlaps the previous kernel's tail; the operands may be that kernel's output
+    pdl_wait();
 
     auto issue = [&](int kt) {
       const int stage = kt % STAGES;

@@ -20,6 +20,9 @@ def ktime(fn, fam, n=10):
     tnb._lib.ktimer_reset()
     tnb._lib.ktimer_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # a sleeping kernel first: the host queues all n calls before the GPU reaches them, so the
+    # events see device time, not the host's per-call overhead
+    torch.cuda._sleep(int(os.environ.get("TNB_AB_SLEEP", "20000000")))
     e0.record()
     for _ in range(n):
         fn()
