@@ -335,7 +335,7 @@ E2E_CHUNKS = int(os.environ.get("TNB_E2E_CHUNKS", "2"))  # 1-8 swept with double
 E2E_SETS = int(os.environ.get("TNB_E2E_SETS", "3"))      # buffer sets rotated by the serving loop (3: 1.907 vs 1.931 ms)
 
 
-def lawr_e2e(tnb, inp, order, steps, warmup, dist, flop):
+def lawr_e2e(tnb, inp, order, steps, warmup, dist, flop, graph=False):
     """End to end through the public API: pinned host inputs -> HBM (upload_), launch, result
     streamed back to pinned host memory (launch(host_out=...)) every step. A serving loop:
     two networks with their own device inputs and pinned host buffers alternate, each refill
@@ -359,6 +359,36 @@ def lawr_e2e(tnb, inp, order, steps, warmup, dist, flop):
 
     def loop(k):
         return lambda: [step(i) for i in range(k)]
+    if graph:
+        # latency-bound sizes: each buffer set's whole step (input uploads, the launch, the
+        # result copy to its pinned buffer) captured once as a CUDA graph and replayed on the
+        # set's own stream -- one graph launch per step instead of the per-call host work
+        cur = torch.cuda.current_stream()
+        streams = [torch.cuda.Stream() for _ in sets]
+        graphs = []
+        for k, (n, ts) in enumerate(sets):
+            def step_k(n=n, ts=ts, k=k):
+                for nm in first_use:
+                    big = pinned[0][nm].numel() * pinned[0][nm].element_size() >= (8 << 20)
+                    ts[nm].get_block_().upload_(pinned[k][nm], chunks=E2E_CHUNKS if big else 1)
+                return n.launch(host_out=outs[k])
+            with torch.cuda.stream(streams[k]):
+                graphs.append(tnb.graphs.capture(step_k))
+        torch.cuda.synchronize()
+
+        def gstep(i):
+            k = i % E2E_SETS
+            streams[k].wait_stream(cur)
+            with torch.cuda.stream(streams[k]):
+                graphs[k].replay()
+
+        def loop(k):  # noqa: F811
+            def run():
+                for i in range(k):
+                    gstep(i)
+                for st_ in streams:
+                    cur.wait_stream(st_)
+            return run
     time_region(loop(max(2, warmup)), dist)
     ems = time_region(loop(steps), dist)
     lat = time_region(loop(1), dist)
@@ -366,10 +396,17 @@ def lawr_e2e(tnb, inp, order, steps, warmup, dist, flop):
     e2e = {"value": round(dist.sum(flop) / (ems / steps) / 1e6, 3), "unit": "GFLOP/s",
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ems / steps, 4),
            "single_step_latency_ms": round(lat, 4)}
+    if graph:
+        e2e["api"] = "graphs.capture(upload_ per input, Network.launch(host_out=...)) per buffer set"
+    # every set's host result is the network's output (a chunk-uploaded operand computes the
+    # root step panel by panel: other stream-K splits, so equal to rounding, not bit for bit)
+    torch.cuda.synchronize()
+    want = probe.cpu().numpy()
+    e2e["host_result_rel_err"] = _r(max(rel_err(o.reshape(want.shape).numpy(), want) for o in outs), 3)
     return e2e
 
 
-def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, graph=False, seed=1234):
+def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, graph=False, seed=1234, e2e_graph=False):
     """One L.A.W.R matvec per step (replicated per rank, weak scaling)."""
     import torch
     inp = WL.lawr_inputs(chi, dtype=dtype, seed=seed)  # same instance on every rank (replicas)
@@ -393,7 +430,11 @@ def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, graph=False,
         res["graph_ms_per_step"] = gms
         res["gflops_graph"] = dist.sum(flop) / gms / 1e6
     if e2e:
-        res["e2e"] = lawr_e2e(tnb, inp, order, steps, warmup, dist, flop)
+        if e2e_graph or os.environ.get("TNB_E2E_GRAPH"):
+            res["e2e"] = lawr_e2e(tnb, inp, order, steps, warmup, dist, flop, graph=True)
+            res["e2e_eager"] = lawr_e2e(tnb, inp, order, steps, warmup, dist, flop)
+        else:
+            res["e2e"] = lawr_e2e(tnb, inp, order, steps, warmup, dist, flop)
     # dominant kernel = the stream-K DMMA GEMM (A.L and T2.R): kernel timer over the same
     # timed region (flush, K steps)
     (n_g, ms_g, fl_g), (n_s, ms_s, _) = ktimer(tnb, lambda: time_steps(net.launch, steps, flush, dist),
@@ -998,7 +1039,8 @@ def main():
         only = os.environ.get("TNB_BENCH_ONLY")  # dev: comma-separated subset of workloads
 
         def w_c1():
-            r = gpu_lawr(tnb, 128, np.float64, max(10, args.steps), args.warmup, flush, dist, e2e=True, graph=True)
+            r = gpu_lawr(tnb, 128, np.float64, max(10, args.steps), args.warmup, flush, dist, e2e=True, graph=True,
+                         e2e_graph=True)
             detail["C1"] = {k: v for k, v in r.items() if k not in ("out", "inp")}
             cpu = cpu_lawr(128, np.float64, budget_s=2, max_iter=50) if cpu_on else None
             detail["C1"]["cpu_baseline"] = cpu

@@ -187,3 +187,34 @@ def test_payload_serving_loop_async_ordering(cuda):
     torch.cuda.synchronize()
     for i in range(9):
         assert torch.equal(outs[i], expect[i % 3]), i
+
+
+@pytest.mark.gpu
+def test_payload_step_captured_in_a_graph(cuda):
+    """The serving step (two payload uploads, contract, payload download) captured once with
+    graphs.capture replays with whatever the pinned host buffers hold at replay time."""
+    import torch
+    import bench
+    import paper_2401_01921_b200 as tnb
+    from paper_2401_01921_b200 import io as tio
+    src = [bench.c4_tensors(tnb, seed=41 + 2 * j) for j in range(2)]
+    A, E = bench.c4_tensors(tnb, seed=97)
+    hA = torch.empty(tio.payload_nbytes(A), dtype=torch.uint8, pin_memory=True)
+    hE = torch.empty(tio.payload_nbytes(E), dtype=torch.uint8, pin_memory=True)
+    out0 = tnb.contract(A, E)
+    hO = torch.empty(tio.payload_nbytes(out0), dtype=torch.uint8, pin_memory=True)
+
+    def step():
+        A.upload_payload_(hA)
+        E.upload_payload_(hE)
+        return tnb.contract(A, E).download_payload(hO)
+    g = tnb.graphs.capture(step)
+    for sa, se in src + src[::-1]:
+        sa.download_payload(hA)
+        se.download_payload(hE)
+        torch.cuda.synchronize()
+        want = torch.empty_like(hO)
+        tnb.contract(sa, se).download_payload(want)
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(hO, want)
