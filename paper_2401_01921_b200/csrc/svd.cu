@@ -48,6 +48,7 @@ struct SvdTask {
   double* norm;    // [m] scratch: |b_i|
   double* coef;    // [2m + 2] scratch: Gram-Schmidt coefficients (re, im) + the candidate's norm
   int m, n;
+  int bsz, nb;     // block kernel: rows per block, blocks (a multiple of 2 x kCluster)
 };
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -133,13 +134,25 @@ __device__ __forceinline__ void stcg(T* p, T v) {
 // Returns false if the pair is already orthogonal to the threshold.
 __device__ __forceinline__ bool rotation(double al, double be, double gre, double gim, double thresh, double& c,
                                          double& s, double& pr, double& pi) {
-  const double ga = sqrt(gre * gre + gim * gim);
-  if (!(ga > thresh * sqrt(al * be)) || al == 0.0 || be == 0.0) return false;
-  pr = gre / ga;  // e^{-i phi} = conj(g) / |g|
-  pi = -gim / ga;
-  const double zeta = (be - al) / (2.0 * ga);
-  const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-  c = 1.0 / sqrt(1.0 + tt * tt);
+  // (one sqrt, one division, one reciprocal square root on the dependent chain -- the
+  // block kernel's inner rounds wait on it -- instead of three sqrt and four divisions)
+  const double g2 = gre * gre + gim * gim;
+  if (!(g2 > thresh * thresh * (al * be)) || al == 0.0 || be == 0.0) return false;
+  double ga;
+  if (gim == 0.0) {  // real rows: the phase is the sign
+    ga = fabs(gre);
+    pr = copysign(1.0, gre);
+    pi = 0.0;
+  } else {
+    ga = sqrt(g2);
+    const double inv = 1.0 / ga;
+    pr = gre * inv;  // e^{-i phi} = conj(g) / |g|
+    pi = -gim * inv;
+  }
+  // tan of the rotation angle, Rutishauser's stable form: t = sign(d) 2|g| / (|d| + sqrt(d^2 + 4|g|^2))
+  const double d = be - al;
+  const double tt = copysign(2.0 * ga, d) / (fabs(d) + sqrt(fma(d, d, 4.0 * g2)));
+  c = rsqrt(fma(tt, tt, 1.0));
   s = c * tt;
   return true;
 }
@@ -228,6 +241,55 @@ __device__ void complete_rows(typename Sc<CPLX>::T* __restrict__ VH, int r0, int
       if (ok) break;
     }
   }
+}
+
+// ---- finalize: sigma_i = |b_i| -> rank (descending, ties by row) -> U = Q^H, S, Vh = B / S
+template <bool CPLX>
+__device__ void finalize_sector(const SvdTask& t, const typename Sc<CPLX>::T* __restrict__ B,
+                                const typename Sc<CPLX>::T* __restrict__ Q, int ldb, int ldq, int status,
+                                double rank_tol, int gw, int lane, int crank) {
+  using S = Sc<CPLX>;
+  using T = typename S::T;
+  constexpr int NW = kCluster * kWarps;
+  const int m = t.m, n = t.n;
+  T* __restrict__ U = static_cast<T*>(t.u);
+  T* __restrict__ VH = static_cast<T*>(t.vh);
+  for (int i = gw; i < m; i += NW) {
+    double x2 = 0.0;
+    for (int j = lane; j < n; j += 32) x2 += S::abs2(ldcg(B + (int64_t)i * ldb + j));
+    x2 = warp_sum(x2);
+    if (lane == 0) __stcg(t.norm + i, sqrt(x2));
+  }
+  cluster_sync_all();
+  double smax = 0.0;
+  for (int k = lane; k < m; k += 32) smax = fmax(smax, __ldcg(t.norm + k));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+  // rows whose sigma is below rank_tol * sigma_max (they rank last): their Vh rows are
+  // completed below instead of normalised
+  int nd = 0;
+  for (int k = lane; k < m; k += 32) nd += __ldcg(t.norm + k) <= rank_tol * smax ? 1 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nd += __shfl_xor_sync(0xffffffffu, nd, o);
+  for (int i = gw; i < m; i += NW) {
+    const double si = __ldcg(t.norm + i);
+    int rank = 0;
+    for (int k = lane; k < m; k += 32) {
+      const double sk = __ldcg(t.norm + k);
+      rank += (sk > si || (sk == si && k < i)) ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    if (lane == 0) t.s[rank] = si;
+    if (rank < m - nd) {
+      const double inv = 1.0 / si;
+      for (int j = lane; j < n; j += 32) stcg(VH + (int64_t)rank * n + j, S::scale(inv, ldcg(B + (int64_t)i * ldb + j)));
+    }
+    for (int j = lane; j < m; j += 32) U[(int64_t)j * m + rank] = S::conj(ldcg(Q + (int64_t)i * ldq + j));
+  }
+  cluster_sync_all();
+  if (nd > 0) complete_rows<CPLX>(VH, m - nd, m, n, t.coef, gw, lane);
+  if (crank == 0 && threadIdx.x == 0) *t.status = status;
 }
 
 template <bool CPLX>
@@ -427,59 +489,405 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32)
     status = 1;
   }
   cluster_sync_all();
-  // ---- finalize: sigma_i = |b_i| -> rank (descending, ties by row) -> U = Q^H, S, Vh = B / S
-  T* __restrict__ U = static_cast<T*>(t.u);
-  T* __restrict__ VH = static_cast<T*>(t.vh);
-  for (int i = gw; i < m; i += NW) {
-    double x2 = 0.0;
-    for (int j = lane; j < n; j += 32) x2 += S::abs2(ldcg(B + (int64_t)i * ldb + j));
-    x2 = warp_sum(x2);
-    if (lane == 0) __stcg(t.norm + i, sqrt(x2));
+  finalize_sector<CPLX>(t, B, Q, ldb, ldq, status, rank_tol, gw, lane, crank);
+}
+
+// ===================================================================== block Jacobi
+// Blocked one-sided Jacobi (the round-robin tournament over BLOCKS of rows): the rows are
+// split into nb blocks of bsz rows; in every round the 16 CTAs of the sector's cluster
+// each take one pair of blocks (I, J), stage its h <= 2 bsz rows W in shared memory, form
+// their Gram matrix G = W W^H with DMMA, run one cyclic Jacobi sweep on G (the same
+// Hestenes rotation of rows p, q -- applied as G <- J G J^H and accumulated as V <- J V),
+// and rewrite the rows as V W (B) and V Q_R (the matching rows of Q) with DMMA. One
+// cluster barrier per round instead of one per row-pair round: a sweep of an m x n sector
+// moves every row through L2 (m / bsz) times instead of m times, and the rotations'
+// arithmetic (6 m^2 n FMA per sweep) runs on the tensor pipe. Convergence as for the
+// row kernel: a sweep in which no pair (whichever block pair it met in) needed rotating.
+constexpr int kBlkSmemMax = 220 * 1024;
+
+__host__ __device__ __forceinline__ int blk_hp(int bsz) { return ((2 * bsz + 7) / 8) * 8; }
+// shared-memory row stride of the staged rows (elements): >= n, 4 mod 16 doubles (two
+// doubles per complex element) so the DMMA fragment loads of 4 rows hit distinct banks
+__host__ __device__ __forceinline__ int blk_ldw(int n, bool cplx) {
+  const int e = cplx ? 2 : 1;
+  int w = ((n * e + 15) / 16) * 16 + 4;
+  return w / e;
+}
+__host__ __device__ __forceinline__ size_t blk_smem(int bsz, int n, bool cplx) {
+  const int hp = blk_hp(bsz), es = cplx ? 16 : 8;
+  return (size_t)hp * blk_ldw(n, cplx) * es + 2 * (size_t)hp * (hp + 1) * es + (size_t)(hp / 2) * 4 * 8 +
+         (size_t)hp * 8;  // W, G, V, rotations, row indices, pairs
+}
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <bool CPLX>
+struct Frag;
+template <>
+struct Frag<false> {
+  // C (8 x 8) += A (8 x 4) B (4 x 8)
+  __device__ static void mma(double (&c)[2][2], double a, double b) { dmma884(c[0][0], c[0][1], a, b); }
+  // C += A B^H (B given as its 8 x 4 rows: b = B^T fragment)
+  __device__ static void mma_h(double (&c)[2][2], double a, double b) { dmma884(c[0][0], c[0][1], a, b); }
+  __device__ static double re(double x) { return x; }
+};
+template <>
+struct Frag<true> {
+  // complex A B: re = Ar Br - Ai Bi, im = Ar Bi + Ai Br (c[0] = re pair, c[1] = im pair)
+  __device__ static void mma(double (&c)[2][2], double2 a, double2 b) {
+    dmma884(c[0][0], c[0][1], a.x, b.x);
+    dmma884(c[0][0], c[0][1], -a.y, b.y);
+    dmma884(c[1][0], c[1][1], a.x, b.y);
+    dmma884(c[1][0], c[1][1], a.y, b.x);
+  }
+  // A conj(B): re = Ar Br + Ai Bi, im = Ai Br - Ar Bi
+  __device__ static void mma_h(double (&c)[2][2], double2 a, double2 b) {
+    dmma884(c[0][0], c[0][1], a.x, b.x);
+    dmma884(c[0][0], c[0][1], a.y, b.y);
+    dmma884(c[1][0], c[1][1], a.y, b.x);
+    dmma884(c[1][0], c[1][1], -a.x, b.y);
+  }
+};
+
+template <bool CPLX>
+__device__ __forceinline__ typename Sc<CPLX>::T frag_out(const double (&c)[2][2], int e) {
+  if constexpr (CPLX) return make_double2(c[0][e], c[1][e]);
+  else return c[0][e];
+}
+
+// Out (h x ncols, rows R in global, row stride ld) = V (hp x hp) X (hp x ncols, smem stride ldw).
+// A warp computes an 8 x 16 output tile (one V fragment feeds two DMMAs); K runs over the
+// first round4(h) rows only (rows h.. of X are zero).
+template <bool CPLX>
+__device__ void blk_apply(const typename Sc<CPLX>::T* __restrict__ V, int ldv, const typename Sc<CPLX>::T* __restrict__ X,
+                          int ldw, int h, int hp, int ncols, typename Sc<CPLX>::T* __restrict__ out, int ld,
+                          const int* rows, int warp, int lane) {
+  using T = typename Sc<CPLX>::T;
+  const int tiles_i = (h + 7) / 8, tiles_j = (ncols + 15) / 16, kend = (h + 3) & ~3;
+  const int r = lane >> 2, q = lane & 3;
+  for (int tt = warp; tt < tiles_i * tiles_j; tt += kWarps) {
+    const int ti = tt % tiles_i, tj = tt / tiles_i;
+    const int i0 = ti * 8, j0 = tj * 16;
+    double c0[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, c1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    const bool two = j0 + 8 < ncols;
+    for (int k0 = 0; k0 < kend; k0 += 4) {
+      const T a = V[(i0 + r) * ldv + k0 + q];
+      const T* xb = X + (k0 + q) * ldw + j0 + r;
+      Frag<CPLX>::mma(c0, a, xb[0]);
+      if (two) Frag<CPLX>::mma(c1, a, xb[8]);
+    }
+    const int i = i0 + r;
+    if (i < h) {
+      T* dst = out + (int64_t)rows[i] * ld;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = j0 + 2 * q + e;
+        if (j < ncols) stcg(dst + j, frag_out<CPLX>(c0, e));
+        if (j + 8 < ncols) stcg(dst + j + 8, frag_out<CPLX>(c1, e));
+      }
+    }
+  }
+}
+
+// W[i][0, ncols) = src row rows[i] (i < h) by 16-byte cp.async (rows are 16-byte aligned:
+// float64 workspace rows have even length), zero elsewhere in [0, hp) x [0, ldw); the
+// copies are all in flight at once (a load -> store loop would wait out each L2 round trip)
+template <bool CPLX>
+__device__ void blk_stage(typename Sc<CPLX>::T* __restrict__ W, int ldw, const typename Sc<CPLX>::T* __restrict__ src,
+                          int ld, const int* rows, int h, int hp, int ncols, int tid) {
+  using T = typename Sc<CPLX>::T;
+  constexpr int EPC = CPLX ? 1 : 2;  // elements per 16-byte chunk
+  const int cpr = ncols / EPC;        // chunks per row (ncols is even for float64)
+  for (int x = tid; x < h * cpr; x += blockDim.x) {
+    const int i = x / cpr, c = x - i * cpr;
+    const T* g = src + (int64_t)rows[i] * ld + c * EPC;
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(W + i * ldw + c * EPC);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(g));
+  }
+  const int tail = ldw - ncols;
+  for (int x = tid; x < h * tail; x += blockDim.x) {
+    const int i = x / tail;
+    W[i * ldw + ncols + (x - i * tail)] = Sc<CPLX>::zero();
+  }
+  for (int x = h * ldw + tid; x < hp * ldw; x += blockDim.x) W[x] = Sc<CPLX>::zero();
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+template <bool CPLX>
+__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32, 1)
+    jacobi_block_kernel(const SvdTask* __restrict__ tasks, int max_sweeps, double tol, double rank_tol) {
+  using S = Sc<CPLX>;
+  using T = typename S::T;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_rot;
+  const SvdTask t = tasks[blockIdx.x / kCluster];
+  const int crank = (int)cluster_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gw = crank * kWarps + warp;
+  constexpr int NW = kCluster * kWarps;
+  const int m = t.m, n = t.n, bsz = t.bsz, nb = t.nb;
+  T* __restrict__ B = static_cast<T*>(t.b);
+  T* __restrict__ Q = static_cast<T*>(t.q);
+  const T* __restrict__ Ain = static_cast<const T*>(t.a);
+  const int ldb = CPLX ? n : n + (n & 1), ldq = CPLX ? m : m + (m & 1);
+  const int hp = blk_hp(bsz), ldw = blk_ldw(n, CPLX), ldg = hp + 1;
+  T* W = reinterpret_cast<T*>(smem);
+  T* G = W + (size_t)hp * ldw;
+  T* V = G + (size_t)hp * ldg;
+  double* rot = reinterpret_cast<double*>(V + (size_t)hp * ldg);  // [hp / 2][4]: c, s, pr, pi
+  int* rows = reinterpret_cast<int*>(rot + (hp / 2) * 4);           // [hp]
+  int* prs = rows + hp;                                              // [hp]: this round's pairs
+  // Q = I, B = A
+  for (int64_t x = (int64_t)gw * 32 + lane; x < (int64_t)m * ldq; x += (int64_t)NW * 32) {
+    const int64_t i = x / ldq, j = x - i * ldq;
+    stcg(Q + x, (i == j) ? S::one() : S::zero());
+  }
+  for (int64_t x = (int64_t)gw * 32 + lane; x < (int64_t)m * ldb; x += (int64_t)NW * 32) {
+    const int64_t i = x / ldb, j = x - i * ldb;
+    stcg(B + x, j < n ? Ain[i * n + j] : S::zero());
   }
   cluster_sync_all();
-  double smax = 0.0;
-  for (int k = lane; k < m; k += 32) smax = fmax(smax, __ldcg(t.norm + k));
+  const double thresh = tol * sqrt((double)n) * 2.220446049250313e-16;
+  int sweep = 0, status = -1;
+  if (m > 1) {
+    for (sweep = 1; sweep <= max_sweeps; ++sweep) {
+      int* cnt = t.counter + (sweep & 1);
+      if (tid == 0) s_rot = 0;
+      for (int r = 0; r < nb - 1; ++r) {
+        for (int pi_ = crank; pi_ < nb / 2; pi_ += kCluster) {
+          int I, J;
+          rr_pair(nb, r, pi_, I, J);
+          const int i0 = I * bsz, i1 = min(m, i0 + bsz), j0 = J * bsz, j1 = min(m, j0 + bsz);
+          const int hI = max(0, i1 - i0), hJ = max(0, j1 - j0), h = hI + hJ;
+          if (h < 2) continue;  // (CTA-uniform)
+          __syncthreads();      // the previous pair's smem reads are done
+          for (int i = tid; i < hp; i += blockDim.x) rows[i] = i < hI ? i0 + i : (i < h ? j0 + i - hI : 0);
+          __syncthreads();
+#ifdef TNB_SVD_TRACE
+          long long tc[8];
+          tc[0] = clock64();
+#define TNB_SVD_STAMP(k) \
+  do {                   \
+    __syncthreads();     \
+    tc[k] = clock64();   \
+  } while (0)
+#else
+#define TNB_SVD_STAMP(k) \
+  do {                   \
+  } while (0)
+#endif
+          blk_stage<CPLX>(W, ldw, B, ldb, rows, h, hp, ldb, tid);  // W = B[rows]
+          // V = I
+          for (int x = tid; x < hp * ldg; x += blockDim.x) {
+            const int i = x / ldg, j = x - i * ldg;
+            V[x] = (i == j) ? S::one() : S::zero();
+          }
+          __syncthreads();
+          TNB_SVD_STAMP(1);
+          // G = W W^H: 8 x 8 tiles on and above the diagonal, mirrored
+          {
+            const int ti_n = (h + 7) / 8, ntile = ti_n * (ti_n + 1) / 2;  // (G rows / columns >= h stay unused)
+            const int rr = lane >> 2, qq = lane & 3;
+            for (int tt = warp; tt < ntile; tt += kWarps) {
+              int ti = 0, rem = tt;
+              while (rem >= ti_n - ti) {
+                rem -= ti_n - ti;
+                ++ti;
+              }
+              const int tj = ti + rem;
+              double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+              const T* wa = W + (ti * 8 + rr) * ldw + qq;
+              const T* wb = W + (tj * 8 + rr) * ldw + qq;
+              for (int k0 = 0; k0 < ldb; k0 += 4) Frag<CPLX>::mma_h(c, wa[k0], wb[k0]);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
-  // rows whose sigma is below rank_tol * sigma_max (they rank last): their Vh rows are
-  // completed below instead of normalised
-  int nd = 0;
-  for (int k = lane; k < m; k += 32) nd += __ldcg(t.norm + k) <= rank_tol * smax ? 1 : 0;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) nd += __shfl_xor_sync(0xffffffffu, nd, o);
-  for (int i = gw; i < m; i += NW) {
-    const double si = __ldcg(t.norm + i);
-    int rank = 0;
-    for (int k = lane; k < m; k += 32) {
-      const double sk = __ldcg(t.norm + k);
-      rank += (sk > si || (sk == si && k < i)) ? 1 : 0;
+              for (int e = 0; e < 2; ++e) {
+                const int gi = ti * 8 + rr, gj = tj * 8 + 2 * qq + e;
+                const T v = frag_out<CPLX>(c, e);
+                G[gi * ldg + gj] = v;
+                if (ti != tj) G[gj * ldg + gi] = S::conj(v);  // (a diagonal tile holds both)
+              }
+            }
+          }
+          __syncthreads();
+          TNB_SVD_STAMP(2);
+          // one cyclic Jacobi sweep over the h rows, on G (two-sided) and V (rows). Per round:
+          // the npair rotations (one thread each), then ONE update phase in which a thread
+          // applies rotation k to rows {p, q} and rotation k' to columns {p', q'} of a 2 x 2
+          // block of G at once (G <- J G J^H), or rotation k to a column of rows {p, q} of V
+          const int hh = h + (h & 1), npair = hh / 2;
+          for (int ir = 0; ir < hh - 1; ++ir) {
+#ifdef TNB_SVD_TRACE
+            const long long t_ir = clock64();
+#endif
+            if (tid < 32) {  // (npair <= hp / 2 <= 32: warp 0 computes every rotation)
+              // round-robin pair `tid` of round ir (rr_pair without the integer divisions)
+              int p = 0, q = 0;
+              if (tid < npair) {
+                const int M = hh - 1;
+                if (tid == 0) {
+                  p = ir;
+                  q = M;
+                } else {
+                  p = ir + tid;
+                  if (p >= M) p -= M;
+                  q = ir - tid;
+                  if (q < 0) q += M;
+                }
+              }
+              if (p > q) {
+                const int x = p;
+                p = q;
+                q = x;
+              }
+              double c = 1.0, sn = 0.0, pr = 1.0, pim = 0.0;
+              bool did = false;
+              if (tid < npair && q < h) {
+                // <b_p, b_q> = sum conj(b_p) b_q = G[q][p]
+                const T g = G[q * ldg + p];
+                double gre, gim, al, be;
+                if constexpr (CPLX) {
+                  gre = g.x;
+                  gim = g.y;
+                  al = G[p * ldg + p].x;
+                  be = G[q * ldg + q].x;
+                } else {
+                  gre = g;
+                  gim = 0.0;
+                  al = G[p * ldg + p];
+                  be = G[q * ldg + q];
+                }
+                did = rotation(al, be, gre, gim, thresh, c, sn, pr, pim);
+                if (!did) {
+                  c = 1.0;
+                  sn = 0.0;
+                  pr = 1.0;
+                  pim = 0.0;
+                }
+              }
+#ifdef TNB_SVD_TRACE
+              if (tid == 0 && crank == 1 && blockIdx.x < kCluster && r == 3 && sweep == 2 && ir < 3)
+                printf("  inner ir %d: rotation phase %lld cycles\n", ir, clock64() - t_ir);
+#endif
+              const unsigned nrot_w = __popc(__ballot_sync(0xffffffffu, did));  // (no same-address atomics)
+              if (tid == 0) s_rot += (int)nrot_w;
+              if (tid < npair) {
+                rot[4 * tid] = c;
+                rot[4 * tid + 1] = sn;
+                rot[4 * tid + 2] = pr;
+                rot[4 * tid + 3] = pim;
+                prs[2 * tid] = p;
+                prs[2 * tid + 1] = q;
+              }
+            }
+            __syncthreads();
+#ifdef TNB_SVD_TRACE
+            const long long t_mid = clock64();
+#endif
+            // warp w takes row pairs k = w, w + 16: lane l updates the G block (rows of pair k) x
+            // (columns of pair l) and columns l, l + 32 of V's rows p, q
+            for (int k = warp; k < npair; k += kWarps) {
+              const double s1 = rot[4 * k + 1];
+              const int p = prs[2 * k], q = prs[2 * k + 1];
+              const double c1 = rot[4 * k], pr1 = rot[4 * k + 2], pi1 = rot[4 * k + 3];
+              if (lane < npair) {
+                const int k2 = lane;
+                const double s2 = rot[4 * k2 + 1];
+                if (s1 != 0.0 || s2 != 0.0) {
+                  const int p2 = prs[2 * k2], q2 = prs[2 * k2 + 1];
+                  T a00 = G[p * ldg + p2], a01 = G[p * ldg + q2], a10 = G[q * ldg + p2], a11 = G[q * ldg + q2];
+                  if (s1 != 0.0) {  // rows: x_p' = c x_p - s ph x_q, x_q' = s x_p + c ph x_q
+                    const T y0 = S::mulph(pr1, pi1, a10), y1 = S::mulph(pr1, pi1, a11);
+                    const T n00 = S::lin(c1, a00, -s1, y0), n01 = S::lin(c1, a01, -s1, y1);
+                    a10 = S::lin(s1, a00, c1, y0);
+                    a11 = S::lin(s1, a01, c1, y1);
+                    a00 = n00;
+                    a01 = n01;
+                  }
+                  if (s2 != 0.0) {  // columns: g_p' = c g_p - s conj(ph) g_q, g_q' = s g_p + c conj(ph) g_q
+                    const double c = rot[4 * k2], pr = rot[4 * k2 + 2], pim = rot[4 * k2 + 3];
+                    const T y0 = S::mulph(pr, -pim, a01), y1 = S::mulph(pr, -pim, a11);
+                    const T n00 = S::lin(c, a00, -s2, y0), n10 = S::lin(c, a10, -s2, y1);
+                    a01 = S::lin(s2, a00, c, y0);
+                    a11 = S::lin(s2, a10, c, y1);
+                    a00 = n00;
+                    a10 = n10;
+                  }
+                  G[p * ldg + p2] = a00;
+                  G[p * ldg + q2] = a01;
+                  G[q * ldg + p2] = a10;
+                  G[q * ldg + q2] = a11;
+                }
+              }
+              if (s1 != 0.0) {
+                for (int col = lane; col < hp; col += 32) {
+                  T* vp = V + p * ldg + col;
+                  T* vq = V + q * ldg + col;
+                  const T yp = *vp, yq = S::mulph(pr1, pi1, *vq);
+                  *vp = S::lin(c1, yp, -s1, yq);
+                  *vq = S::lin(s1, yp, c1, yq);
+                }
+              }
+            }
+            __syncthreads();
+#ifdef TNB_SVD_TRACE
+            if (tid == 0 && crank == 1 && blockIdx.x < kCluster && r == 3 && sweep == 2 && ir < 3)
+              printf("  inner ir %d h %d: to mid %lld, update %lld cycles\n", ir, h, t_mid - t_ir, clock64() - t_mid);
+#endif
+          }
+          TNB_SVD_STAMP(3);
+          // B[rows] = V W ; then Q[rows] = V Q[rows]
+          blk_apply<CPLX>(V, ldg, W, ldw, h, hp, ldb, B, ldb, rows, warp, lane);
+          __syncthreads();
+          TNB_SVD_STAMP(4);
+          blk_stage<CPLX>(W, ldw, Q, ldq, rows, h, hp, ldq, tid);  // W = Q[rows]
+          __syncthreads();
+          TNB_SVD_STAMP(5);
+          blk_apply<CPLX>(V, ldg, W, ldw, h, hp, ldq, Q, ldq, rows, warp, lane);
+#ifdef TNB_SVD_TRACE
+          TNB_SVD_STAMP(6);
+          if (tid == 0 && crank == 0 && blockIdx.x < kCluster && (r == 0 || r == 7) && sweep <= 2)
+            printf("svd blk sweep %d round %d h %d: stageB %lld gram %lld inner %lld applyB %lld stageQ %lld applyQ %lld\n",
+                   sweep, r, h, tc[1] - tc[0], tc[2] - tc[1], tc[3] - tc[2], tc[4] - tc[3], tc[5] - tc[4], tc[6] - tc[5]);
+#endif
+        }
+        cluster_sync_all();
+      }
+      __syncthreads();
+      if (tid == 0 && s_rot) atomicAdd(cnt, s_rot);
+      cluster_sync_all();
+      const int rot_all = __ldcg(cnt);
+      cluster_sync_all();  // everyone has read the counter before it is reset
+      if (crank == 0 && tid == 0) *cnt = 0;
+      if (rot_all == 0) {
+        status = sweep;
+        break;
+      }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
-    if (lane == 0) t.s[rank] = si;
-    if (rank < m - nd) {
-      const double inv = 1.0 / si;
-      for (int j = lane; j < n; j += 32) stcg(VH + (int64_t)rank * n + j, S::scale(inv, ldcg(B + (int64_t)i * ldb + j)));
-    }
-    for (int j = lane; j < m; j += 32) U[(int64_t)j * m + rank] = S::conj(ldcg(Q + (int64_t)i * ldq + j));
+  } else {
+    status = 1;
   }
   cluster_sync_all();
-  if (nd > 0) complete_rows<CPLX>(VH, m - nd, m, n, t.coef, gw, lane);
-  if (crank == 0 && threadIdx.x == 0) *t.status = status;
+  finalize_sector<CPLX>(t, B, Q, ldb, ldq, status, rank_tol, gw, lane, crank);
 }
 
 template <bool CPLX>
 int launch_jacobi(const void* tasks, int nsec, int max_sweeps, double tol, double rank_tol, double work,
-                  cudaStream_t st) {
-  auto kern = jacobi_rows_kernel<CPLX>;
-  static bool configured = false;
-  if (!configured) {
+                  size_t block_smem, cudaStream_t st) {
+  auto kern = block_smem ? jacobi_block_kernel<CPLX> : jacobi_rows_kernel<CPLX>;
+  static bool configured[2] = {false, false};
+  if (!configured[block_smem ? 1 : 0]) {
     TNB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured = true;
+    if (block_smem) TNB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kBlkSmemMax));
+    configured[block_smem ? 1 : 0] = true;
   }
   {
     KTimer kt(TNB_KF_OTHER, st, work);
-    kern<<<nsec * kCluster, kWarps * 32, 0, st>>>(static_cast<const SvdTask*>(tasks), max_sweeps, tol, rank_tol);
+    kern<<<nsec * kCluster, kWarps * 32, block_smem, st>>>(static_cast<const SvdTask*>(tasks), max_sweeps, tol,
+                                                           rank_tol);
   }
   count_launch();
   TNB_CUDA_CHECK(cudaGetLastError());
@@ -506,10 +914,31 @@ extern "C" int tnb_svd_jacobi_batched(int dtype, int nsec, const TnbSvdSector* s
     if (x.m < 1 || x.n < x.m || !x.a || !x.b || !x.q || !x.u || !x.s || !x.vh || !x.status)
       return fail(TNB_EINVAL, "svd_jacobi: sector needs 1 <= m <= n and all buffers");
     h[i] = {x.a, x.b, x.q, x.u, static_cast<double*>(x.s), x.vh, x.status, nullptr, nullptr, nullptr, (int)x.m,
-            (int)x.n};
+            (int)x.n, 1, 2};
     msum += x.m;
     work += 2.0 * x.m * (double)x.m * x.n;
   }
+  // block kernel: ~one block pair per CTA and round (nb = 2 x cluster blocks, or one row per
+  // block below that), more blocks where 2 bsz staged rows would not fit in shared memory;
+  // a sector whose single-row blocks still do not fit takes the whole batch to the row kernel
+  const bool cplx = dtype == TNB_C128;
+  static const bool rows_only = getenv("TNB_SVD_ROWS") != nullptr;  // dev A/B switch
+  size_t block_smem = 0;
+  bool block_ok = !rows_only;
+  for (int i = 0; i < nsec && block_ok; ++i) {
+    const int m = h[i].m, n = h[i].n;
+    int nb = std::min(2 * kCluster, m + (m & 1));
+    int bsz = (m + nb - 1) / nb;
+    while ((blk_smem(bsz, n, cplx) > kBlkSmemMax || blk_hp(bsz) > 64) && bsz > 1) {  // (warp 0: <= 32 pairs)
+      nb += 2 * kCluster;
+      bsz = (m + nb - 1) / nb;
+    }
+    if (blk_smem(bsz, n, cplx) > kBlkSmemMax) block_ok = false;
+    h[i].bsz = bsz;
+    h[i].nb = std::max(2, nb);
+    block_smem = std::max(block_smem, blk_smem(bsz, n, cplx));
+  }
+  if (!block_ok) block_smem = 0;
   // device task table + rotation counters + norm scratch in one allocation
   const size_t tb = sizeof(SvdTask) * (size_t)nsec, cb = sizeof(int) * 2 * (size_t)nsec;
   const size_t nb = sizeof(double) * (size_t)(3 * msum + 2 * nsec);  // norms [m] + coefficients [2m + 2]
@@ -529,8 +958,8 @@ extern "C" int tnb_svd_jacobi_batched(int dtype, int nsec, const TnbSvdSector* s
     cudaFreeAsync(mem, st);
     return cuda_fail(e, "svd_jacobi: task upload");
   }
-  rc = dtype == TNB_F64 ? launch_jacobi<false>(mem, nsec, max_sweeps, tol, rank_tol, work, st)
-                        : launch_jacobi<true>(mem, nsec, max_sweeps, tol, rank_tol, work, st);
+  rc = dtype == TNB_F64 ? launch_jacobi<false>(mem, nsec, max_sweeps, tol, rank_tol, work, block_smem, st)
+                        : launch_jacobi<true>(mem, nsec, max_sweeps, tol, rank_tol, work, block_smem, st);
   cudaFreeAsync(mem, st);
   return rc;
 }

@@ -1,43 +1,46 @@
-"""Dev aid: block-sparse truncated SVD of a C4-scale two-site wavefunction (GPU vs oracle CPU)."""
+"""Block SVD of the f3 workload (C4-bond two-site wavefunction): kernel time, sector shapes and
+sweeps used (dev aid)."""
 import os
 import sys
-import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "oracle"))
+sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
 import numpy as np
 import torch
 
+import bench
 import paper_2401_01921_b200 as tnb
-from paper_2401_01921_b200 import linalg, workloads as WL
+from paper_2401_01921_b200 import linalg
 
 torch.cuda.set_device(0)
-u1 = tnb.Symmetry.u1()
-V = tnb.Bond(btype=tnb.IN, sectors=WL.c4_sectors(), syms=[u1])
-P = tnb.Bond(btype=tnb.IN, sectors=[(1, 1), (-1, 1)], syms=[u1])
-psi = tnb.UniTensor([V, P, P, V.redirect()], labels=["vl", "p1", "p2", "vr"], name="psi", rowrank=2)
-tnb.random.normal_(psi, seed=5)
-print("blocks", psi.nblocks, "elements", sum(b.size for b in psi.get_blocks_()))
-for driver in (None,):
-    for _ in range(2):
-        linalg.svd_truncate(psi, keepdim=1024)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(3):
-        linalg.svd_truncate(psi, keepdim=1024)
-    torch.cuda.synchronize()
-    print("gpu svd_truncate ms", (time.perf_counter() - t0) / 3 * 1e3)
-mz = linalg._Matricized(psi)
-print("sectors", [(s.m, s.n) for s in mz.sectors])
+psi = bench.c4_two_site(tnb)
+orig = tnb._lib.svd_jacobi_batched
+seen = {}
+
+
+def spy(jobs, stream, dtype):
+    seen["jobs"] = jobs.copy()
+    return orig(jobs, stream, dtype=dtype)
+
+
+tnb._lib.svd_jacobi_batched = spy
+linalg.svd_truncate(psi, keepdim=1024)
 torch.cuda.synchronize()
-for m, n, members, off, view in mz.groups:
-    t0 = time.perf_counter()
-    torch.linalg.svd(view, full_matrices=False)
-    torch.cuda.synchronize()
-    print("group", m, n, len(members), "ms %.2f" % ((time.perf_counter() - t0) * 1e3))
-mats = [view[k].cpu().numpy() for m, n, members, off, view in mz.groups for k in range(len(members))]
-import tnkit_np as oracle
-t0 = time.perf_counter()
-oracle.svd_truncate_values(mats, 1024)
-print("cpu oracle ms", (time.perf_counter() - t0) * 1e3)
+tnb._lib.svd_jacobi_batched = orig
+jobs = seen["jobs"]
+shapes = sorted(((int(j["m"]), int(j["n"])) for j in jobs), reverse=True)
+print("sectors", len(shapes), "largest", shapes[:6])
+for _ in range(2):
+    linalg.svd_truncate(psi, keepdim=1024)
+torch.cuda.synchronize()
+tnb._lib.ktimer_reset()
+tnb._lib.ktimer_enable(True)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(5):
+    linalg.svd_truncate(psi, keepdim=1024)
+e1.record()
+torch.cuda.synchronize()
+tnb._lib.ktimer_enable(False)
+k, ms, _ = tnb._lib.ktimer_read(tnb._lib.KF_OTHER)
+print(f"svd_truncate {e0.elapsed_time(e1) / 5:.2f} ms/call; jacobi kernel {ms / max(k, 1):.2f} ms/launch ({k} launches)")
