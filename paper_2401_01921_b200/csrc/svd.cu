@@ -12,11 +12,16 @@
 // rounds per sweep) and sweeps repeat until a whole sweep performs no rotation
 // (|b_p . b_q| <= tol |b_p| |b_q| for every pair) or max_sweeps is hit.
 //
-// One thread-block CLUSTER (16 CTAs x 16 warps) owns one sector: a warp rotates one
-// row pair per task, the cluster barrier (barrier.cluster arrive.release /
-// wait.acquire) separates rounds, and B / Q live in global memory read with .cg loads
-// (L2; the 126 MB L2 holds every sector of a C4-sized two-site tensor). All sectors
-// run concurrently, one cluster each. The finalize pass (same kernel) ranks the
+// One thread-block CLUSTER (16 CTAs) owns one sector and B / Q live in global memory read
+// with .cg loads (L2; the 126 MB L2 holds every sector of a C4-sized two-site tensor). All
+// sectors run concurrently, one cluster each. Two schedules of the same rotations:
+//  * jacobi_block_kernel (default): rows in blocks, a tournament over block pairs, each CTA
+//    staging its pair's rows in shared memory and doing their Gram matrix, one inner
+//    Jacobi sweep and the row / Q updates on chip (DMMA for the products) -- one cluster
+//    barrier per block round (see the section comment below);
+//  * jacobi_rows_kernel (sectors whose staged rows cannot fit in shared memory, i.e. rows
+//    longer than ~13k float64 elements): a warp rotates one row pair per task and the
+//    cluster barrier (barrier.cluster arrive.release / wait.acquire) separates rounds. The finalize pass (same kernel) ranks the
 // singular values (descending, ties by row) and writes the torch-compatible thin
 // factors U (m x m), S (m), Vh (m x n). Rows with sigma below rank_tol * sigma_max
 // (rank-deficient sectors: product states, degenerate wavefunctions) cannot be normalised
@@ -171,10 +176,9 @@ __device__ __forceinline__ double rnd_unit(uint64_t key) {
 // cluster cooperate on every step (rows are sequentially dependent).
 template <bool CPLX>
 __device__ void complete_rows(typename Sc<CPLX>::T* __restrict__ VH, int r0, int m, int n, double* coef, int gw,
-                              int lane) {
+                              int lane, int NW) {
   using S = Sc<CPLX>;
   using T = typename S::T;
-  constexpr int NW = kCluster * kWarps;
   const int gt = gw * 32 + lane;
   for (int r = r0; r < m; ++r) {
     T* v = VH + (int64_t)r * n;
@@ -247,10 +251,9 @@ __device__ void complete_rows(typename Sc<CPLX>::T* __restrict__ VH, int r0, int
 template <bool CPLX>
 __device__ void finalize_sector(const SvdTask& t, const typename Sc<CPLX>::T* __restrict__ B,
                                 const typename Sc<CPLX>::T* __restrict__ Q, int ldb, int ldq, int status,
-                                double rank_tol, int gw, int lane, int crank) {
+                                double rank_tol, int gw, int lane, int crank, int NW) {
   using S = Sc<CPLX>;
   using T = typename S::T;
-  constexpr int NW = kCluster * kWarps;
   const int m = t.m, n = t.n;
   T* __restrict__ U = static_cast<T*>(t.u);
   T* __restrict__ VH = static_cast<T*>(t.vh);
@@ -288,7 +291,7 @@ __device__ void finalize_sector(const SvdTask& t, const typename Sc<CPLX>::T* __
     for (int j = lane; j < m; j += 32) U[(int64_t)j * m + rank] = S::conj(ldcg(Q + (int64_t)i * ldq + j));
   }
   cluster_sync_all();
-  if (nd > 0) complete_rows<CPLX>(VH, m - nd, m, n, t.coef, gw, lane);
+  if (nd > 0) complete_rows<CPLX>(VH, m - nd, m, n, t.coef, gw, lane, NW);
   if (crank == 0 && threadIdx.x == 0) *t.status = status;
 }
 
@@ -489,7 +492,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32)
     status = 1;
   }
   cluster_sync_all();
-  finalize_sector<CPLX>(t, B, Q, ldb, ldq, status, rank_tol, gw, lane, crank);
+  finalize_sector<CPLX>(t, B, Q, ldb, ldq, status, rank_tol, gw, lane, crank, NW);
 }
 
 // ===================================================================== block Jacobi
@@ -504,6 +507,9 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32)
 // arithmetic (6 m^2 n FMA per sweep) runs on the tensor pipe. Convergence as for the
 // row kernel: a sweep in which no pair (whichever block pair it met in) needed rotating.
 constexpr int kBlkSmemMax = 220 * 1024;
+// 17 warps: a block pair of h <= 34 rows has <= 17 row pairs per inner round, one warp each
+// (with 16, warp 0 took two and set every round's latency)
+constexpr int kBlkWarps = 17;
 
 __host__ __device__ __forceinline__ int blk_hp(int bsz) { return ((2 * bsz + 7) / 8) * 8; }
 // shared-memory row stride of the staged rows (elements): >= n, 4 mod 16 doubles (two
@@ -569,7 +575,7 @@ __device__ void blk_apply(const typename Sc<CPLX>::T* __restrict__ V, int ldv, c
   using T = typename Sc<CPLX>::T;
   const int tiles_i = (h + 7) / 8, tiles_j = (ncols + 15) / 16, kend = (h + 3) & ~3;
   const int r = lane >> 2, q = lane & 3;
-  for (int tt = warp; tt < tiles_i * tiles_j; tt += kWarps) {
+  for (int tt = warp; tt < tiles_i * tiles_j; tt += kBlkWarps) {
     const int ti = tt % tiles_i, tj = tt / tiles_i;
     const int i0 = ti * 8, j0 = tj * 16;
     double c0[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, c1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
@@ -618,7 +624,7 @@ __device__ void blk_stage(typename Sc<CPLX>::T* __restrict__ W, int ldw, const t
 }
 
 template <bool CPLX>
-__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32, 1)
+__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kBlkWarps * 32, 1)
     jacobi_block_kernel(const SvdTask* __restrict__ tasks, int max_sweeps, double tol, double rank_tol) {
   using S = Sc<CPLX>;
   using T = typename S::T;
@@ -627,8 +633,8 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32, 
   const SvdTask t = tasks[blockIdx.x / kCluster];
   const int crank = (int)cluster_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gw = crank * kWarps + warp;
-  constexpr int NW = kCluster * kWarps;
+  const int gw = crank * kBlkWarps + warp;
+  constexpr int NW = kCluster * kBlkWarps;
   const int m = t.m, n = t.n, bsz = t.bsz, nb = t.nb;
   T* __restrict__ B = static_cast<T*>(t.b);
   T* __restrict__ Q = static_cast<T*>(t.q);
@@ -667,19 +673,6 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32, 
           __syncthreads();      // the previous pair's smem reads are done
           for (int i = tid; i < hp; i += blockDim.x) rows[i] = i < hI ? i0 + i : (i < h ? j0 + i - hI : 0);
           __syncthreads();
-#ifdef TNB_SVD_TRACE
-          long long tc[8];
-          tc[0] = clock64();
-#define TNB_SVD_STAMP(k) \
-  do {                   \
-    __syncthreads();     \
-    tc[k] = clock64();   \
-  } while (0)
-#else
-#define TNB_SVD_STAMP(k) \
-  do {                   \
-  } while (0)
-#endif
           blk_stage<CPLX>(W, ldw, B, ldb, rows, h, hp, ldb, tid);  // W = B[rows]
           // V = I
           for (int x = tid; x < hp * ldg; x += blockDim.x) {
@@ -687,12 +680,11 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32, 
             V[x] = (i == j) ? S::one() : S::zero();
           }
           __syncthreads();
-          TNB_SVD_STAMP(1);
           // G = W W^H: 8 x 8 tiles on and above the diagonal, mirrored
           {
             const int ti_n = (h + 7) / 8, ntile = ti_n * (ti_n + 1) / 2;  // (G rows / columns >= h stay unused)
             const int rr = lane >> 2, qq = lane & 3;
-            for (int tt = warp; tt < ntile; tt += kWarps) {
+            for (int tt = warp; tt < ntile; tt += kBlkWarps) {
               int ti = 0, rem = tt;
               while (rem >= ti_n - ti) {
                 rem -= ti_n - ti;
@@ -713,16 +705,12 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32, 
             }
           }
           __syncthreads();
-          TNB_SVD_STAMP(2);
           // one cyclic Jacobi sweep over the h rows, on G (two-sided) and V (rows). Per round:
           // the npair rotations (one thread each), then ONE update phase in which a thread
           // applies rotation k to rows {p, q} and rotation k' to columns {p', q'} of a 2 x 2
           // block of G at once (G <- J G J^H), or rotation k to a column of rows {p, q} of V
           const int hh = h + (h & 1), npair = hh / 2;
           for (int ir = 0; ir < hh - 1; ++ir) {
-#ifdef TNB_SVD_TRACE
-            const long long t_ir = clock64();
-#endif
             if (tid < 32) {  // (npair <= hp / 2 <= 32: warp 0 computes every rotation)
               // round-robin pair `tid` of round ir (rr_pair without the integer divisions)
               int p = 0, q = 0;
@@ -768,10 +756,6 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32, 
                   pim = 0.0;
                 }
               }
-#ifdef TNB_SVD_TRACE
-              if (tid == 0 && crank == 1 && blockIdx.x < kCluster && r == 3 && sweep == 2 && ir < 3)
-                printf("  inner ir %d: rotation phase %lld cycles\n", ir, clock64() - t_ir);
-#endif
               const unsigned nrot_w = __popc(__ballot_sync(0xffffffffu, did));  // (no same-address atomics)
               if (tid == 0) s_rot += (int)nrot_w;
               if (tid < npair) {
@@ -784,12 +768,9 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32, 
               }
             }
             __syncthreads();
-#ifdef TNB_SVD_TRACE
-            const long long t_mid = clock64();
-#endif
             // warp w takes row pairs k = w, w + 16: lane l updates the G block (rows of pair k) x
             // (columns of pair l) and columns l, l + 32 of V's rows p, q
-            for (int k = warp; k < npair; k += kWarps) {
+            for (int k = warp; k < npair; k += kBlkWarps) {
               const double s1 = rot[4 * k + 1];
               const int p = prs[2 * k], q = prs[2 * k + 1];
               const double c1 = rot[4 * k], pr1 = rot[4 * k + 2], pi1 = rot[4 * k + 3];
@@ -833,26 +814,13 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32, 
               }
             }
             __syncthreads();
-#ifdef TNB_SVD_TRACE
-            if (tid == 0 && crank == 1 && blockIdx.x < kCluster && r == 3 && sweep == 2 && ir < 3)
-              printf("  inner ir %d h %d: to mid %lld, update %lld cycles\n", ir, h, t_mid - t_ir, clock64() - t_mid);
-#endif
           }
-          TNB_SVD_STAMP(3);
           // B[rows] = V W ; then Q[rows] = V Q[rows]
           blk_apply<CPLX>(V, ldg, W, ldw, h, hp, ldb, B, ldb, rows, warp, lane);
           __syncthreads();
-          TNB_SVD_STAMP(4);
           blk_stage<CPLX>(W, ldw, Q, ldq, rows, h, hp, ldq, tid);  // W = Q[rows]
           __syncthreads();
-          TNB_SVD_STAMP(5);
           blk_apply<CPLX>(V, ldg, W, ldw, h, hp, ldq, Q, ldq, rows, warp, lane);
-#ifdef TNB_SVD_TRACE
-          TNB_SVD_STAMP(6);
-          if (tid == 0 && crank == 0 && blockIdx.x < kCluster && (r == 0 || r == 7) && sweep <= 2)
-            printf("svd blk sweep %d round %d h %d: stageB %lld gram %lld inner %lld applyB %lld stageQ %lld applyQ %lld\n",
-                   sweep, r, h, tc[1] - tc[0], tc[2] - tc[1], tc[3] - tc[2], tc[4] - tc[3], tc[5] - tc[4], tc[6] - tc[5]);
-#endif
         }
         cluster_sync_all();
       }
@@ -871,7 +839,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kWarps * 32, 
     status = 1;
   }
   cluster_sync_all();
-  finalize_sector<CPLX>(t, B, Q, ldb, ldq, status, rank_tol, gw, lane, crank);
+  finalize_sector<CPLX>(t, B, Q, ldb, ldq, status, rank_tol, gw, lane, crank, NW);
 }
 
 template <bool CPLX>
@@ -886,7 +854,7 @@ int launch_jacobi(const void* tasks, int nsec, int max_sweeps, double tol, doubl
   }
   {
     KTimer kt(TNB_KF_OTHER, st, work);
-    kern<<<nsec * kCluster, kWarps * 32, block_smem, st>>>(static_cast<const SvdTask*>(tasks), max_sweeps, tol,
+    kern<<<nsec * kCluster, (block_smem ? kBlkWarps : kWarps) * 32, block_smem, st>>>(static_cast<const SvdTask*>(tasks), max_sweeps, tol,
                                                            rank_tol);
   }
   count_launch();

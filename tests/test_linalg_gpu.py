@@ -197,7 +197,11 @@ def test_jacobi_kernel_converges_without_fallback(cuda, dt):
     from paper_2401_01921_b200 import _lib, dense
     rng = np.random.default_rng(8)
     jobs, keep = [], []
-    for m, n in [(1, 1), (5, 9), (64, 64), (100, 130)]:
+    # (block kernel: one block pair per CTA and round up to m = 64, bsz > 1 beyond; the wide
+    # sectors need more blocks than 2 x 16 to fit their staged rows in shared memory, so each
+    # CTA takes several block pairs per round)
+    extra = [(300, 3000), (516, 520)] if dt == np.float64 else [(150, 1000), (200, 210)]
+    for m, n in [(1, 1), (5, 9), (64, 64), (100, 130)] + extra:
         a = rng.standard_normal((m, n))
         if dt == np.complex128:
             a = a + 1j * rng.standard_normal((m, n))
