@@ -669,7 +669,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kBlkWarps * 3
           rr_pair(nb, r, pi_, I, J);
           const int i0 = I * bsz, i1 = min(m, i0 + bsz), j0 = J * bsz, j1 = min(m, j0 + bsz);
           const int hI = max(0, i1 - i0), hJ = max(0, j1 - j0), h = hI + hJ;
-          if (h < 2) continue;  // (CTA-uniform)
+          if (h < 2 || (r > 0 && (hI == 0 || hJ == 0))) continue;  // nothing to rotate (CTA-uniform)
           __syncthreads();      // the previous pair's smem reads are done
           for (int i = tid; i < hp; i += blockDim.x) rows[i] = i < hI ? i0 + i : (i < h ? j0 + i - hI : 0);
           __syncthreads();
@@ -709,21 +709,56 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kBlkWarps * 3
           // the npair rotations (one thread each), then ONE update phase in which a thread
           // applies rotation k to rows {p, q} and rotation k' to columns {p', q'} of a 2 x 2
           // block of G at once (G <- J G J^H), or rotation k to a column of rows {p, q} of V
-          const int hh = h + (h & 1), npair = hh / 2;
-          for (int ir = 0; ir < hh - 1; ++ir) {
+          // The first block round of a sweep visits every pair of the h rows (a round-robin
+          // tournament, h - 1 rounds); later rounds only the cross pairs I x J (max(hI, hJ)
+          // rounds of min(hI, hJ) disjoint pairs): every pair of rows of the sector is still
+          // visited at least once per sweep -- within-block pairs in round 0, where every block
+          // plays -- so a sweep without rotations still means B did not change during it.
+          // (A row in no pair of an inner round still needs that round's column rotations in
+          // its row of G: the |hI - hJ| rows left over by the cross pairs of unequal blocks
+          // ride along in identity "pairs", two to a pair, the last with the spare row h.)
+          const bool cross = r > 0;
+          const int hh = h + (h & 1);
+          const int nreal = cross ? min(hI, hJ) : hh / 2;
+          const int npair = cross ? nreal + (abs(hI - hJ) + 1) / 2 : nreal;
+          const int nround = cross ? max(hI, hJ) : hh - 1;
+          for (int ir = 0; ir < nround; ++ir) {
             if (tid < 32) {  // (npair <= hp / 2 <= 32: warp 0 computes every rotation)
-              // round-robin pair `tid` of round ir (rr_pair without the integer divisions)
+              // pair `tid` of inner round ir (no integer divisions)
               int p = 0, q = 0;
+              bool idle = false;
               if (tid < npair) {
-                const int M = hh - 1;
-                if (tid == 0) {
-                  p = ir;
-                  q = M;
+                if (cross) {
+                  // the larger block (n rows, offset o) cycles against the smaller one: its
+                  // row (t + ir) mod n meets row t of the smaller block, t < nreal; rows
+                  // t >= nreal of the cycle are idle this round
+                  const bool iBig = hI > hJ;
+                  const int n = iBig ? hI : hJ, o = iBig ? 0 : hI, so = iBig ? hI : 0;
+                  auto big = [&](int t) {
+                    int x = t + ir;
+                    if (x >= n) x -= n;
+                    return o + x;
+                  };
+                  if (tid < nreal) {
+                    p = so + tid;
+                    q = big(tid);
+                  } else {
+                    idle = true;
+                    const int t = nreal + 2 * (tid - nreal);
+                    p = big(t);
+                    q = t + 1 < n ? big(t + 1) : h;  // (h: the spare row, h < hp when used)
+                  }
                 } else {
-                  p = ir + tid;
-                  if (p >= M) p -= M;
-                  q = ir - tid;
-                  if (q < 0) q += M;
+                  const int M = hh - 1;
+                  if (tid == 0) {
+                    p = ir;
+                    q = M;
+                  } else {
+                    p = ir + tid;
+                    if (p >= M) p -= M;
+                    q = ir - tid;
+                    if (q < 0) q += M;
+                  }
                 }
               }
               if (p > q) {
@@ -733,7 +768,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kBlkWarps * 3
               }
               double c = 1.0, sn = 0.0, pr = 1.0, pim = 0.0;
               bool did = false;
-              if (tid < npair && q < h) {
+              if (tid < npair && q < h && !idle) {
                 // <b_p, b_q> = sum conj(b_p) b_q = G[q][p]
                 const T g = G[q * ldg + p];
                 double gre, gim, al, be;
