@@ -1064,12 +1064,12 @@ def main():
             return d
 
         def w_c3():
-            r = gpu_lawr(tnb, 1024, np.complex128, max(3, args.steps // 2), args.warmup, flush, dist, e2e=True)
+            r = gpu_lawr(tnb, 1024, np.complex128, max(8, args.steps), args.warmup, flush, dist, e2e=True)
             par = parity_lawr(r["out"], 1024, np.complex128, 1234) if dist.rank == 0 else None
             old = tnb.get_complex_mode()
             try:
                 tnb.set_complex_mode("3M")
-                r3 = gpu_lawr(tnb, 1024, np.complex128, max(3, args.steps // 2), args.warmup, flush, dist, e2e=False)
+                r3 = gpu_lawr(tnb, 1024, np.complex128, max(8, args.steps), args.warmup, flush, dist, e2e=False)
                 par3 = parity_lawr(r3["out"], 1024, np.complex128, 1234) if dist.rank == 0 else None
             finally:
                 tnb.set_complex_mode(old)
