@@ -129,6 +129,16 @@ typedef struct {
 } TnbCopy2D;
 int tnb_copy2d_batched(const void* src, void* dst, int64_t nseg, const TnbCopy2D* segs, void* stream);
 
+/* ---- file payload -> HBM (the .utn loader, io.py:83-107's payload read) ----
+ * nbytes bytes of the open file fd from byte offset `offset` are read with pread() by up to
+ * nthreads threads (the caller's included) in `chunk`-byte pieces into the PINNED host
+ * buffer `pinned` (>= nbytes), and each piece is copied to dst (device) with
+ * cudaMemcpyAsync on `stream` as soon as it and every earlier piece have landed. Returns
+ * once every read is done and every copy is queued; the caller must keep `pinned`
+ * untouched until the copies complete (an event on `stream`). TNB_EINVAL on a short read. */
+int tnb_file_to_device(int fd, int64_t offset, int64_t nbytes, void* pinned, void* dst, int64_t chunk,
+                       int nthreads, void* stream);
+
 /* ---- one Lanczos orthogonalisation step (linalg.py:474-562 vector work) ----
  * q: r basis vectors as ROWS (row pitch ldq elements), w: the matvec result (n elements,
  * overwritten by w - sum_k <q_k, w> q_k), q_next: receives w / |w| (may be NULL);

@@ -23,7 +23,7 @@ EXPORTS = (
     "tnb_zero_flux_blocks", "tnb_bs_contract", "tnb_bs_contract_masked", "tnb_optimal_order",
     "tnb_ktimer_enable", "tnb_ktimer_reset", "tnb_ktimer_read",
     "tnb_bs_plan", "tnb_bs_execute", "tnb_bs_execute_batched", "tnb_bs_plan_pairs", "tnb_copy2d_batched", "tnb_svd_jacobi_batched",
-    "tnb_lanczos_work_bytes", "tnb_lanczos_step",
+    "tnb_lanczos_work_bytes", "tnb_lanczos_step", "tnb_file_to_device",
 )
 
 # kernel families of the kernel timer (TNB_KF_* in include/tnb.h)
@@ -87,6 +87,7 @@ def _declare(lib):
         "tnb_bs_execute_batched": ([_i64, _i64, _p, _p, _p, _p], ctypes.c_int),
         "tnb_bs_plan_pairs": ([_i64, _i64, _pi32, _pi64, _p], ctypes.c_int),
         "tnb_copy2d_batched": ([_p, _p, _i64, _p, _p], ctypes.c_int),
+        "tnb_file_to_device": ([ctypes.c_int, _i64, _i64, _p, _p, _i64, ctypes.c_int, _p], ctypes.c_int),
         "tnb_lanczos_work_bytes": ([ctypes.c_int, _i64], _i64),
         "tnb_lanczos_step": ([ctypes.c_int, _p, _i64, ctypes.c_int, _p, _i64, _p, _p, _p, _p, _p], ctypes.c_int),
         "tnb_svd_jacobi_batched": ([ctypes.c_int, ctypes.c_int, _p, ctypes.c_int, ctypes.c_double,
@@ -365,6 +366,13 @@ def lanczos_step(dtype, q_ptr, ldq, r, w_ptr, n, q_next_ptr, alpha_ptr, beta_ptr
     """tnb_lanczos_step: reorthogonalise w against r basis rows, alpha / beta to device memory."""
     check(lib().tnb_lanczos_step(dtype, q_ptr, ldq, r, w_ptr, n, q_next_ptr, alpha_ptr, beta_ptr, work_ptr, stream),
           "lanczos_step")
+
+
+def file_to_device(fd, offset, nbytes, pinned_ptr, dst_ptr, chunk, nthreads, stream):
+    """tnb_file_to_device: pooled pread of a file range into pinned memory, each piece copied
+    to the device as it lands (returns once every copy is queued on `stream`)."""
+    check(lib().tnb_file_to_device(int(fd), int(offset), int(nbytes), pinned_ptr, dst_ptr, int(chunk), int(nthreads),
+                                   stream), "file_to_device")
 
 
 def copy2d_batched(src_ptr, dst_ptr, segs, stream):
