@@ -33,6 +33,7 @@
 #include <array>
 #include <map>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -286,14 +287,18 @@ __global__ void __launch_bounds__(1024) bs_pair_kernel(const BsMeta m) {
 }
 
 // ---- grouped stream-K GEMM --------------------------------------------------
-template <bool CPLX, int MODE>
+template <bool CPLX, int MODE, int SHAPE = 0>
 struct BsCfg {
   // 64x64 tiles suit the sector sizes; at this tile size the gather rate, not the DMMA
   // rate, is the limit, so two producer warpgroups feed the 16 math warps (measured: 4 math
   // warps of 32x32 tiles at 1 or 2 CTAs per SM 15% slower; 8 math warps of 32x16 tiles + one
   // producer warpgroup at 2 CTAs per SM 10% slower)
   // (r02, 64 x C4 batch: NPROD 64 / 128 and BK 32 with 4-5 stages measured no better)
-  static constexpr int BM = 64, BN = 64, BK = CPLX ? 8 : 16, WM = 4, WN = 4, STAGES = 8, NPROD = 256;
+  // SHAPE 1 (float64 batches): 64 x 128 tiles, 6 stages -- per stage twice the DMMA work for
+  // the same ring hand-off, which pays once every CTA walks thousands of k-iterations (64 x C4:
+  // 1.116 -> 1.021 ms) but not for one contraction (C4: 33.3 -> 35.4 us)
+  static constexpr int BM = 64, BN = SHAPE ? 128 : 64, BK = CPLX ? 8 : 16, WM = 4, WN = 4, STAGES = SHAPE ? 6 : 8,
+                       NPROD = 256;
   using Core = SKCore<CPLX, MODE, BM, BN, BK, WM, WN, STAGES, NPROD>;
 };
 
@@ -319,10 +324,10 @@ struct BsSK {
 constexpr int kTraceW = 64;
 
 
-template <bool CPLX, int MODE, bool AMF, bool BNF, int NP>
-__global__ void __launch_bounds__(BsCfg<CPLX, MODE>::Core::NT, 1)
+template <bool CPLX, int MODE, bool AMF, bool BNF, int NP, int SHAPE>
+__global__ void __launch_bounds__(BsCfg<CPLX, MODE, SHAPE>::Core::NT, 1)
     bs_sk_kernel(const __grid_constant__ BsMeta m, const __grid_constant__ PtrTable<NP> pt, const BsSK sk) {
-  using Cfg = BsCfg<CPLX, MODE>;
+  using Cfg = BsCfg<CPLX, MODE, SHAPE>;
   using Core = typename Cfg::Core;
   using Base = typename Core::Base;
   using T = typename Core::T;
@@ -721,9 +726,19 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 // structure -- metadata uploaded, pairing table computed by the pairing kernel --
 // and cached on the device; every later call with the same structure launches
 // just the grouped GEMM with its data pointers as a kernel parameter.
+// A structure's build inputs, kept so a batched execute can derive the wide-tile twin plan.
+struct PlanInputs {
+  int dtype, na, nb, nout, rank_a, rank_b, nc;
+  std::vector<int32_t> a_qn, a_perm, b_qn, b_perm, a_axes, b_axes, out_qn;
+  std::vector<int64_t> a_shape, b_shape, out_shape;
+};
+
 struct Plan {
   unsigned char* dblob = nullptr;
   BsMeta meta;
+  int shape = 0;       // BsCfg tile shape (1: 64 x 128 tiles, float64 batches)
+  int64_t twin = 0;    // plan id of the shape-1 twin (0: not built)
+  std::shared_ptr<PlanInputs> in;  // shape-0, unmasked plans
   int64_t npairs = 0;
   size_t o_optr = 0, o_pairs = 0;
   int dtype = 0;
@@ -770,10 +785,10 @@ PlanCache& cur_cache() {
 constexpr int kMaxBsCtas = 2048;  // flags region: one int per persistent CTA
 constexpr size_t kBsPartialOff = 16384;
 
-template <bool CPLX, int MODE, bool AMF, bool BNF, int NP>
+template <bool CPLX, int MODE, bool AMF, bool BNF, int NP, int SHAPE>
 int launch_bs_one(const BsMeta& meta, const void* const* hp, int nptr, BsSK sk, bool capturing, cudaStream_t st) {
-  using Core = typename BsCfg<CPLX, MODE>::Core;
-  auto kern = bs_sk_kernel<CPLX, MODE, AMF, BNF, NP>;
+  using Core = typename BsCfg<CPLX, MODE, SHAPE>::Core;
+  auto kern = bs_sk_kernel<CPLX, MODE, AMF, BNF, NP, SHAPE>;
   PtrTable<NP> pt;
   for (int x = 0; x < nptr && x < NP; ++x) pt.p[x] = hp[x];
   const size_t smem = al16(Core::kSmem) + (size_t)meta.sched_smem;
@@ -850,7 +865,7 @@ int launch_bs_one(const BsMeta& meta, const void* const* hp, int nptr, BsSK sk, 
 }
 
 // Caller holds g_cache.mu.
-template <bool CPLX, int MODE>
+template <bool CPLX, int MODE, int SH>
 int launch_bs(const Plan& plan, const BsMeta& meta, const void* const* hp, int nptr, cudaStream_t st) {
   if (meta.ntiles == 0) return TNB_OK;
   const bool capturing = tnb::capturing(st);
@@ -861,17 +876,17 @@ int launch_bs(const Plan& plan, const BsMeta& meta, const void* const* hp, int n
   const bool small = meta.ptrs || nptr <= kInlinePtrsSmall;
   constexpr int S = kInlinePtrsSmall, L = kInlinePtrs;
   if (plan.amf && plan.bnf)
-    rc = small ? launch_bs_one<CPLX, MODE, true, true, S>(meta, hp, nptr, sk, capturing, st)
-               : launch_bs_one<CPLX, MODE, true, true, L>(meta, hp, nptr, sk, capturing, st);
+    rc = small ? launch_bs_one<CPLX, MODE, true, true, S, SH>(meta, hp, nptr, sk, capturing, st)
+               : launch_bs_one<CPLX, MODE, true, true, L, SH>(meta, hp, nptr, sk, capturing, st);
   else if (plan.amf)
-    rc = small ? launch_bs_one<CPLX, MODE, true, false, S>(meta, hp, nptr, sk, capturing, st)
-               : launch_bs_one<CPLX, MODE, true, false, L>(meta, hp, nptr, sk, capturing, st);
+    rc = small ? launch_bs_one<CPLX, MODE, true, false, S, SH>(meta, hp, nptr, sk, capturing, st)
+               : launch_bs_one<CPLX, MODE, true, false, L, SH>(meta, hp, nptr, sk, capturing, st);
   else if (plan.bnf)
-    rc = small ? launch_bs_one<CPLX, MODE, false, true, S>(meta, hp, nptr, sk, capturing, st)
-               : launch_bs_one<CPLX, MODE, false, true, L>(meta, hp, nptr, sk, capturing, st);
+    rc = small ? launch_bs_one<CPLX, MODE, false, true, S, SH>(meta, hp, nptr, sk, capturing, st)
+               : launch_bs_one<CPLX, MODE, false, true, L, SH>(meta, hp, nptr, sk, capturing, st);
   else
-    rc = small ? launch_bs_one<CPLX, MODE, false, false, S>(meta, hp, nptr, sk, capturing, st)
-               : launch_bs_one<CPLX, MODE, false, false, L>(meta, hp, nptr, sk, capturing, st);
+    rc = small ? launch_bs_one<CPLX, MODE, false, false, S, SH>(meta, hp, nptr, sk, capturing, st)
+               : launch_bs_one<CPLX, MODE, false, false, L, SH>(meta, hp, nptr, sk, capturing, st);
   if (rc) return rc;
   if (!capturing) {
     if (!C.ws_ev) TNB_CUDA_CHECK(cudaEventCreateWithFlags(&C.ws_ev, cudaEventDisableTiming));
@@ -897,7 +912,7 @@ int bs_plan_locked(int dtype, int na, int nb, int nout, int rank_a, int rank_b, 
                    const int64_t* a_shape, const int32_t* a_perm, const int32_t* b_qn, const int64_t* b_shape,
                    const int32_t* b_perm, int nc, const int32_t* a_axes, const int32_t* b_axes,
                    const int32_t* out_qn, const int64_t* out_shape, int64_t npanels, const uint8_t* panel_mask,
-                   cudaStream_t st, int64_t* plan_id, int64_t* npairs) {
+                   cudaStream_t st, int64_t* plan_id, int64_t* npairs, int shape = 0) {
   int rc = require_device();
   if (rc) return rc;
   if (dtype != TNB_F64 && dtype != TNB_C128)
@@ -910,7 +925,7 @@ int bs_plan_locked(int dtype, int na, int nb, int nout, int rank_a, int rank_b, 
   // ---- plan lookup (structure only)
   std::string key;
   {
-    int32_t hdr[8] = {dtype, na, nb, nout, rank_a, rank_b, nc, 0};
+    int32_t hdr[8] = {dtype, na, nb, nout, rank_a, rank_b, nc, shape};
     append(key, hdr, 8);
     append(key, a_qn, (size_t)na * rank_a);
     append(key, a_shape, (size_t)na * rank_a);
@@ -944,6 +959,22 @@ int bs_plan_locked(int dtype, int na, int nb, int nout, int rank_a, int rank_b, 
     }
     Plan plan;
     plan.dtype = dtype;
+    plan.shape = shape;
+    if (shape == 0 && !(panel_mask && npanels > 0)) {
+      auto in = std::make_shared<PlanInputs>();
+      *in = {dtype, na, nb, nout, rank_a, rank_b, nc, {}, {}, {}, {}, {}, {}, {}, {}, {}, {}};
+      in->a_qn.assign(a_qn, a_qn + (size_t)na * rank_a);
+      in->a_shape.assign(a_shape, a_shape + (size_t)na * rank_a);
+      in->a_perm.assign(a_perm, a_perm + rank_a);
+      in->b_qn.assign(b_qn, b_qn + (size_t)nb * rank_b);
+      in->b_shape.assign(b_shape, b_shape + (size_t)nb * rank_b);
+      in->b_perm.assign(b_perm, b_perm + rank_b);
+      in->a_axes.assign(a_axes, a_axes + nc);
+      in->b_axes.assign(b_axes, b_axes + nc);
+      in->out_qn.assign(out_qn, out_qn + (size_t)nout * ro);
+      in->out_shape.assign(out_shape, out_shape + (size_t)nout * ro);
+      plan.in = in;
+    }
     BsMeta& meta = plan.meta;
     memset(&meta, 0, sizeof(meta));
     meta.nbatch = 1;
@@ -1018,7 +1049,8 @@ int bs_plan_locked(int dtype, int na, int nb, int nout, int rank_a, int rank_b, 
       plan.amf = wa[1] >= wa[0];
       plan.bnf = wb[1] >= wb[0];
     }
-    const int BM = 64, BN = 64;
+    const int BM = BsCfg<false, 0>::BM, BN = shape ? BsCfg<false, 0, 1>::BN : BsCfg<false, 0>::BN;
+    static_assert(BsCfg<false, 0, 1>::BM == BsCfg<false, 0>::BM, "panels are BM-row based in every shape");
     meta.bk = (dtype == TNB_C128) ? BsCfg<true, 0>::BK : BsCfg<false, 0>::BK;
     std::vector<int32_t> oM(nout), oN(nout);
     std::vector<TileRef> tiles;
@@ -1227,8 +1259,9 @@ int bs_execute_locked(Plan& plan, const void* const* a_ptrs, const void* const* 
   if (tnb::capturing(st)) plan.captured = true;
   const void* const* hp = meta.ptrs ? nullptr : hv.data();
   const int nin = meta.ptrs ? 0 : (int)nptr;
-  if (plan.dtype == TNB_F64) rc = launch_bs<false, 0>(plan, meta, hp, nin, st);
-  else rc = launch_bs<true, 0>(plan, meta, hp, nin, st);
+  if (plan.dtype == TNB_F64) rc = plan.shape ? launch_bs<false, 0, 1>(plan, meta, hp, nin, st)
+                                             : launch_bs<false, 0, 0>(plan, meta, hp, nin, st);
+  else rc = launch_bs<true, 0, 0>(plan, meta, hp, nin, st);
   if (meta.ptrs) cudaFreeAsync(const_cast<void*>(static_cast<const void*>(meta.ptrs)), st);
   if (rc != TNB_OK) return rc;
   return TNB_OK;
@@ -1309,6 +1342,27 @@ extern "C" int tnb_bs_execute_batched(int64_t plan_id, int64_t nbatch, const voi
     return fail(TNB_EINVAL, "bs_execute_batched: NULL pointer table");
   if (plan->meta.mask && nbatch != 1)
     return fail(TNB_EUNSUP, "bs_execute_batched: panel-masked plans run one contraction per launch");
+  // float64 batches of >= kWideBatch contractions run on the structure's 64 x 128-tile twin
+  // (built once from the stored inputs; same pairs and per-tile pair order)
+  constexpr int64_t kWideBatch = 4;
+  static const bool no_wide = getenv("TNB_BS_NO_WIDE") != nullptr;  // dev A/B switch
+  if (!no_wide && nbatch >= kWideBatch && plan->dtype == TNB_F64 && plan->shape == 0 && plan->in) {
+    Plan* twin = plan->twin ? plan_of(plan->twin) : nullptr;
+    if (!twin) {
+      std::shared_ptr<PlanInputs> in = plan->in;  // (plan may move: the cache vector grows)
+      int64_t tid = 0;
+      rc = bs_plan_locked(in->dtype, in->na, in->nb, in->nout, in->rank_a, in->rank_b, in->a_qn.data(),
+                          in->a_shape.data(), in->a_perm.data(), in->b_qn.data(), in->b_shape.data(),
+                          in->b_perm.data(), in->nc, in->a_axes.data(), in->b_axes.data(), in->out_qn.data(),
+                          in->out_shape.data(), 0, nullptr, (cudaStream_t)stream, &tid, nullptr, 1);
+      if (rc) return rc;
+      plan = plan_of(plan_id);
+      if (!plan) return fail(TNB_EINVAL, "bs_execute_batched: stale or unknown plan id (plan cache was flushed)");
+      plan->twin = tid;
+      twin = plan_of(tid);
+    }
+    if (twin) return bs_execute_locked(*twin, a_ptrs, b_ptrs, out_ptrs, (cudaStream_t)stream, nbatch);
+  }
   return bs_execute_locked(*plan, a_ptrs, b_ptrs, out_ptrs, (cudaStream_t)stream, nbatch);
 }
 
