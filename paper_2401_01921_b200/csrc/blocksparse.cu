@@ -1348,7 +1348,9 @@ extern "C" int tnb_bs_execute_batched(int64_t plan_id, int64_t nbatch, const voi
   static const bool no_wide = getenv("TNB_BS_NO_WIDE") != nullptr;  // dev A/B switch
   if (!no_wide && nbatch >= kWideBatch && plan->dtype == TNB_F64 && plan->shape == 0 && plan->in) {
     Plan* twin = plan->twin ? plan_of(plan->twin) : nullptr;
-    if (!twin) {
+    // (not built under stream capture: its pairing kernel would only run when the graph does,
+    // leaving the twin's schedule unwritten for eager calls; the parent plan serves instead)
+    if (!twin && !tnb::capturing((cudaStream_t)stream)) {
       std::shared_ptr<PlanInputs> in = plan->in;  // (plan may move: the cache vector grows)
       int64_t tid = 0;
       rc = bs_plan_locked(in->dtype, in->na, in->nb, in->nout, in->rank_a, in->rank_b, in->a_qn.data(),
