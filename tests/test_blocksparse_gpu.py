@@ -494,3 +494,36 @@ def test_graph_owned_workspaces_are_released(cuda):
     torch.cuda.empty_cache()
     free1, _ = torch.cuda.mem_get_info()
     assert free0 - free1 < (24 << 20), (free0, free1)  # 12 x 4.9 MB would leak ~59 MB
+
+
+def test_batched_twin_plan_capture_before_eager(cuda):
+    """A float64 batch (>= 4 contractions) first seen INSIDE a stream capture runs on the
+    parent plan (the 64 x 128-tile twin is only built eagerly); later eager calls build and
+    use the twin. Graph replays and eager calls agree with the pairwise results."""
+    import torch
+    from paper_2401_01921_b200 import graphs
+    u1 = Symmetry.u1()
+    V = Bond(btype=IN, sectors=[(-2, 70), (-1, 130), (0, 150), (1, 120), (2, 60)], syms=[u1])
+    P = Bond(btype=IN, sectors=[(1, 1), (-1, 1)], syms=[u1])
+
+    def mk(seed):
+        A = UniTensor([V, P, V.redirect()], labels=["vl", "p", "vr"])
+        E = UniTensor([V, P.redirect(), V.redirect()], labels=["vr", "p", "x"])
+        trandom.normal_(A, seed=seed)
+        trandom.normal_(E, seed=seed + 1)
+        return A, E
+
+    pairs = [mk(1300 + 2 * i) for i in range(6)]
+    want = [[b.numpy() for b in tnb.contract_pair(a, e).get_blocks_()] for a, e in pairs]
+    holder = {}
+    g = graphs.capture(lambda: holder.__setitem__("outs", tnb.contract_batched(pairs)), warmup=0)
+    g.replay()
+    torch.cuda.synchronize()
+    eager = tnb.contract_batched(pairs)  # builds the twin
+    eager2 = tnb.contract_batched(pairs)
+    g.replay()
+    torch.cuda.synchronize()
+    for outs in (holder["outs"], eager, eager2):
+        for k, o in enumerate(outs):
+            for gb, w in zip(o.get_blocks_(), want[k]):
+                assert np.linalg.norm(gb.numpy() - w) <= 1e-13 * max(np.linalg.norm(w), 1e-300)
