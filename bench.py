@@ -260,6 +260,12 @@ def time_steps(fn, steps, flush, dist):
     dist.barrier()
     torch.cuda.synchronize()
     with _NoGC():
+        # two untimed steps first: the GPU would otherwise enter the first timed step from the
+        # idle gap of the barrier / synchronize above (measured: +0.14 ms on the headline's
+        # first step, +0.9-1.6 ms on C3 c128's, every later step level)
+        for _ in range(2):
+            flush()
+            fn()
         for _ in range(steps):
             flush()
             e0, e1 = _events()
@@ -269,7 +275,12 @@ def time_steps(fn, steps, flush, dist):
             pairs.append((e0, e1))
         torch.cuda.synchronize()
     dist.barrier()
-    return dist.max(sum(a.elapsed_time(b) for a, b in pairs))
+    each = [a.elapsed_time(b) for a, b in pairs]
+    _LAST_STEPS[:] = each
+    return dist.max(sum(each))
+
+
+_LAST_STEPS = []  # per-step ms of the last time_steps call (detail only)
 
 
 def time_region(fn, dist):
@@ -416,11 +427,16 @@ def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, graph=False,
     for _ in range(warmup):
         net.launch()
     l0 = tnb._lib.launch_count()
+    m0 = torch.cuda.memory_stats()
     ms = time_steps(net.launch, steps, flush, dist)
+    m1 = torch.cuda.memory_stats()
+    each = [round(x, 4) for x in _LAST_STEPS]
+    allocs = {k: m1.get(k, 0) - m0.get(k, 0) for k in ("num_device_alloc", "num_device_free", "num_alloc_retries")}
     launches = (tnb._lib.launch_count() - l0) // max(steps, 1)
     assert net.get_order() == order
     out = net.launch().numpy()
-    res = {"ms_per_step": ms / steps, "flop_per_step": flop, "order": order, "launches_per_step": launches,
+    res = {"ms_per_step": ms / steps, "ms_each_step": each, "allocator": allocs, "flop_per_step": flop, "order": order,
+           "launches_per_step": launches,
            "gflops": dist.sum(flop) / (ms / steps) / 1e6, "out": out, "inp": inp}
     if graph:
         cn = net.compile()
@@ -1158,6 +1174,11 @@ def main():
             except Exception as e:  # noqa: BLE001
                 wl[name] = {"error": f"{type(e).__name__}: {e}"[:200]}
             torch.cuda.empty_cache()
+            if cpu_on:
+                # a workload's CPU leg leaves 16 OpenBLAS threads spinning for ~0.1 s: they
+                # would steal the next workload's host thread (measured: C3 c128 6.09 vs 5.09
+                # ms per step right after C1's CPU leg)
+                time.sleep(0.5)
         line["workloads"] = wl
         line["workloads_keys"] = "v, frac=roofline, cpu=oracle port, e2e=host buffers, par=rel.err vs oracle, ms/step"
     if cpu_on:
