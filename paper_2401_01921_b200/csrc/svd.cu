@@ -510,6 +510,8 @@ constexpr int kBlkSmemMax = 220 * 1024;
 // 17 warps: a block pair of h <= 34 rows has <= 17 row pairs per inner round, one warp each
 // (with 16, warp 0 took two and set every round's latency)
 constexpr int kBlkWarps = 17;
+constexpr int kSortSweeps = 3;  // sweeps that start by sorting the rows by norm (1 / 3 / all: 13 / 13 / 13
+                                // sweeps at 516^2, 12 / 11 / 12 at 256^2)
 
 __host__ __device__ __forceinline__ int blk_hp(int bsz) { return ((2 * bsz + 7) / 8) * 8; }
 // shared-memory row stride of the staged rows (elements): >= n, 4 mod 16 doubles (two
@@ -663,6 +665,38 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kBlkWarps * 3
     for (sweep = 1; sweep <= max_sweeps; ++sweep) {
       int* cnt = t.counter + (sweep & 1);
       if (tid == 0) s_rot = 0;
+      if (sweep <= kSortSweeps) {
+        // rows sorted by decreasing norm at the start of the first sweeps (de Rijk's ordering:
+        // 516 x 516 14 -> 13 sweeps, 256 x 256 12 -> 11): B, Q rows -> the output buffers
+        // (scratch until the finalize) in rank order, then back
+        T* __restrict__ VHs = static_cast<T*>(t.vh);
+        T* __restrict__ Us = static_cast<T*>(t.u);
+        for (int i = gw; i < m; i += NW) {
+          double x2 = 0.0;
+          for (int j = lane; j < n; j += 32) x2 += S::abs2(ldcg(B + (int64_t)i * ldb + j));
+          x2 = warp_sum(x2);
+          if (lane == 0) __stcg(t.norm + i, x2);
+        }
+        cluster_sync_all();
+        for (int i = gw; i < m; i += NW) {
+          const double si = __ldcg(t.norm + i);
+          int rank = 0;
+          for (int k = lane; k < m; k += 32) {
+            const double sk = __ldcg(t.norm + k);
+            rank += (sk > si || (sk == si && k < i)) ? 1 : 0;
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+          for (int j = lane; j < n; j += 32) stcg(VHs + (int64_t)rank * n + j, ldcg(B + (int64_t)i * ldb + j));
+          for (int j = lane; j < m; j += 32) stcg(Us + (int64_t)rank * m + j, ldcg(Q + (int64_t)i * ldq + j));
+        }
+        cluster_sync_all();
+        for (int i = gw; i < m; i += NW) {
+          for (int j = lane; j < n; j += 32) stcg(B + (int64_t)i * ldb + j, ldcg(VHs + (int64_t)i * n + j));
+          for (int j = lane; j < m; j += 32) stcg(Q + (int64_t)i * ldq + j, ldcg(Us + (int64_t)i * m + j));
+        }
+        cluster_sync_all();
+      }
       for (int r = 0; r < nb - 1; ++r) {
         for (int pi_ = crank; pi_ < nb / 2; pi_ += kCluster) {
           int I, J;
