@@ -252,7 +252,10 @@ class _NoGC:
             gc.enable()
 
 
-def time_steps(fn, steps, flush, dist):
+WARM_UNTIMED = 2  # untimed steps time_steps runs first (the kernel timer sees them too)
+
+
+def time_steps(fn, steps, flush, dist, warm=WARM_UNTIMED):
     """Device time of `steps` calls of fn, each bracketed by its own events; L2 flushed
     (untimed) before every call; barrier + synchronize around the region; max over ranks."""
     import torch
@@ -263,7 +266,7 @@ def time_steps(fn, steps, flush, dist):
         # two untimed steps first: the GPU would otherwise enter the first timed step from the
         # idle gap of the barrier / synchronize above (measured: +0.14 ms on the headline's
         # first step, +0.9-1.6 ms on C3 c128's, every later step level)
-        for _ in range(2):
+        for _ in range(warm):
             flush()
             fn()
         for _ in range(steps):
@@ -456,8 +459,9 @@ def gpu_lawr(tnb, chi, dtype, steps, warmup, flush, dist, e2e=True, graph=False,
     (n_g, ms_g, fl_g), (n_s, ms_s, _) = ktimer(tnb, lambda: time_steps(net.launch, steps, flush, dist),
                                                tnb._lib.KF_GEMM, tnb._lib.KF_GEMM_SKINNY)
     ach = fl_g / (dist.max(ms_g) / 1e3) / 1e12 if n_g else 0.0
-    res["steps_ms"] = {"gemm": round(ms_g / steps, 4), "skinny_T1W": round(ms_s / steps, 4),
-                       "gemm_launches_per_step": n_g / steps, "gemm_share_of_step": round(ms_g / ms, 4)}
+    ks = steps + WARM_UNTIMED  # steps the kernel timer saw
+    res["steps_ms"] = {"gemm": round(ms_g / ks, 4), "skinny_T1W": round(ms_s / ks, 4),
+                       "gemm_launches_per_step": n_g / ks, "gemm_share_of_step": round((ms_g / ks) / (ms / steps), 4)}
     res["roofline"] = roofline_tensor(ach, "gemm_sk_kernel (stream-K DMMA.8x8x4), steps A.L + T2.R",
                                       traffic_per_launch("gemm_sk_kernel", dtype))
     res["roofline_how"] = ("achieved = algorithmic flop of the GEMM launches / their summed CUDA-event durations on "
@@ -677,7 +681,7 @@ def gpu_c4_batch(tnb, n_total, steps, warmup, flush, dist):
         step()
     ms = time_steps(step, steps, flush, dist) / steps
     ((n_k, ms_k, _),) = ktimer(tnb, lambda: time_steps(step, steps, flush, dist), tnb._lib.KF_BS_GEMM)
-    kms = dist.max(ms_k / max(steps, 1))
+    kms = dist.max(ms_k / max(n_k, 1))  # (one grouped launch per step)
     res = {"ms_per_step": ms, "instances": n_total, "per_rank": len(mine),
            "gflops": 2 * C4_MACS * n_total / ms / 1e6, "api": "contract_batched (tnb_bs_execute_batched)",
            "bs_gemm_kernel_ms": kms,
@@ -715,8 +719,8 @@ def gpu_peps(tnb, n_sites, chi, D, d, steps, warmup, flush, dist):
             vals.copy_(mine_buf[:n_sites])
     for _ in range(max(1, warmup)):
         step()
-    ms = time_steps(step, steps, flush, dist) / steps
-    ((n_g, ms_g, fl_g),) = ktimer(tnb, lambda: time_steps(step, 1, flush, dist), tnb._lib.KF_GEMM)
+    ms = time_steps(step, steps, flush, dist, warm=0) / steps  # (0.5 s steps: warm-up above suffices)
+    ((n_g, ms_g, fl_g),) = ktimer(tnb, lambda: time_steps(step, 1, flush, dist, warm=0), tnb._lib.KF_GEMM)
     ach = fl_g / (dist.max(ms_g) / 1e3) / 1e12 if n_g else 0.0
     return {"ms_per_step": ms, "sites": n_sites, "per_rank": len(mine), "order": tnb.render_order(tree),
             "flop_per_site": flop, "gflops": flop * n_sites / ms / 1e6,
