@@ -352,11 +352,15 @@ __global__ void __launch_bounds__(WARPS * 32) narrow_slab_kernel(const typename 
   const uint32_t span_bytes = (uint32_t)(ROWS * s.kin * ES);
   auto issue = [&](int64_t pn, int b) {  // lane 0 only
     const T* src = A + group_offset(d.rowA, (uint32_t)(pn * ROWS));
+    TNB_DCHECK(group_offset(d.rowA, (uint32_t)(pn * ROWS)) + ROWS * s.kin <= d.a_elems, "narrow_slab panel row range");
     const uint32_t dst = smem_u32(wbase + b * panel);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&bar[b])),
                  "r"(span_bytes * (uint32_t)s.kout)
                  : "memory");
-    for (int j = 0; j < s.kout; ++j) detail::bulk_load(dst + j * span_bytes, src + s.so[j], span_bytes, &bar[b]);
+    for (int j = 0; j < s.kout; ++j) {
+      TNB_DCHECK(src + s.so[j] - A >= 0 && src + s.so[j] - A + ROWS * s.kin <= d.a_elems, "narrow_slab span");
+      detail::bulk_load(dst + j * span_bytes, src + s.so[j], span_bytes, &bar[b]);
+    }
   };
   const int64_t first = (int64_t)blockIdx.x * WARPS + warp;
   if (lane == 0)

@@ -612,6 +612,7 @@ __device__ void blk_stage(typename Sc<CPLX>::T* __restrict__ W, int ldw, const t
   const int cpr = ncols / EPC;        // chunks per row (ncols is even for float64)
   for (int x = tid; x < h * cpr; x += blockDim.x) {
     const int i = x / cpr, c = x - i * cpr;
+    TNB_DCHECK(i < hp && c * EPC + EPC <= ldw, "svd blk_stage range");
     const T* g = src + (int64_t)rows[i] * ld + c * EPC;
     const uint32_t d = (uint32_t)__cvta_generic_to_shared(W + i * ldw + c * EPC);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(g));
