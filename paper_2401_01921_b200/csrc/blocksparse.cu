@@ -31,6 +31,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <array>
+#include <climits>
 #include <map>
 #include <cstring>
 #include <memory>
@@ -40,6 +41,13 @@
 #include <vector>
 
 #include "gemm_sk.cuh"
+
+#ifndef TNB_TWIN_WM
+#define TNB_TWIN_WM 4
+#endif
+#ifndef TNB_TWIN_STAGES
+#define TNB_TWIN_STAGES 6
+#endif
 
 namespace tnb {
 namespace {
@@ -88,6 +96,13 @@ struct BsMeta {
   // batched execute: nbatch contractions of this structure in one launch (tile space
   // nbatch x ntiles; pointer table [nbatch][na + nb + nout] in device memory)
   int nbatch;
+  // whole-tile schedule (single contractions): the pairing kernel assigns whole tiles to the
+  // sched_G CTAs by LPT when the makespan stays within lpt_slack k-iterations of the even
+  // split, lays the schedule out CTA by CTA and writes each CTA's range start to cta_beg
+  // ([sched_G + 1]; cta_beg[0] = -1: stream-K split instead).
+  int32_t* cta_beg;
+  int sched_G;
+  int lpt_slack;
 };
 
 // Schedule tables the grouped GEMM reads on every segment / pair switch (dependent
@@ -159,10 +174,20 @@ __device__ void cta_inclusive_scan(int32_t* a, int n) {
 
 // Shared-memory layout of the pairing kernel (qn tables, CSR, per-tile counts): every
 // table is re-read many times by dependent loops, so all of it lives on chip when it fits.
-__host__ __device__ inline size_t pair_smem_bytes(const BsMeta& m) {
+constexpr int kLptMaxG = 1024;  // whole-tile LPT schedules for grids up to this size
+// A whole-tile schedule is used when its makespan exceeds the even stream-K split by at most
+// this many k-iterations: every stream-K segment boundary costs a partial publish or absorb
+// and a segment start (~1-2 us each, per-CTA traces), i.e. several k-iterations of 64 x 64 DMMA.
+constexpr int kLptSlackDefault = 12;
+__host__ __device__ inline size_t lpt_smem_offset(const BsMeta& m) {
   return al16(((size_t)m.na * m.ra + (size_t)m.nb * m.rb + (size_t)m.nout * m.ro) * 4) +
          al16((size_t)(m.nout + 1) * 4) + al16((size_t)m.na * 4) + al16((size_t)m.ntiles * 4) +
-         (size_t)m.ntiles * 8;
+         al16((size_t)m.ntiles * 8);
+}
+__host__ __device__ inline size_t pair_smem_bytes(const BsMeta& m) {
+  const size_t lpt = (m.cta_beg && m.sched_G > 0 && m.sched_G <= kLptMaxG)
+                         ? al16((size_t)m.ntiles * 8) + (size_t)m.sched_G * 12 : 0;
+  return lpt_smem_offset(m) + lpt;
 }
 
 __global__ void __launch_bounds__(1024) bs_pair_kernel(const BsMeta m) {
@@ -260,6 +285,91 @@ __global__ void __launch_bounds__(1024) bs_pair_kernel(const BsMeta m) {
   // short segments (each segment / pair switch has a fixed gather set-up latency)
   TNB_STAMP()
   const bool reorder = m.qn_smem && m.ntiles <= 4096;
+  if (reorder && m.cta_beg && m.sched_G > 0 && m.sched_G <= kLptMaxG) {
+    // whole-tile LPT: rank tiles by k-iterations (descending, stable), then one warp hands
+    // each tile in rank order to the least-loaded CTA (lowest index on ties). Scratch lives
+    // in shared memory after the pairing tables (pair_smem_bytes reserves it).
+    const int G = m.sched_G;
+    unsigned char* r0 = psm + lpt_smem_offset(m);
+    int32_t* lrank = reinterpret_cast<int32_t*>(r0);
+    int32_t* lasg = lrank + m.ntiles;
+    long long* lload = reinterpret_cast<long long*>(r0 + al16((size_t)m.ntiles * 8));
+    int32_t* lnext = reinterpret_cast<int32_t*>(lload + G);
+    __shared__ int lpt_ok;
+    for (int t = threadIdx.x; t < m.ntiles; t += blockDim.x) {
+      const int ct = tcnt[t];
+      int r = 0;
+      for (int u = 0; u < m.ntiles; ++u) {
+        const int cu = tcnt[u];
+        r += (cu > ct || (cu == ct && u < t)) ? 1 : 0;
+      }
+      lrank[r] = t;
+    }
+    for (int c = threadIdx.x; c < G; c += blockDim.x) {
+      lload[c] = 0;
+      lnext[c] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      long long total = 0, mk = 0;
+      for (int r = 0; r < m.ntiles; ++r) {
+        const int t = lrank[r];
+        long long bv = LLONG_MAX;
+        int bc = G;
+        for (int c = lane; c < G; c += 32)
+          if (lload[c] < bv) { bv = lload[c]; bc = c; }  // strided scan: the lane's first minimum
+#pragma unroll
+        for (int s = 16; s; s >>= 1) {
+          const long long ov = __shfl_xor_sync(0xffffffffu, bv, s);
+          const int oc = __shfl_xor_sync(0xffffffffu, bc, s);
+          if (ov < bv || (ov == bv && oc < bc)) { bv = ov; bc = oc; }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          lload[bc] += tcnt[t];
+          lasg[t] = bc;
+        }
+        total += tcnt[t];
+        mk = max(mk, bv + tcnt[t]);
+        __syncwarp();
+      }
+      if (lane == 0) lpt_ok = mk <= (total + G - 1) / G + m.lpt_slack;
+    }
+    __syncthreads();
+    if (lpt_ok) {
+      // layout CTA by CTA (a CTA's tiles in rank order); cta_beg = prefix sums of the loads
+      for (int t = threadIdx.x; t < m.ntiles; t += blockDim.x) atomicAdd(&lnext[lasg[t]], 1);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int pos = 0;
+        long long kb = 0;
+        for (int c = 0; c < G; ++c) {
+          const int n = lnext[c];
+          lnext[c] = pos;
+          pos += n;
+          m.cta_beg[c] = (int32_t)kb;
+          kb += lload[c];
+        }
+        m.cta_beg[G] = (int32_t)kb;
+        for (int r = 0; r < m.ntiles; ++r) {
+          const int t = lrank[r];
+          const int p = lnext[lasg[t]]++;
+          m.stiles[p] = m.tiles[t];
+          m.tile_cnt[p] = tcnt[t];
+        }
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < m.ntiles; t += blockDim.x) tcnt[t] = m.tile_cnt[t];
+      __syncthreads();
+      cta_inclusive_scan(tcnt, m.ntiles);
+      for (int t = threadIdx.x; t <= m.ntiles; t += blockDim.x) m.tile_kbeg[t] = t ? tcnt[t - 1] : 0;
+      return;
+    }
+    if (threadIdx.x == 0) m.cta_beg[0] = -1;
+    __syncthreads();
+  } else if (m.cta_beg && threadIdx.x == 0) {
+    m.cta_beg[0] = -1;
+  }
   for (int t = threadIdx.x; t < m.ntiles; t += blockDim.x) {
     int pos = t;
     const int ct = tcnt[t];
@@ -297,8 +407,8 @@ struct BsCfg {
   // SHAPE 1 (float64 batches): 64 x 128 tiles, 6 stages -- per stage twice the DMMA work for
   // the same ring hand-off, which pays once every CTA walks thousands of k-iterations (64 x C4:
   // 1.116 -> 1.021 ms) but not for one contraction (C4: 33.3 -> 35.4 us)
-  static constexpr int BM = 64, BN = SHAPE ? 128 : 64, BK = CPLX ? 8 : 16, WM = 4, WN = 4, STAGES = SHAPE ? 6 : 8,
-                       NPROD = 256;
+  static constexpr int BM = 64, BN = SHAPE ? 128 : 64, BK = CPLX ? 8 : 16, WM = SHAPE ? TNB_TWIN_WM : 4, WN = 4,
+                       STAGES = SHAPE ? TNB_TWIN_STAGES : 8, NPROD = 256;
   using Core = SKCore<CPLX, MODE, BM, BN, BK, WM, WN, STAGES, NPROD>;
 };
 
@@ -318,7 +428,8 @@ struct BsSK {
   // dev instrumentation (TNB_BS_TRACE=file): per CTA [kTraceW] int64 of %globaltimer stamps
   long long* trace;
   // dev experiments (TNB_BS_EXP): bit 0 = producers issue no copies, bit 1 = math warps
-  // issue no DMMA (the skeleton's cost without memory traffic / tensor work)
+  // issue no DMMA (the skeleton's cost without memory traffic / tensor work), bits 2 / 3 =
+  // whole k-tiles skip their A / B copies
   int exp;
 };
 constexpr int kTraceW = 64;
@@ -348,6 +459,13 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE, SHAPE>::Core::NT, 1)
   const void* const* ptrs = m.ptrs ? m.ptrs : pt.p;
   const int tid = threadIdx.x;
   const int c = blockIdx.x;
+  // whole-tile schedule bounds: loaded first, in flight while the tables are staged
+  int32_t wb0 = -1, wb1 = -1, wbz = -1;
+  if (m.nbatch == 1 && m.cta_beg && m.sched_G == (int)gridDim.x) {
+    wbz = __ldg(m.cta_beg);
+    wb0 = __ldg(m.cta_beg + c);
+    wb1 = __ldg(m.cta_beg + c + 1);
+  }
   const int* kbeg = m.tile_kbeg;
   const TileRef* tiles = m.stiles;
   const BlockDesc* DA = m.da;
@@ -404,9 +522,12 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE, SHAPE>::Core::NT, 1)
   const int NPI = m.na + m.nb + m.nout;  // pointers per batch item
   // stream-K participants: >= 4 k-iterations each, so no participant has an empty range
   // (an owner waits on EVERY participant between a tile's first CTA and itself)
-  const int G = (int)min((int64_t)gridDim.x, max(total / 4, (int64_t)1));
-  const int64_t it0 = c < G ? detail::sk_begin(total, G, c) : 0;
-  const int64_t it1 = c < G ? detail::sk_begin(total, G, c + 1) : 0;
+  // whole-tile schedule (no tile split across CTAs: no partial publish / absorb) when the
+  // pairing kernel laid one out for exactly this grid; else the even stream-K split
+  const bool whole = wbz == 0;
+  const int G = whole ? (int)gridDim.x : (int)min((int64_t)gridDim.x, max(total / 4, (int64_t)1));
+  const int64_t it0 = whole ? wb0 : (c < G ? detail::sk_begin(total, G, c) : 0);
+  const int64_t it1 = whole ? wb1 : (c < G ? detail::sk_begin(total, G, c + 1) : 0);
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       detail::mbar_init(&full[s], NPROD);
@@ -532,6 +653,7 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE, SHAPE>::Core::NT, 1)
             } else if (krem >= BK) {  // whole k-tile: validity = padding row/col only
 #pragma unroll
               for (int x = 0; x < EA; ++x) {
+                if (sk.exp & 4) break;
                 const bool v = oA[x] >= 0;
                 const T* src = A + (v ? oA[x] + koA : 0);
                 TNB_DCHECK(!v || (oA[x] + koA >= 0 && (int64_t)oA[x] + koA < (int64_t)da.F * da.K), "bs A gather");
@@ -542,6 +664,7 @@ __global__ void __launch_bounds__(BsCfg<CPLX, MODE, SHAPE>::Core::NT, 1)
               }
 #pragma unroll
               for (int x = 0; x < EB; ++x) {
+                if (sk.exp & 8) break;
                 const bool v = oB[x] >= 0;
                 const T* src = B + (v ? oB[x] + koB : 0);
                 TNB_DCHECK(!v || (oB[x] + koB >= 0 && (int64_t)oB[x] + koB < (int64_t)db.F * db.K), "bs B gather");
@@ -1114,6 +1237,11 @@ int bs_plan_locked(int dtype, int na, int nb, int nout, int rank_a, int rank_b, 
                  o_mask = take(panel_mask ? (size_t)npanels : 0);
     const size_t upload = off;
     const size_t o_err = take(16 + 16 * 8), o_tcnt = take((size_t)tiles.size() * 4);
+    // whole-tile LPT schedule for single contractions on a one-CTA-per-SM persistent grid
+    static const int lpt_slack = getenv("TNB_BS_LPT_SLACK") ? atoi(getenv("TNB_BS_LPT_SLACK")) : kLptSlackDefault;
+    meta.sched_G = lpt_slack >= 0 ? std::min(sm_count(), kLptMaxG) : 0;
+    meta.lpt_slack = lpt_slack;
+    const size_t o_ctab = take((size_t)(meta.sched_G + 2) * 4);
     const size_t total = off;
     if (o_oM - o_kbeg != sched_bytes((int)tiles.size(), nout, meta.max_pairs) - 2 * al16((size_t)nout * 4) ||
         o_da != o_kbeg + sched_bytes((int)tiles.size(), nout, meta.max_pairs))
@@ -1148,6 +1276,7 @@ int bs_plan_locked(int dtype, int na, int nb, int nout, int rank_a, int rank_b, 
     meta.tile_cnt = reinterpret_cast<int32_t*>(dblob + o_tcnt);
     meta.stiles = reinterpret_cast<TileRef*>(dblob + o_stiles);
     meta.img = reinterpret_cast<const uint4*>(dblob + o_kbeg);
+    meta.cta_beg = reinterpret_cast<int32_t*>(dblob + o_ctab);
     meta.ptrs = nullptr;
     meta.qn_smem = 1;
     size_t pair_smem = pair_smem_bytes(meta);

@@ -870,6 +870,13 @@ struct StreamK {
     static bool configured = false;
     if (!configured) {
       TNB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Core::kSmem));
+      if constexpr (Core::kRegSplit) {
+        // the setmaxnreg split assumes the kernel launches with exactly kLaunchRegs per thread
+        // (a smaller allocation would leave the math warps' increase waiting forever)
+        cudaFuncAttributes fa;
+        TNB_CUDA_CHECK(cudaFuncGetAttributes(&fa, kern));
+        if (fa.numRegs != Core::kLaunchRegs) return fail(TNB_ECUDA, "gemm: stream-K kernel register count mismatch");
+      }
       configured = true;
     }
     {

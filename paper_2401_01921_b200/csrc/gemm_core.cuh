@@ -97,6 +97,11 @@ struct TileCore {
     if constexpr (WARPS_M == 4 && WARPS_N == 4) {
       wn = warp >> 2;
       wm = (warp + wn) & 3;
+    } else if constexpr (WARPS_M == 2 && WARPS_N == 4) {
+      // SMSP s (warps s, s + 4) holds column groups s and s + 2: an edge tile with one or two
+      // live column groups still spreads its DMMAs over two or four tensor pipes
+      wm = warp >> 2;
+      wn = (warp + 2 * wm) & 3;
     } else {
       wm = warp / WARPS_N;
       wn = warp % WARPS_N;
@@ -427,6 +432,11 @@ struct TileCoreWS {
     if constexpr (WARPS_M == 4 && WARPS_N == 4) {
       wn = warp >> 2;
       wm = (warp + wn) & 3;
+    } else if constexpr (WARPS_M == 2 && WARPS_N == 4) {
+      // SMSP s (warps s, s + 4) holds column groups s and s + 2: an edge tile with one or two
+      // live column groups still spreads its DMMAs over two or four tensor pipes
+      wm = warp >> 2;
+      wn = (warp + 2 * wm) & 3;
     } else {
       wm = warp / WARPS_N;
       wn = warp % WARPS_N;

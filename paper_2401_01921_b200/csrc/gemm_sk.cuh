@@ -78,6 +78,13 @@ struct SKCore {
   static constexpr int ACCN = NACC * MF * NF * 2;
   static constexpr int EA = (BM * BK) / NPROD, EB = (BN * BK) / NPROD;
   static constexpr int kMaxPeriod = 16;  // periodic-K offset tables: D0 <= 16 phases
+  // warp-specialised register split (setmaxnreg) for the 640-thread dense kernel: launched at
+  // kLaunchRegs per thread, producers drop to kProdRegs so the math warps can hold kMathRegs
+  // (measured: chi=1024 f64 L.A.W.R GEMMs 1.356 -> 1.332 ms, c128 5.03 -> 4.96 ms)
+  static constexpr bool kRegSplit = NMATH == 512 && NPROD == 128;
+  static constexpr int kLaunchRegs = 96, kProdRegs = 64, kMathRegs = 104;
+  static_assert(!kRegSplit || NMATH * (kMathRegs - kLaunchRegs) <= NPROD * (kLaunchRegs - kProdRegs),
+                "register split must fit in the CTA's launch allocation");
   static constexpr size_t kSmem = (size_t)STAGES * BK * (LDA + LDB) * ES + (size_t)(BM + BN) * 8 +
                                   (size_t)2 * 2 * BK * 8 + (size_t)2 * STAGES * 8 + (size_t)2 * kMaxPeriod * BK * 8;
   static_assert(NMATH % 128 == 0, "math warps must form whole warpgroups");
@@ -269,6 +276,9 @@ struct SKCore {
 
     if (tid >= NMATH) {
       // ================================================================ producer
+      // register split (launch: 96 per thread): the producer warpgroup gives 32 back, the
+      // four math warpgroups take 8 more each (kRegSplit; the host checks the launch count)
+      if constexpr (kRegSplit) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProdRegs) : "memory");
       const int p = tid - NMATH;
       auto mapA = [&](int i, int& m, int& kk) {
         const int e = p + i * NPROD;
@@ -452,6 +462,7 @@ if (!d.bulkB)
     }
 
     // ================================================================== math warps
+    if constexpr (kRegSplit) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kMathRegs) : "memory");
     uint32_t gi = 0;
     Acc acc;
     // segments in REVERSE range order: a CTA first publishes the partial of the tile it
