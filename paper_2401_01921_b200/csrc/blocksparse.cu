@@ -48,6 +48,12 @@
 #ifndef TNB_TWIN_STAGES
 #define TNB_TWIN_STAGES 6
 #endif
+#ifndef TNB_BS_NPROD0
+#define TNB_BS_NPROD0 256
+#endif
+#ifndef TNB_BS_NPROD1
+#define TNB_BS_NPROD1 128  // twin plan: one producer warpgroup (64 x C4: 1.031 -> 1.016 ms)
+#endif
 
 namespace tnb {
 namespace {
@@ -408,7 +414,7 @@ struct BsCfg {
   // the same ring hand-off, which pays once every CTA walks thousands of k-iterations (64 x C4:
   // 1.116 -> 1.021 ms) but not for one contraction (C4: 33.3 -> 35.4 us)
   static constexpr int BM = 64, BN = SHAPE ? 128 : 64, BK = CPLX ? 8 : 16, WM = SHAPE ? TNB_TWIN_WM : 4, WN = 4,
-                       STAGES = SHAPE ? TNB_TWIN_STAGES : 8, NPROD = 256;
+                       STAGES = SHAPE ? TNB_TWIN_STAGES : 8, NPROD = SHAPE ? TNB_BS_NPROD1 : TNB_BS_NPROD0;
   using Core = SKCore<CPLX, MODE, BM, BN, BK, WM, WN, STAGES, NPROD>;
 };
 
