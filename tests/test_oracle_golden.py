@@ -95,7 +95,7 @@ def test_network_golden():
         slots.append((n.strip(), [t.strip() for t in rhs.split(",")]))
     arrays = {n: np.ones(c["shapes"][n]) for n, _ in slots}
     got, _ = oracle.launch(slots, "", arrays, order=c["net"][-1].split(":", 1)[1].strip())
-    assert float(got) == c["scalar"] == 4096.0
+    assert np.asarray(got).item() == c["scalar"] == 4096.0
     c = meta["cases"][4]
     slots = []
     for line in c["net"][:-1]:
@@ -104,7 +104,7 @@ def test_network_golden():
     arrays = {n: z[f"n3_{n}"] for n in c["names"]}
     got, tree = oracle.launch(slots, "", arrays)
     assert oracle.render_order(tree) == c["order"]
-    assert abs(float(got) - c["scalar"]) <= 1e-10 * max(1.0, abs(c["scalar"]))
+    assert abs(np.asarray(got).item() - c["scalar"]) <= 1e-10 * max(1.0, abs(c["scalar"]))
 
 
 def test_c4_structure_golden():
