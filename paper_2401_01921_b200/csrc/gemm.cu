@@ -1231,6 +1231,17 @@ int contract_dense_device(const void* a, int dta, int ra, const int64_t* sa, con
   if (!(d.colB.n > 0 && d.colB.stride[d.colB.n - 1] == 1 && d.colB.dim[d.colB.n - 1] >= 4) && d.kB.n > 0 &&
       d.kB.stride[d.kB.n - 1] == 1)
     d.b_nfast = 0;
+  static const bool dbg = getenv("TNB_DEBUG_GEMM") != nullptr;  // dev: the GEMM view of a contraction
+  if (dbg) {
+    fprintf(stderr, "[tnb gemm] M=%lld N=%lld K=%lld kaff=%d a_mfast=%d b_nfast=%d\n", (long long)M, (long long)N,
+            (long long)K, d.kaff.ok, d.a_mfast, d.b_nfast);
+    auto pr = [](const char* nm, const Group& g) {
+      fprintf(stderr, "  %s:", nm);
+      for (int q = 0; q < g.n; ++q) fprintf(stderr, " (%d,%lld)", g.dim[q], (long long)g.stride[q]);
+      fprintf(stderr, "\n");
+    };
+    pr("rowA", d.rowA), pr("kA", d.kA), pr("kB", d.kB), pr("colB", d.colB);
+  }
   if (!cplx) rc = dispatch<false, 0>(a, b, out, d, st);
   else if (cplx_mode == TNB_CPLX_3M) rc = dispatch<true, 1>(a, b, out, d, st);
   else rc = dispatch<true, 0>(a, b, out, d, st);
