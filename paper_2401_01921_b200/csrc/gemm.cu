@@ -1051,6 +1051,13 @@ int dispatch(const void* A, const void* B, void* C, GemmDesc& d, cudaStream_t st
       }
       return StreamK<false, 0, 64, 64, 16, 4, 4, 4>::run(A, B, C, d, st);
     }
+    // a few output tiles over a very long, irregular K (the PEPS closing step: M = 128, N = 64,
+    // K = 4.2M, both operands K-gathered): every operand element is read once, in short strided
+    // runs -- 32-wide k-tiles double each run per stage
+    static const bool no_bk32 = getenv("TNB_NO_BK32") != nullptr;  // dev A/B switch
+    if (!no_bk32 && d.kaff.ok == 0 && aN64 <= a128 && pad(d.M, 128) * pad(d.N, 64) <= 4 * 128 * 64 &&
+        d.K >= (1 << 16))
+      return StreamK<false, 0, 128, 64, 32, 4, 4, 4>::run(A, B, C, d, st);
     if (aN64 < a128 && aN64 <= aM64) return StreamK<false, 0, 128, 64, 16, 4, 4, 4>::run(A, B, C, d, st);
     if (aM64 < a128) return StreamK<false, 0, 64, 128, 16, 4, 4, 4>::run(A, B, C, d, st);
     // (measured: BK = 32 / 3 stages 15% slower; 3, 5 and 6 stages of BK = 16 no faster than 4)
