@@ -299,3 +299,18 @@ def test_narrow_row_panel_path(cuda, dt):
             if wl[1] == "q":
                 want = want.transpose(0, 1, 3, 2)
             assert rel_fro(got.numpy(), want) <= 1e-13, ((p, vr, b, w), wl)
+
+
+def test_long_gathered_k_few_tiles_vs_oracle(cuda):
+    """The PEPS closing-step shape at reduced chi (M = 128, N = 64, K = 65536 over four
+    interleaved digits, the free s axis innermost in A): the 32-wide k-tile stream-K
+    instantiation (dispatch: few output tiles, irregular K >= 2^16) against the oracle."""
+    al = ["c0", "u", "c2", "r", "l", "dn", "s"]
+    bl = ["dn", "dn2", "c2", "c0", "l", "l2"]
+    dims = {"c0": 32, "u": 8, "c2": 32, "r": 8, "l": 8, "dn": 8, "s": 2, "dn2": 8, "l2": 8}
+    a = oracle.normal([dims[x] for x in al], seed=41)
+    b = oracle.normal([dims[x] for x in bl], seed=42)
+    got = contract(UniTensor(storage.from_numpy(a), labels=al), UniTensor(storage.from_numpy(b), labels=bl))
+    want, wl = oracle.contract_dense(a, al, b, bl)
+    assert got.labels == wl == ["u", "r", "s", "dn2", "l2"]
+    assert rel_fro(got.numpy(), want) <= 1e-12
