@@ -180,6 +180,19 @@ int tnb_contract_dense_ld(const void* a, int dtype_a, int rank_a,
                           int nc, const int32_t* a_axes, const int32_t* b_axes,
                           void* out, int64_t out_ld, int cplx_mode, void* stream);
 
+/* Same contraction writing the output in a chosen PHYSICAL axis order: out_order[p] is the
+ * logical output axis (a_free..., b_free...) stored at physical position p (row-major over
+ * the physical order); NULL = the logical order (tnb_contract_dense). The result is read
+ * back as a lazily permuted tensor. Network launches use it to lay an intermediate out
+ * K-major for the long-K contraction that consumes it (network.py:213-244 semantics are
+ * unchanged: only the storage order of an intermediate differs). */
+int tnb_contract_dense_out(const void* a, int dtype_a, int rank_a,
+                           const int64_t* shape_a, const int32_t* perm_a,
+                           const void* b, int dtype_b, int rank_b,
+                           const int64_t* shape_b, const int32_t* perm_b,
+                           int nc, const int32_t* a_axes, const int32_t* b_axes,
+                           void* out, const int32_t* out_order, int cplx_mode, void* stream);
+
 /* ---- a3: zero-flux block enumeration (unitensor.py:31-45), host only ------
  * Bonds are given as flattened charge tables:
  *   nbonds, nsyms; nsec[b]; btype[b] (+1 IN, -1 OUT);

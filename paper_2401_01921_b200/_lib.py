@@ -23,7 +23,7 @@ EXPORTS = (
     "tnb_zero_flux_blocks", "tnb_bs_contract", "tnb_bs_contract_masked", "tnb_optimal_order",
     "tnb_ktimer_enable", "tnb_ktimer_reset", "tnb_ktimer_read",
     "tnb_bs_plan", "tnb_bs_execute", "tnb_bs_execute_batched", "tnb_bs_plan_pairs", "tnb_copy2d_batched", "tnb_svd_jacobi_batched",
-    "tnb_lanczos_work_bytes", "tnb_lanczos_step", "tnb_file_to_device",
+    "tnb_lanczos_work_bytes", "tnb_lanczos_step", "tnb_file_to_device", "tnb_contract_dense_out",
 )
 
 # kernel families of the kernel timer (TNB_KF_* in include/tnb.h)
@@ -65,6 +65,9 @@ def _declare(lib):
         "tnb_contract_dense": ([_p, ctypes.c_int, ctypes.c_int, _pi64, _pi32,
                                 _p, ctypes.c_int, ctypes.c_int, _pi64, _pi32,
                                 ctypes.c_int, _pi32, _pi32, _p, ctypes.c_int, _p], ctypes.c_int),
+        "tnb_contract_dense_out": ([_p, ctypes.c_int, ctypes.c_int, _pi64, _pi32,
+                                    _p, ctypes.c_int, ctypes.c_int, _pi64, _pi32,
+                                    ctypes.c_int, _pi32, _pi32, _p, _pi32, ctypes.c_int, _p], ctypes.c_int),
         "tnb_contract_dense_ld": ([_p, ctypes.c_int, ctypes.c_int, _pi64, _pi32,
                                    _p, ctypes.c_int, ctypes.c_int, _pi64, _pi32,
                                    ctypes.c_int, _pi32, _pi32, _p, _i64, ctypes.c_int, _p], ctypes.c_int),
@@ -197,8 +200,11 @@ def dense_args(a_shape, a_perm, b_shape, b_perm, a_axes, b_axes):
     return arrs, [p for _, p in arrs]
 
 
+_ORDER_ARGS = {}  # marshalled output orders (tuple -> (array, pointer))
+
+
 def contract_dense(a_ptr, a_dt, a_shape, a_perm, b_ptr, b_dt, b_shape, b_perm,
-                   a_axes, b_axes, out_ptr, cplx_mode, stream, out_ld=0):
+                   a_axes, b_axes, out_ptr, cplx_mode, stream, out_ld=0, out_order=None):
     # the integer descriptor arrays of a contraction shape are marshalled once and reused
     # (a Network relaunched on same-shape operands re-marshals nothing)
     key = (tuple(a_shape), tuple(a_perm), tuple(b_shape), tuple(b_perm), tuple(a_axes), tuple(b_axes))
@@ -209,6 +215,15 @@ def contract_dense(a_ptr, a_dt, a_shape, a_perm, b_ptr, b_dt, b_shape, b_perm,
             _DENSE_ARGS.clear()
         _DENSE_ARGS[key] = args
     psa, ppa, psb, ppb, pxa, pxb = args[1]
+    if out_order is not None:
+        oo = _ORDER_ARGS.get(out_order)
+        if oo is None:
+            oo = _ORDER_ARGS[out_order] = _arr32(out_order)
+        check(lib().tnb_contract_dense_out(a_ptr, a_dt, len(a_shape), psa, ppa,
+                                           b_ptr, b_dt, len(b_shape), psb, ppb,
+                                           len(a_axes), pxa, pxb, out_ptr, oo[1], cplx_mode, stream),
+              "contract_dense_out")
+        return
     if out_ld:
         check(lib().tnb_contract_dense_ld(a_ptr, a_dt, len(a_shape), psa, ppa,
                                           b_ptr, b_dt, len(b_shape), psb, ppb,

@@ -134,8 +134,11 @@ def _result_dtype(da, db):
     return dt
 
 
-def contract_pair(a, b):
-    """Contract two UniTensors over all shared labels; output = a_free then b_free labels."""
+def contract_pair(a, b, out_order=None):
+    """Contract two UniTensors over all shared labels; output = a_free then b_free labels.
+    out_order (dense operands only): the PHYSICAL order of the output's axes (a tuple of
+    logical axis indices) -- the result is the same tensor, stored in that order and read
+    back as a lazy permute (Network launches lay intermediates out for their consumer)."""
     if not isinstance(a, UniTensor) or not isinstance(b, UniTensor):
         raise TypeError("contract expects UniTensors")
     if a.is_sym != b.is_sym:
@@ -146,23 +149,32 @@ def contract_pair(a, b):
             return out
     a_pos, b_pos, a_free, b_free, out_labels, out_bonds = _pair_layout(a, b)
     if not a.is_sym:
-        return _contract_dense(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds)
+        return _contract_dense(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds, out_order)
     return _contract_blocks(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds)
 
 
-def _contract_dense(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds):
+def _contract_dense(a, b, a_pos, b_pos, a_free, b_free, out_labels, out_bonds, out_order=None):
     A, B = a._blocks[0], b._blocks[0]
     dt = _result_dtype(A.dtype, B.dtype)
     out_shape = [A.shape[i] for i in a_free] + [B.shape[j] for j in b_free]
-    out = DenseTensor.empty(out_shape, dt)
     chunks = dense.pending_chunks(B)
     k0 = B.perm.index(0) if B.rank else -1  # logical axis stored outermost
+    if out_order is not None and (chunks or tuple(out_order) == tuple(range(len(out_shape)))):
+        out_order = None
+    if out_order is not None:
+        out_order = tuple(int(x) for x in out_order)
+        inv = [0] * len(out_order)
+        for p, x in enumerate(out_order):
+            inv[x] = p
+        out = DenseTensor.empty([out_shape[x] for x in out_order], dt).permute(*inv)
+    else:
+        out = DenseTensor.empty(out_shape, dt)
     if chunks and b_free and b_free[0] == k0 and A.dtype == B.dtype:
         _contract_dense_panels(A, B, a_pos, b_pos, b_free, out, chunks)
     else:
         _lib.contract_dense(A.data_ptr, dense.dtype_code(A.dtype), A.storage_shape, A.perm,
                             B.data_ptr, dense.dtype_code(B.dtype), B.storage_shape, B.perm,
-                            a_pos, b_pos, out.data_ptr, _CPLX_MODE, dense.stream_handle())
+                            a_pos, b_pos, out.data_ptr, _CPLX_MODE, dense.stream_handle(), out_order=out_order)
         if _RECORD is not None:
             _RECORD.append((A, B, tuple(a_pos), tuple(b_pos), tuple(out_shape), dt, out,
                             out_bonds, out_labels, len(a_free)))

@@ -1016,7 +1016,8 @@ int run_dot(const void* A, const void* B, void* C, const GemmDesc& d, cudaStream
 template <bool CPLX, int MODE>
 int dispatch(const void* A, const void* B, void* C, GemmDesc& d, cudaStream_t st) {
   // the memory-bound kernels write packed rows; a strided output (column panel) takes stream-K
-  const bool packed = d.out_ld == d.N;
+  // (an output index map is written by the stream-K epilogue only)
+  const bool packed = d.out_ld == d.N && !d.outmap;
   if (packed && (int64_t)d.M * d.N <= 16) return run_dot<CPLX>(A, B, C, d, st);
   // (N, K <= 10: the MPO step of L.A.W.R with D = 5, d = 2 -- registers sized to it)
   if (packed && d.N <= 10 && d.K <= 10 && d.M >= 4096) return run_narrow<CPLX, 10, 10>(A, B, C, d, st);
@@ -1042,7 +1043,7 @@ int dispatch(const void* A, const void* B, void* C, GemmDesc& d, cudaStream_t st
       // dropped: the reduce inside the GEMM, each of a tile's S co-resident CTAs summing 1/S
       // of its rows after a per-tile arrival counter -- 48 us: the CTAs of a tile wait for
       // the slowest.)
-      if (d.out_ld == d.N) {
+      if (packed) {
         // 64 x 64 tiles, 8 warps of 32 x 16 (C1 graph 28.8 us; 4 warps of 32 x 32: 30.8; 16
         // warps: 30.8; 32 x 32 tiles: 28.8; BK = 32: 39.0; 4 stages: 30.9)
         int split = 1;
@@ -1078,7 +1079,8 @@ __global__ void widen_kernel(const double* __restrict__ x, double2* __restrict__
 
 int contract_dense_device(const void* a, int dta, int ra, const int64_t* sa, const int32_t* pa, const void* b,
                           int dtb, int rb, const int64_t* sb, const int32_t* pb, int nc, const int32_t* aax,
-                          const int32_t* bax, void* out, int64_t out_ld, int cplx_mode, cudaStream_t st) {
+                          const int32_t* bax, void* out, int64_t out_ld, int cplx_mode, cudaStream_t st,
+                          const int32_t* out_order = nullptr) {
   if ((dta != TNB_F64 && dta != TNB_C128) || (dtb != TNB_F64 && dtb != TNB_C128))
     return fail(TNB_EUNSUP, "contract: only float64 and complex128 are supported on the GPU path (no CPU fallback)");
   Operand A, B;
@@ -1230,6 +1232,47 @@ int contract_dense_device(const void* a, int dta, int ra, const int64_t* sa, con
     return fail(TNB_EINVAL, "contract: out_ld must be 0 or >= the output column count");
   }
   d.out_ld = (int)(out_ld ? out_ld : N);
+  if (out_order) {
+    // physical order of the output axes (a's free axes, then b's, logically): element (m, n)
+    // lands at rowC(m) + colC(n), digits in the same enumeration order as rowA / colB
+    if (out_ld) {
+      if (tmp) cudaFreeAsync(tmp, st);
+      return fail(TNB_EINVAL, "contract: an output order needs a packed output");
+    }
+    std::vector<int64_t> odim;
+    int na = 0;
+    for (int k = 0; k < ra; ++k)
+      if (!acon[k]) odim.push_back(A.ldim[k]), ++na;
+    for (int k = 0; k < rb; ++k)
+      if (!bcon[k]) odim.push_back(B.ldim[k]);
+    const int ro = (int)odim.size();
+    std::vector<int64_t> pstride(ro, 0);
+    std::vector<int> seen(ro, 0);
+    bool ident = true;
+    int64_t acc_stride = 1;
+    for (int q = ro - 1; q >= 0; --q) {
+      const int x = out_order[q];
+      if (x < 0 || x >= ro || seen[x]) {
+        if (tmp) cudaFreeAsync(tmp, st);
+        return fail(TNB_EINVAL, "contract: out_order is not a permutation of the output axes");
+      }
+      seen[x] = 1;
+      ident = ident && x == q;
+      pstride[x] = acc_stride;
+      acc_stride *= odim[x];
+    }
+    if (!ident) {
+      std::vector<Digit> rc, cc;
+      for (int q = 0; q < ro; ++q) (q < na ? rc : cc).push_back({odim[q], pstride[q]});
+      int64_t Mc, Nc;
+      if (!build_group(merge_digits(rc), d.rowC, Mc) || !build_group(merge_digits(cc), d.colC, Nc) || Mc != M ||
+          Nc != N) {
+        if (tmp) cudaFreeAsync(tmp, st);
+        return fail(TNB_EUNSUP, "contract: output order has too many non-mergeable axes");
+      }
+      d.outmap = 1;
+    }
+  }
   d.a_mfast = 1;
   if (!(d.rowA.n > 0 && d.rowA.stride[d.rowA.n - 1] == 1 && d.rowA.dim[d.rowA.n - 1] >= 4) && d.kA.n > 0 &&
       d.kA.stride[d.kA.n - 1] == 1)
@@ -1269,6 +1312,20 @@ extern "C" int tnb_contract_dense(const void* a, int dtype_a, int rank_a, const 
     return tnb::fail(TNB_EINVAL, "contract: NULL argument");
   return tnb::contract_dense_device(a, dtype_a, rank_a, shape_a, perm_a, b, dtype_b, rank_b, shape_b, perm_b, nc,
                                     a_axes, b_axes, out, 0, cplx_mode, (cudaStream_t)stream);
+}
+
+extern "C" int tnb_contract_dense_out(const void* a, int dtype_a, int rank_a, const int64_t* shape_a,
+                                      const int32_t* perm_a, const void* b, int dtype_b, int rank_b,
+                                      const int64_t* shape_b, const int32_t* perm_b, int nc, const int32_t* a_axes,
+                                      const int32_t* b_axes, void* out, const int32_t* out_order, int cplx_mode,
+                                      void* stream) {
+  int rc = tnb::require_device();
+  if (rc) return rc;
+  if ((rank_a > 0 && (!shape_a || !perm_a)) || (rank_b > 0 && (!shape_b || !perm_b)) ||
+      (nc > 0 && (!a_axes || !b_axes)) || !a || !b || !out)
+    return tnb::fail(TNB_EINVAL, "contract: NULL argument");
+  return tnb::contract_dense_device(a, dtype_a, rank_a, shape_a, perm_a, b, dtype_b, rank_b, shape_b, perm_b, nc,
+                                    a_axes, b_axes, out, 0, cplx_mode, (cudaStream_t)stream, out_order);
 }
 
 extern "C" int tnb_contract_dense_ld(const void* a, int dtype_a, int rank_a, const int64_t* shape_a,

@@ -30,6 +30,10 @@ struct GemmDesc {
   int bulkA, bulkB;
   KAffine kaff;
   Group rowA, kA, kB, colB;
+  // outmap: the output is written at rowC(m) + colC(n) (the caller's physical order of the
+  // output axes, e.g. K-major for the step that consumes it) instead of m * out_ld + n
+  int outmap;
+  Group rowC, colC;
 };
 
 struct SKParams {
@@ -86,7 +90,8 @@ struct SKCore {
   static_assert(!kRegSplit || NMATH * (kMathRegs - kLaunchRegs) <= NPROD * (kLaunchRegs - kProdRegs),
                 "register split must fit in the CTA's launch allocation");
   static constexpr size_t kSmem = (size_t)STAGES * BK * (LDA + LDB) * ES + (size_t)(BM + BN) * 8 +
-                                  (size_t)2 * 2 * BK * 8 + (size_t)2 * STAGES * 8 + (size_t)2 * kMaxPeriod * BK * 8;
+                                  (size_t)2 * 2 * BK * 8 + (size_t)2 * STAGES * 8 + (size_t)2 * kMaxPeriod * BK * 8 +
+                                  (size_t)(BM + BN) * 8;  // output-map offsets of the tile (outmap)
   static_assert(NMATH % 128 == 0, "math warps must form whole warpgroups");
   static_assert((BM * BK) % NPROD == 0 && (BN * BK) % NPROD == 0, "tile/producer mismatch");
   using Acc = typename Base::Acc;
@@ -185,6 +190,59 @@ struct SKCore {
       __syncwarp();
       if (lane == 0) detail::mbar_arrive(&empty[s]);
     }
+  }
+
+  // Epilogue through the output index map (outmap): element (m, n) at rowC(m) + colC(n); a
+  // lane's column pair goes out as one 16-byte store when the two are adjacent and aligned.
+  // The tile's BM row and BN column offsets are computed once (one per math thread) into
+  // shared memory (tab: BM + BN entries) between two math-warp barriers.
+  __device__ static void store_mapped(T* __restrict__ C, const GemmDesc& d, int m0, int n0, const Acc& acc,
+                                      int64_t* tab) {
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    static_assert(BM + BN <= NMATH, "one output-map offset per math thread");
+    if (tid < BM) tab[tid] = m0 + tid < d.M ? group_offset(d.rowC, (uint32_t)(m0 + tid)) : -1;
+    else if (tid < BM + BN) tab[tid] = n0 + tid - BM < d.N ? group_offset(d.colC, (uint32_t)(n0 + tid - BM)) : -1;
+    detail::named_sync(3, NMATH);
+    int wm, wn;
+    Base::warp_mn(warp, wm, wn);
+    const int kq = lane & 3;
+    int64_t co[NF][2];
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+      const int n = wn * WTN + j * 8 + 2 * kq;
+      co[j][0] = tab[BM + n];
+      co[j][1] = tab[BM + n + 1];
+    }
+#pragma unroll
+    for (int i = 0; i < MF; ++i) {
+      const int64_t ro = tab[wm * WTM + i * 8 + (lane >> 2)];
+      if (ro < 0) continue;
+      T* row = C + ro;
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        T v0, v1;
+        if constexpr (!CPLX) {
+          v0 = acc[0][i][j][0];
+          v1 = acc[0][i][j][1];
+        } else if constexpr (MODE == 0) {
+          v0 = make_double2(acc[0][i][j][0], acc[1][i][j][0]);
+          v1 = make_double2(acc[0][i][j][1], acc[1][i][j][1]);
+        } else {
+          v0 = make_double2(acc[0][i][j][0] - acc[1][i][j][0], acc[2][i][j][0] - acc[0][i][j][0] - acc[1][i][j][0]);
+          v1 = make_double2(acc[0][i][j][1] - acc[1][i][j][1], acc[2][i][j][1] - acc[0][i][j][1] - acc[1][i][j][1]);
+        }
+        if constexpr (!CPLX) {
+          if (co[j][1] == co[j][0] + 1 && co[j][0] >= 0 && ((reinterpret_cast<uintptr_t>(row + co[j][0]) & 15) == 0)) {
+            *reinterpret_cast<double2*>(row + co[j][0]) = make_double2(v0, v1);
+            continue;
+          }
+        }
+        if (co[j][0] >= 0) row[co[j][0]] = v0;
+        if (co[j][1] >= 0) row[co[j][1]] = v1;
+      }
+    }
+    detail::named_sync(3, NMATH);  // the table is rewritten by the next mapped epilogue
   }
 
   // Stream-K fix-up. A CTA that computed the head/middle of a tile finished by a later
@@ -483,7 +541,8 @@ if (!d.bulkB)
         publish(sk.ws, sk.flags, c, acc);
       } else {
         if (kt0 > 0) absorb(sk.ws, sk.flags, detail::sk_cta_of(sk.total, sk.G, tile * (int64_t)KT), c, acc, sk.clear != 0);
-        Base::store(C, d.out_ld, m0, n0, d.M, d.N, acc);
+        if (d.outmap) store_mapped(C, d, m0, n0, acc, perB + kMaxPeriod * BK);
+        else Base::store(C, d.out_ld, m0, n0, d.M, d.N, acc);
       }
       e = sb;
     }

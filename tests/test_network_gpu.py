@@ -363,3 +363,51 @@ def test_repeated_small_launch_graph_replay_returns_fresh_results(cuda):
     t = UniTensor(storage.from_numpy(inp["A"]), labels=["A0", "A1", "A2"])
     net.put_tensor("A", t, t.labels)
     assert rel_fro(net.launch().numpy(), want) <= 1e-12
+
+
+@pytest.mark.parametrize("dt,mode", [(np.float64, 0), (np.complex128, 0), (np.complex128, 1)])
+def test_contract_pair_output_order_vs_oracle(cuda, dt, mode):
+    """contract_pair(out_order=...) (tnb_contract_dense_out): the same tensor, stored in the
+    requested physical axis order and read back as a lazy permute."""
+    from paper_2401_01921_b200 import contraction
+    rng = np.random.default_rng(7)
+    old = contraction._CPLX_MODE
+    contraction.set_complex_mode("3M" if mode else "4M")
+    try:
+        for _ in range(6):
+            al, bl = ["i", "k", "j", "m"], ["k", "n", "m", "p"]
+            dims = {x: int(rng.integers(2, 40)) for x in "ijkmnp"}
+            a = oracle.normal([dims[x] for x in al], dtype=dt, seed=int(rng.integers(1 << 30)))
+            b = oracle.normal([dims[x] for x in bl], dtype=dt, seed=int(rng.integers(1 << 30)))
+            oo = tuple(int(x) for x in rng.permutation(4))
+            got = contract_pair(UniTensor(storage.from_numpy(a), labels=al), UniTensor(storage.from_numpy(b), labels=bl),
+                                out_order=oo)
+            want, wl = oracle.contract_dense(a, al, b, bl)
+            assert got.labels == wl
+            blk = got.get_block_()
+            assert [blk.perm[x] for x in oo] == [0, 1, 2, 3]  # storage in the requested order
+            assert rel_fro(got.numpy(), want) <= 1e-12
+    finally:
+        contraction._CPLX_MODE = old
+
+
+def test_network_lays_out_long_k_intermediate(cuda):
+    """A network whose root contraction is a few-tile, long-K GEMM (the PEPS closing-step
+    shape at reduced size): the planner asks the right subtree for a K-major result; the
+    launch (and its recorded replay) still equals the oracle."""
+    from paper_2401_01921_b200 import blueprint
+    lines = ["X: c0, u, c2, r, l, dn, s", "Y1: dn, dn2, c2, t", "Y2: t, c0, l, l2", "TOUT: u, r, s, dn2, l2"]
+    dims = {"c0": 32, "u": 8, "c2": 32, "r": 8, "l": 8, "dn": 8, "s": 2, "dn2": 8, "l2": 8, "t": 16}
+    slots = oracle.net_slots(lines)
+    arrays = {n: oracle.normal([dims[x] for x in ls], seed=60 + i) for i, (n, ls) in enumerate(slots)}
+    net = Network(lines)
+    for n, ls in slots:
+        net.put_tensor(n, UniTensor(storage.from_numpy(arrays[n]), labels=ls))
+    net.set_order(contract_order="(X,(Y1,Y2))")
+    tensors = {n: UniTensor(storage.from_numpy(arrays[n]), labels=ls) for n, ls in slots}
+    lo, ro = blueprint._plan_children(("X", ("Y1", "Y2")), tensors)
+    assert lo is None and ro is not None  # K = (c0, c2, l, dn) outermost in the intermediate
+    want, _ = oracle.launch(slots, "u, r, s, dn2, l2", arrays, order="(X,(Y1,Y2))")
+    for _ in range(3):  # eager, recorded, replayed
+        got = net.launch()
+        assert rel_fro(got.numpy(), want) <= 1e-12

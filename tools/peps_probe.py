@@ -26,10 +26,10 @@ orig = contraction.contract_pair
 rec = []
 
 
-def timed(a, b):
+def timed(a, b, out_order=None):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    out = orig(a, b)
+    out = orig(a, b, out_order=out_order)
     e1.record()
     rec.append((a.labels, b.labels, a.shape, b.shape, out.shape, e0, e1))
     if len(a.shape) == 7:
