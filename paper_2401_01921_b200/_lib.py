@@ -218,6 +218,8 @@ def contract_dense(a_ptr, a_dt, a_shape, a_perm, b_ptr, b_dt, b_shape, b_perm,
     if out_order is not None:
         oo = _ORDER_ARGS.get(out_order)
         if oo is None:
+            if len(_ORDER_ARGS) >= 4096:
+                _ORDER_ARGS.clear()
             oo = _ORDER_ARGS[out_order] = _arr32(out_order)
         check(lib().tnb_contract_dense_out(a_ptr, a_dt, len(a_shape), psa, ppa,
                                            b_ptr, b_dt, len(b_shape), psb, ppb,
